@@ -1,0 +1,390 @@
+#!/usr/bin/env python
+"""Benchmark of the volume ray-casting hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+Metric: frames/s (and samples/s) rendering the torso phantom 512^3 int16 CT to
+1024^2 with tricubic sampling, 64^3/overlap-3 bricks with empty-space leaping,
+bone TF, headlight shading, ET 0.99.  One step = one
+frame: TF visibility (K2b) + the ray-cast kernel (K3) + stats; for N > 1 the
+frame is split sort-first into interleaved 16x8 cells across ranks and the
+packed cells are gathered to rank 0 over NCCL (strong scaling).
+
+``value`` is device time with the volume resident in HBM (CUDA events on the
+render stream, L2 flushed between steps by writing a 512 MiB buffer; max over
+ranks).  ``e2e`` is the same metric through the public host API
+``render(volume, camera, tf, settings)`` (LUT uploaded and the uint8 image +
+stats downloaded every step; the volume stays cached on the device as the
+reference's volume store caches it).  ``--impl reference`` times the CPU
+oracle (oracle/, a C restatement of the reference's numba march pinned to the
+reference's goldens) on all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: phantom dims, image size, settings overrides, tf
+    "c1": dict(dims=(64, 64, 64), size=128, tf="bone", projection="orthographic",
+               settings=dict(interpolation="tricubic"), desc="64^3 -> 128^2 orthographic, tricubic, monolithic"),
+    "c2": dict(dims=(256, 256, 256), size=512, tf="bone", projection="pinhole",
+               settings=dict(interpolation="tricubic"), desc="256^3 -> 512^2 pinhole, tricubic, monolithic"),
+    "c3": dict(dims=(512, 512, 512), size=1024, tf="bone", projection="pinhole",
+               settings=dict(interpolation="tricubic", use_blocks=True),
+               desc="512^3 -> 1024^2 pinhole, tricubic, bricks 64/3 + empty-space leaping"),
+    "c3soft": dict(dims=(512, 512, 512), size=1024, tf="soft-tissue", projection="pinhole",
+                   settings=dict(interpolation="tricubic", use_blocks=True),
+                   desc="C3 with the soft-tissue TF"),
+    "c3stress": dict(dims=(512, 512, 512), size=1024, tf="grayscale", projection="pinhole",
+                     settings=dict(interpolation="tricubic", lighting=False, early_termination_alpha=1.0),
+                     desc="C3-stress: monolithic, grayscale, ET off, no lighting (every step sampled)"),
+    "c4": dict(dims=(512, 512, 2048), size=2048, tf="bone", projection="pinhole",
+               settings=dict(interpolation="tricubic", use_blocks=True),
+               desc="512x512x2048 -> 2048^2, tricubic, bricks 64/3"),
+}
+
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def centered_camera(cls, extent, size, **kw):
+    """tests/conftest.py:34-43 of the reference: +x side at 2.2x the largest extent."""
+    cx, cy, cz = (0.5 * e for e in extent)
+    d = 2.2 * max(extent)
+    return cls(position=(cx + d, cy, cz), look_at=(cx, cy, cz), width=size, height=size, **kw)
+
+
+def make_camera(vr, cfg, extent):
+    if cfg["projection"] == "orthographic":
+        half = 0.5 * max(extent) + 1.0
+        return centered_camera(vr.OrthographicCamera, extent, cfg["size"], half_height_mm=half)
+    return centered_camera(vr.Camera, extent, cfg["size"])
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+def committed_traffic(config):
+    """dram bytes per launch of the ray-cast kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / f"ncu_raycast_{config}.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["dram_bytes_per_launch"])
+        except Exception:
+            return None
+    return None
+
+
+def dist_setup(n):
+    if n <= 1:
+        return 0, 1, 0
+    import torch
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def cpu_oracle_frame(values, spacing, camera, tf, settings, nthreads=0):
+    """One full frame through the CPU oracle (prep + march), like reference render()."""
+    from oracle import oracle as O
+
+    t0 = time.perf_counter()
+    r = O.render(values, spacing, camera, tf.values, tf.rgba, tf.domain, settings,
+                 projection=getattr(camera, "projection", "pinhole"),
+                 ortho_half_h=getattr(camera, "half_height_mm", None), nthreads=nthreads)
+    return time.perf_counter() - t0, r
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle port on all host threads, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import paper_2005_01442_b200 as vr
+    from oracle import oracle as O
+
+    cfg = CONFIGS[args.config]
+    values = O.phantom("torso", cfg["dims"]) if np.prod(cfg["dims"]) <= 64 ** 3 else None
+    if values is None:
+        # the product's device generator is bit-identical to the numpy phantom
+        # (pinned by tests/test_gpu_parity.py); use it when a GPU is present
+        try:
+            values = vr.device_phantom("torso", cfg["dims"]).download()
+        except Exception:
+            values = O.phantom("torso", cfg["dims"])
+    spacing = (1.0, 1.0, 1.0)
+    nz, ny, nx = values.shape
+    extent = ((nx - 1) * spacing[0], (ny - 1) * spacing[1], (nz - 1) * spacing[2])
+    camera = make_camera(vr, cfg, extent)
+    tf = vr.get_preset(cfg["tf"])
+    settings = vr.RenderSettings(**cfg["settings"])
+    threads = O.num_threads()
+    for _ in range(max(args.warmup, 0)):
+        cpu_oracle_frame(values, spacing, camera, tf, settings)
+    times, taken = [], 0
+    for _ in range(args.steps):
+        t, r = cpu_oracle_frame(values, spacing, camera, tf, settings)
+        times.append(t)
+        taken = r.samples_taken
+    total = sum(times)
+    fps = args.steps / total
+    line = {
+        "impl": "reference", "metric": "frames/sec", "value": fps, "unit": "frames/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "samples_per_sec": taken * fps,
+        "config": {"workload": args.config, "desc": cfg["desc"], "volume": list(cfg["dims"]),
+                   "image": [cfg["size"], cfg["size"]], "tf": cfg["tf"]},
+        "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} full {args.config} frames via oracle.render "
+                                   "(C restatement of _kernels.march, OpenMP over pixels, prep included)"},
+        "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2005_01442_b200 as vr
+    from paper_2005_01442_b200 import _lib
+    from paper_2005_01442_b200.distributed import gather_frame
+
+    rank, world, local = dist_setup(args.gpus)
+    if world == 1:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cfg = CONFIGS[args.config]
+    spacing = (1.0, 1.0, 1.0)
+    dvol = vr.device_phantom("torso", cfg["dims"], spacing, device=dev.index)
+    nx, ny, nz = dvol.dims
+    extent = ((nx - 1) * spacing[0], (ny - 1) * spacing[1], (nz - 1) * spacing[2])
+    camera = make_camera(vr, cfg, extent)
+    tf = vr.get_preset(cfg["tf"])
+    settings = vr.RenderSettings(**cfg["settings"])
+    rend = vr.Renderer(dvol, camera, tf, settings, device=dev.index,
+                       interleave=(world, rank) if world > 1 else None, time_kernel=True)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    W, H = camera.width, camera.height
+
+    def frame():
+        rend.render_async(stream)
+        if world > 1:
+            gather_frame(rend.pixels.reshape(-1, 4), W, H)
+
+    for _ in range(max(args.warmup, 3)):
+        frame()
+    torch.cuda.synchronize()
+    st = rend.stats()
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([st["samples_taken"], st["samples_skipped"], st["shaded"]], device=dev)
+        dist.all_reduce(t)
+        st["samples_taken"], st["samples_skipped"], st["shaded"] = (int(x) for x in t.tolist())
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    step_ms, kern_ms = [], []
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index if world == 1 else local) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)  # evict the previous frame's working set from L2 (outside the timed pair)
+            ev0.record(stream)
+            frame()
+            ev1.record(stream)
+            ev1.synchronize()
+            step_ms.append(ev0.elapsed_time(ev1))
+            kern_ms.append(rend.kernel_ms())
+        torch.cuda.synchronize()
+    total_ms = sum(step_ms)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([total_ms, sum(kern_ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, kern_total = t.tolist()
+    else:
+        kern_total = sum(kern_ms)
+    fps = args.steps / (total_ms / 1e3)
+    taken, shaded = st["samples_taken"], st["shaded"]
+    kern_s = kern_total / args.steps / 1e3
+    cubic = settings.interpolation == "tricubic"
+    b_sample = 128 if cubic else 16
+    b_grad = 768 if cubic else 96
+    # rank-local bytes for the local kernel: per-rank share of the frame
+    algo_bytes = (taken * b_sample + shaded * b_grad + W * H * 4) / world
+    achieved = algo_bytes / kern_s / 1e9
+    peak, peak_kind = measured_peak()
+    launches_per_step = (5 if settings.use_blocks else 2)
+
+    e2e = None
+    if not args.no_e2e and rank == 0 and world == 1:
+        host_vol = vr.ScalarVolume(dvol.download(), spacing, dvol.value_range)
+        host_vol._attach_device(dvol)
+        for _ in range(3):
+            vr.render(host_vol, camera, tf, settings)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            img = vr.render(host_vol, camera, tf, settings)
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": args.steps / e2e_s, "unit": "frames/s",
+               "h2d_bytes_per_step": 4096 * 4 * 8,
+               "d2h_bytes_per_step": int(img.pixels.nbytes) + 5 * 8,
+               "api": "paper_2005_01442_b200.render(ScalarVolume, Camera, TF, RenderSettings) -> ImageRGBA "
+                      "(C-ABI vr_render_to_host; volume cached on device)"}
+    elif rank == 0 and world > 1:
+        e2e = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+
+        values = dvol.download()
+        t, r = cpu_oracle_frame(values, spacing, camera, tf, settings)
+        cpu = {"value": 1.0 / t, "unit": "frames/s", "cores": O.num_threads(), "kind": "port",
+               "sample": f"one full {args.config} frame via oracle.render (C restatement of "
+                         "_kernels.march + block prep, OpenMP over pixels)",
+               "samples_taken": r.samples_taken}
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": "frames/sec", "value": fps, "unit": "frames/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (torso phantom generated on the device, bit-identical to the reference's)",
+        "samples_per_sec": taken * fps, "samples_taken": taken, "samples_skipped": st["samples_skipped"],
+        "shaded_samples": shaded,
+        "config": {"workload": args.config, "desc": cfg["desc"], "volume": list(cfg["dims"]),
+                   "image": [W, H], "tf": cfg["tf"], "parallelism": f"sort-first x{world}",
+                   "l2": "flushed between steps (512 MiB write)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_kind,
+                     "traffic": committed_traffic(args.config), "kernel": "raycast_kernel",
+                     "kernel_ms": kern_s * 1e3,
+                     "bytes_model": f"taken*{b_sample} + shaded*{b_grad} + W*H*4 per launch"},
+        "clocks": clocks.summary(),
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

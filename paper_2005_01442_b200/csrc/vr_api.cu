@@ -1,0 +1,664 @@
+// vr_api.cu -- the extern "C" boundary declared in include/voxelray_b200.h.
+//
+// Handles own device memory; every entry point selects the handle's device,
+// validates its arguments the way the reference's Python layer does, and
+// reports failures through a status code plus a thread-local message.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/voxelray_b200.h"
+#include "vr_prep.cuh"
+#include "vr_raycast.cuh"
+
+struct vr_volume {
+    int device;
+    int64_t nx, ny, nz;
+    double sx, sy, sz;
+    int16_t *data;
+    int32_t vmin, vmax;
+};
+
+struct vr_grid {
+    vr_volume *vol;
+    int64_t block_size, overlap;
+    vr::Layout L;
+    int nblocks;
+    int *vmin;  // device int32 [nblocks]
+    int *vmax;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+    return fail(VR_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define VR_CUDA(call)                                  \
+    do {                                               \
+        cudaError_t _e = (call);                       \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+vr::Layout monolithic_layout(const vr_volume *v) {
+    vr::Layout L;
+    L.n[0] = (int)v->nx;
+    L.n[1] = (int)v->ny;
+    L.n[2] = (int)v->nz;
+    L.nb[0] = L.nb[1] = L.nb[2] = 1;
+    int m = (int)std::max(v->nx, std::max(v->ny, v->nz));
+    L.bsize = m;  // render.py:393-399: one block, stride = max(n)
+    L.stride = m;
+    L.strided = (double)m;
+    L.inv_stride = 1.0 / (double)m;
+    L.py = v->nx;
+    L.pz = v->nx * v->ny;
+    return L;
+}
+
+// blocks.py:100-107
+int axis_count(int64_t n, int64_t bsize, int64_t stride) {
+    if (n <= bsize) return 1;
+    return (int)std::ceil((double)(n - bsize) / (double)stride) + 1;
+}
+
+// stream-ordered scratch that frees itself on the stream
+struct Scratch {
+    cudaStream_t s;
+    void *p = nullptr;
+    Scratch(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(size_t bytes) {
+        if (bytes == 0) bytes = 8;
+        return cudaMallocAsync(&p, bytes, s);
+    }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+void configure_pool(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;  // keep freed blocks cached across frames
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done[device] = true;
+}
+
+bool finite_positive(double v) { return std::isfinite(v) && v > 0.0; }
+
+// 16x8 cells of the rectangle; cells and pixels one render call produces
+void cell_counts(const vr_camera *c, int &cells_x, int &ncells, int &slots, long long &npix) {
+    cells_x = (c->tile_w + vr::kTileW - 1) / vr::kTileW;
+    int cells_y = (c->tile_h + vr::kTileH - 1) / vr::kTileH;
+    ncells = cells_x * cells_y;
+    if (c->interleave_n > 1) {
+        slots = (ncells + c->interleave_n - 1) / c->interleave_n;
+        npix = (long long)slots * vr::kTileW * vr::kTileH;
+    } else {
+        slots = ncells;
+        npix = (long long)c->tile_w * c->tile_h;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *vr_last_error(void) { return g_err.c_str(); }
+int vr_abi_version(void) { return VR_ABI_VERSION; }
+
+int vr_event_create(void **ev) {
+    if (!ev) return fail(VR_EINVALID, "null pointer");
+    VR_CUDA(cudaEventCreate((cudaEvent_t *)ev));
+    return VR_OK;
+}
+
+int vr_event_destroy(void *ev) {
+    if (ev) cudaEventDestroy((cudaEvent_t)ev);
+    return VR_OK;
+}
+
+int vr_event_elapsed_ms(void *start, void *stop, float *ms) {
+    if (!start || !stop || !ms) return fail(VR_EINVALID, "null pointer");
+    VR_CUDA(cudaEventSynchronize((cudaEvent_t)stop));
+    VR_CUDA(cudaEventElapsedTime(ms, (cudaEvent_t)start, (cudaEvent_t)stop));
+    return VR_OK;
+}
+
+int vr_interleave_size(const vr_camera *cam, int64_t *cells_per_rank, int64_t *pixels_per_rank) {
+    if (!cam) return fail(VR_EINVALID, "null camera");
+    int cx, nc, slots;
+    long long npix;
+    cell_counts(cam, cx, nc, slots, npix);
+    if (cells_per_rank) *cells_per_rank = slots;
+    if (pixels_per_rank) *pixels_per_rank = npix;
+    return VR_OK;
+}
+
+// ------------------------------------------------------------------ volumes
+
+static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
+    long long n = v->nx * v->ny * v->nz;
+    int *d_range = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
+    if (e == cudaSuccess) e = vr::launch_value_range(v->data, n, d_range, s);
+    int h[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, d_range, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (d_range) cudaFreeAsync(d_range, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        cudaFree(v->data);
+        delete v;
+        return cuda_fail(e, "volume value range");
+    }
+    v->vmin = h[0];
+    v->vmax = h[1];
+    *out = v;
+    return VR_OK;
+}
+
+static int check_volume_args(int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz) {
+    // volume.py:44-54
+    if (nx < 2 || ny < 2 || nz < 2)
+        return fail(VR_EINVALID, "every dimension must be >= 2");
+    if (nx > (1 << 30) || ny > (1 << 30) || nz > (1 << 30) || nx * ny * nz > (int64_t)1 << 40)
+        return fail(VR_EINVALID, "volume too large");
+    if (!finite_positive(sx) || !finite_positive(sy) || !finite_positive(sz))
+        return fail(VR_EINVALID, "spacing must be positive");
+    return VR_OK;
+}
+
+int vr_volume_create(int device, int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz,
+                     const int16_t *src, int src_on_device, void *stream, vr_volume **out) {
+    if (!out || !src) return fail(VR_EINVALID, "null pointer");
+    int rc = check_volume_args(nx, ny, nz, sx, sy, sz);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    configure_pool(device);
+    cudaStream_t s = (cudaStream_t)stream;
+    vr_volume *v = new vr_volume{device, nx, ny, nz, sx, sy, sz, nullptr, 0, 0};
+    size_t bytes = (size_t)(nx * ny * nz) * sizeof(int16_t);
+    cudaError_t e = cudaMalloc((void **)&v->data, bytes + 16);
+    if (e != cudaSuccess) {
+        delete v;
+        return fail(VR_ENOMEM, std::string("cudaMalloc volume: ") + cudaGetErrorString(e));
+    }
+    e = cudaMemcpyAsync(v->data, src, bytes, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+        cudaFree(v->data);
+        delete v;
+        return cuda_fail(e, "volume upload");
+    }
+    return finish_volume(v, s, out);
+}
+
+int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz,
+                      void *stream, vr_volume **out) {
+    if (!out) return fail(VR_EINVALID, "null pointer");
+    if (kind < 0 || kind > 2) return fail(VR_EINVALID, "unknown phantom kind");
+    if (nx < 8 || ny < 8 || nz < 8) return fail(VR_EINVALID, "phantom dims must be >= 8 per axis");
+    int rc = check_volume_args(nx, ny, nz, sx, sy, sz);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    configure_pool(device);
+    cudaStream_t s = (cudaStream_t)stream;
+    vr_volume *v = new vr_volume{device, nx, ny, nz, sx, sy, sz, nullptr, 0, 0};
+    size_t bytes = (size_t)(nx * ny * nz) * sizeof(int16_t);
+    cudaError_t e = cudaMalloc((void **)&v->data, bytes + 16);
+    if (e != cudaSuccess) {
+        delete v;
+        return fail(VR_ENOMEM, std::string("cudaMalloc phantom: ") + cudaGetErrorString(e));
+    }
+    e = vr::launch_phantom(kind, (int)nx, (int)ny, (int)nz, v->data, s);
+    if (e != cudaSuccess) {
+        cudaFree(v->data);
+        delete v;
+        return cuda_fail(e, "phantom kernel");
+    }
+    return finish_volume(v, s, out);
+}
+
+int vr_volume_destroy(vr_volume *v) {
+    if (!v) return VR_OK;
+    DeviceGuard g(v->device);
+    cudaFree(v->data);
+    delete v;
+    return VR_OK;
+}
+
+int vr_volume_info(const vr_volume *v, int64_t dims[3], double spacing[3], int32_t value_range[2], int *device) {
+    if (!v) return fail(VR_EINVALID, "null volume");
+    if (dims) {
+        dims[0] = v->nx;
+        dims[1] = v->ny;
+        dims[2] = v->nz;
+    }
+    if (spacing) {
+        spacing[0] = v->sx;
+        spacing[1] = v->sy;
+        spacing[2] = v->sz;
+    }
+    if (value_range) {
+        value_range[0] = v->vmin;
+        value_range[1] = v->vmax;
+    }
+    if (device) *device = v->device;
+    return VR_OK;
+}
+
+const int16_t *vr_volume_data(const vr_volume *v) { return v ? v->data : nullptr; }
+
+int vr_volume_download(const vr_volume *v, int16_t *dst, void *stream) {
+    if (!v || !dst) return fail(VR_EINVALID, "null pointer");
+    DeviceGuard g(v->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    VR_CUDA(cudaMemcpyAsync(dst, v->data, (size_t)(v->nx * v->ny * v->nz) * sizeof(int16_t),
+                            cudaMemcpyDeviceToHost, s));
+    VR_CUDA(cudaStreamSynchronize(s));
+    return VR_OK;
+}
+
+// ------------------------------------------------------------------- blocks
+
+int vr_grid_create(vr_volume *vol, int64_t block_size, int64_t overlap, void *stream, vr_grid **out) {
+    if (!vol || !out) return fail(VR_EINVALID, "null pointer");
+    // blocks.py:120-125
+    if (block_size < 8) return fail(VR_EBLOCKSPEC, "block_size must be >= 8, got " + std::to_string(block_size));
+    if (!(1 <= overlap && overlap < block_size))
+        return fail(VR_EBLOCKSPEC, "overlap must satisfy 1 <= overlap < block_size, got " + std::to_string(overlap));
+    DeviceGuard g(vol->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t stride = block_size - overlap;
+    vr_grid *gr = new vr_grid();
+    gr->vol = vol;
+    gr->block_size = block_size;
+    gr->overlap = overlap;
+    vr::Layout &L = gr->L;
+    L.n[0] = (int)vol->nx;
+    L.n[1] = (int)vol->ny;
+    L.n[2] = (int)vol->nz;
+    L.nb[0] = axis_count(vol->nx, block_size, stride);
+    L.nb[1] = axis_count(vol->ny, block_size, stride);
+    L.nb[2] = axis_count(vol->nz, block_size, stride);
+    L.bsize = (int)block_size;
+    L.stride = (int)stride;
+    L.strided = (double)stride;
+    L.inv_stride = 1.0 / (double)stride;
+    L.py = vol->nx;
+    L.pz = vol->nx * vol->ny;
+    gr->nblocks = L.nb[0] * L.nb[1] * L.nb[2];
+    cudaError_t e = cudaMalloc((void **)&gr->vmin, sizeof(int) * gr->nblocks);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&gr->vmax, sizeof(int) * gr->nblocks);
+    if (e == cudaSuccess) e = vr::launch_block_minmax(vol->data, L, gr->vmin, gr->vmax, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        cudaFree(gr->vmin);
+        cudaFree(gr->vmax);
+        delete gr;
+        return cuda_fail(e, "grid create");
+    }
+    *out = gr;
+    return VR_OK;
+}
+
+int vr_grid_destroy(vr_grid *gr) {
+    if (!gr) return VR_OK;
+    DeviceGuard g(gr->vol->device);
+    cudaFree(gr->vmin);
+    cudaFree(gr->vmax);
+    delete gr;
+    return VR_OK;
+}
+
+int vr_grid_shape(const vr_grid *gr, int64_t shape[3]) {
+    if (!gr || !shape) return fail(VR_EINVALID, "null pointer");
+    for (int k = 0; k < 3; ++k) shape[k] = gr->L.nb[k];
+    return VR_OK;
+}
+
+int vr_grid_minmax(const vr_grid *gr, int64_t *vmin, int64_t *vmax, void *stream) {
+    if (!gr || !vmin || !vmax) return fail(VR_EINVALID, "null pointer");
+    DeviceGuard g(gr->vol->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    std::vector<int> a(gr->nblocks), b(gr->nblocks);
+    VR_CUDA(cudaMemcpyAsync(a.data(), gr->vmin, sizeof(int) * gr->nblocks, cudaMemcpyDeviceToHost, s));
+    VR_CUDA(cudaMemcpyAsync(b.data(), gr->vmax, sizeof(int) * gr->nblocks, cudaMemcpyDeviceToHost, s));
+    VR_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < gr->nblocks; ++i) {
+        vmin[i] = a[i];
+        vmax[i] = b[i];
+    }
+    return VR_OK;
+}
+
+static int check_lut(int32_t nbins, double lo, double hi) {
+    if (nbins < 1 || nbins > 32768) return fail(VR_EINVALID, "LUT bins must be in [1, 32768]");
+    if (!(lo < hi) || !std::isfinite(lo) || !std::isfinite(hi)) return fail(VR_EINVALID, "LUT domain must satisfy lo < hi");
+    return VR_OK;
+}
+
+// device scratch for one visibility evaluation
+struct VisScratch {
+    Scratch mem;
+    vr::VisArgs v{};
+    explicit VisScratch(cudaStream_t s) : mem(s) {}
+    cudaError_t init(const vr_grid *gr, const double *lut_dev, int nbins, double lo, double hi, double margin,
+                     bool want_global) {
+        int nb = gr->nblocks;
+        size_t off_bits = 0, off_empty = off_bits + 2048 * 4, off_aabb = (off_empty + nb + 15) & ~size_t(15);
+        size_t off_box = off_aabb + (size_t)nb * 6 * 4;
+        off_box = (off_box + 15) & ~size_t(15);
+        size_t off_glob = off_box + (size_t)nb * 6 * 8;
+        size_t off_cnt = off_glob + (want_global ? (size_t)nb * 6 * 8 : 0);
+        size_t total = off_cnt + 2 * 8;
+        cudaError_t e = mem.alloc(total);
+        if (e != cudaSuccess) return e;
+        char *base = (char *)mem.p;
+        v.lut = lut_dev;
+        v.nbins = nbins;
+        v.lut_lo = lo;
+        v.bin_width = (hi - lo) / (double)nbins;  // ClassifiedLUT.bin_width, transfer.py:115-118
+        v.vmin = gr->vmin;
+        v.vmax = gr->vmax;
+        v.nblocks = nb;
+        v.visbits = (unsigned int *)(base + off_bits);
+        v.empty = (uint8_t *)(base + off_empty);
+        v.aabb = (int *)(base + off_aabb);
+        v.box = (double *)(base + off_box);
+        v.aabb_global = want_global ? (long long *)(base + off_glob) : nullptr;
+        v.counters = (unsigned long long *)(base + off_cnt);
+        v.margin = margin;
+        return cudaSuccess;
+    }
+};
+
+int vr_grid_visibility(const vr_grid *gr, const double *lut_rgba, int32_t nbins, double lut_lo, double lut_hi,
+                       uint8_t *empty, int64_t *aabb_lo, int64_t *aabb_hi, void *stream) {
+    if (!gr || !lut_rgba || !empty || !aabb_lo || !aabb_hi) return fail(VR_EINVALID, "null pointer");
+    int rc = check_lut(nbins, lut_lo, lut_hi);
+    if (rc) return rc;
+    DeviceGuard g(gr->vol->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch lut(s);
+    VR_CUDA(lut.alloc(sizeof(double) * 4 * nbins));
+    VR_CUDA(cudaMemcpyAsync(lut.p, lut_rgba, sizeof(double) * 4 * nbins, cudaMemcpyHostToDevice, s));
+    VisScratch vs(s);
+    VR_CUDA(vs.init(gr, (const double *)lut.p, nbins, lut_lo, lut_hi, 0.0, true));
+    VR_CUDA(vr::launch_visibility(gr->vol->data, gr->L, vs.v, s));
+    int nb = gr->nblocks;
+    std::vector<long long> glob((size_t)nb * 6);
+    unsigned long long cnt[2];
+    VR_CUDA(cudaMemcpyAsync(empty, vs.v.empty, nb, cudaMemcpyDeviceToHost, s));
+    VR_CUDA(cudaMemcpyAsync(glob.data(), vs.v.aabb_global, sizeof(long long) * 6 * nb, cudaMemcpyDeviceToHost, s));
+    VR_CUDA(cudaMemcpyAsync(cnt, vs.v.counters, sizeof(cnt), cudaMemcpyDeviceToHost, s));
+    VR_CUDA(cudaStreamSynchronize(s));
+    for (int b = 0; b < nb; ++b)
+        for (int k = 0; k < 3; ++k) {
+            aabb_lo[3 * b + k] = glob[6 * b + k];
+            aabb_hi[3 * b + k] = glob[6 * b + 3 + k];
+        }
+    if (cnt[1]) return fail(VR_EINVALID, "EmptyBlock: a block passed the interval test but has no visible voxel");
+    return VR_OK;
+}
+
+// ------------------------------------------------------------------- render
+
+static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_render_params *prm,
+                      const double *lut, const double *table, const uint8_t *rgba, vr::RenderArgs &a) {
+    if (!vol || !cam || !prm || !lut) return fail(VR_EINVALID, "null pointer");
+    if (grid && grid->vol != vol) return fail(VR_EINVALID, "grid belongs to another volume");
+    // render.py:183-208 and Camera.__post_init__ (render.py:67-76) equivalents
+    if (cam->width < 1 || cam->height < 1) return fail(VR_EINVALID, "image size must be positive");
+    if (cam->tile_x < 0 || cam->tile_y < 0 || cam->tile_w < 0 || cam->tile_h < 0 ||
+        cam->tile_x + cam->tile_w > cam->width || cam->tile_y + cam->tile_h > cam->height)
+        return fail(VR_EINVALID, "tile outside the frame");
+    if (cam->projection != VR_PINHOLE && cam->projection != VR_ORTHOGRAPHIC)
+        return fail(VR_EINVALID, "unknown projection");
+    if (cam->interleave_n > 1 && !(0 <= cam->interleave_k && cam->interleave_k < cam->interleave_n))
+        return fail(VR_EINVALID, "interleave_k must be in [0, interleave_n)");
+    if (!finite_positive(prm->step) || !finite_positive(prm->ref_step)) return fail(VR_EINVALID, "step must be positive");
+    if (prm->mode != VR_MODE_DVR && prm->mode != VR_MODE_ISO) return fail(VR_EINVALID, "unknown mode");
+    if (prm->classify < 0 || prm->classify > 2) return fail(VR_EINVALID, "unknown classification");
+    if (!(prm->term_alpha > 0.0 && prm->term_alpha <= 1.0))
+        return fail(VR_EINVALID, "early_termination_alpha must be in (0, 1]");
+    for (int k = 0; k < 4; ++k)
+        if (!(prm->bg[k] >= 0.0 && prm->bg[k] <= 1.0)) return fail(VR_EINVALID, "background must be in [0, 1]");
+    int rc = check_lut(prm->nlut, prm->lut_lo, prm->lut_hi);
+    if (rc) return rc;
+    int classify = prm->mode == VR_MODE_ISO ? VR_CLS_POST : prm->classify;  // render.py:373-374
+    if (classify == VR_CLS_PREINT && (!table || prm->ntbl < 1)) return fail(VR_EINVALID, "pre-integrated table missing");
+    if (classify == VR_CLS_PRE && !rgba) return fail(VR_EINVALID, "preclassified volume missing");
+    if (prm->mode == VR_MODE_ISO && !(vol->vmin <= prm->isovalue && prm->isovalue <= vol->vmax))
+        return fail(VR_EISO, "isovalue outside value range");
+
+    a = vr::RenderArgs();
+    a.vol = vol->data;
+    a.L = grid ? grid->L : monolithic_layout(vol);
+    a.dsx = vr::make_divisor(vol->sx);
+    a.dsy = vr::make_divisor(vol->sy);
+    a.dsz = vr::make_divisor(vol->sz);
+    a.ext_mm[0] = (double)(vol->nx - 1) * vol->sx;
+    a.ext_mm[1] = (double)(vol->ny - 1) * vol->sy;
+    a.ext_mm[2] = (double)(vol->nz - 1) * vol->sz;
+    a.projection = cam->projection;
+    a.W = cam->width;
+    a.H = cam->height;
+    a.tx = cam->tile_x;
+    a.ty = cam->tile_y;
+    a.tw = cam->tile_w;
+    a.th = cam->tile_h;
+    for (int k = 0; k < 3; ++k) {
+        a.pos[k] = cam->position[k];
+        a.fwd[k] = cam->fwd[k];
+        a.right[k] = cam->right[k];
+        a.up[k] = cam->up[k];
+    }
+    a.half_w = cam->half_w;
+    a.half_h = cam->half_h;
+    long long npix_unused;
+    cell_counts(cam, a.cells_x, a.ncells, a.slots, npix_unused);
+    a.il_n = cam->interleave_n > 1 ? cam->interleave_n : 1;
+    a.il_k = cam->interleave_n > 1 ? cam->interleave_k : 0;
+    a.step = prm->step;
+    a.ref_step = prm->ref_step;
+    a.corr = vr::make_pow(prm->step / prm->ref_step);  // _kernels.py:338
+    a.shin = vr::make_pow(prm->shininess);
+    a.mode = prm->mode;
+    a.cubic = prm->cubic ? 1 : 0;
+    a.lighting = prm->lighting ? 1 : 0;
+    a.classify = classify;
+    a.skip_empty = grid ? 1 : 0;
+    a.chained = (prm->mode == VR_MODE_ISO || classify == VR_CLS_PREINT) ? 1 : 0;
+    a.isovalue = prm->isovalue;
+    a.term_alpha = prm->term_alpha;
+    a.ka = prm->ka;
+    a.kd = prm->kd;
+    a.ks = prm->ks;
+    for (int k = 0; k < 4; ++k) a.bg[k] = prm->bg[k];
+    a.lut = lut;
+    a.nlut = prm->nlut;
+    a.lut_lo = prm->lut_lo;
+    a.lut_inv_w = (double)prm->nlut / (prm->lut_hi - prm->lut_lo);  // render.py:423
+    a.table = table;
+    a.ntbl = classify == VR_CLS_PREINT ? prm->ntbl : 1;
+    a.tbl_lo = prm->lut_lo;
+    a.tbl_inv_w = (double)a.ntbl / (prm->lut_hi - prm->lut_lo);  // render.py:425
+    a.rgba = rgba;
+    a.rgba_plane = vol->nx * vol->ny * vol->nz;
+    return VR_OK;
+}
+
+static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_render_params *prm,
+                       const double *lut, const double *table, const uint8_t *rgba, const vr_render_outputs *out,
+                       cudaStream_t s) {
+    vr::RenderArgs a;
+    int rc = build_args(vol, grid, cam, prm, lut, table, rgba, a);
+    if (rc) return rc;
+    if (!out) return fail(VR_EINVALID, "null outputs");
+    a.pixels = out->pixels;
+    a.premult = out->premult;
+    a.depth = out->depth;
+    a.taken = (long long *)out->taken;
+    a.skipped = (long long *)out->skipped;
+    a.blocks_hit = out->blocks_hit;
+    a.totals = (unsigned long long *)out->totals;
+    a.shaded = (unsigned long long *)out->shaded;
+    int nblocks = grid ? grid->nblocks : 1;
+    if (a.blocks_hit) VR_CUDA(cudaMemsetAsync(a.blocks_hit, 0, nblocks, s));
+    VisScratch vs(s);
+    if (grid) {
+        VR_CUDA(vs.init(grid, lut, prm->nlut, prm->lut_lo, prm->lut_hi, prm->margin, false));
+        VR_CUDA(vr::launch_visibility(vol->data, grid->L, vs.v, s));
+        a.empty = vs.v.empty;
+        a.box = vs.v.box;
+        a.vmin = grid->vmin;
+        a.vmax = grid->vmax;
+    }
+    if (out->ev_start) VR_CUDA(cudaEventRecord((cudaEvent_t)out->ev_start, s));
+    VR_CUDA(vr::launch_raycast(a, s));
+    if (out->ev_stop) VR_CUDA(cudaEventRecord((cudaEvent_t)out->ev_stop, s));
+    if (out->totals) {
+        if (a.blocks_hit) VR_CUDA(vr::launch_count_hits(a.blocks_hit, nblocks, a.totals + 2, s));
+        if (grid) {
+            VR_CUDA(cudaMemcpyAsync(a.totals + 3, vs.v.counters, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+            VR_CUDA(cudaMemcpyAsync(a.totals + 4, vs.v.counters + 1, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+        } else {
+            VR_CUDA(cudaMemsetAsync(a.totals + 3, 0, 2 * sizeof(unsigned long long), s));
+        }
+    }
+    return VR_OK;
+}
+
+int vr_render(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_render_params *prm, const double *lut,
+              const double *table, const uint8_t *rgba, const vr_render_outputs *out, void *stream) {
+    if (!vol) return fail(VR_EINVALID, "null volume");
+    DeviceGuard g(vol->device);
+    return render_impl(vol, grid, cam, prm, lut, table, rgba, out, (cudaStream_t)stream);
+}
+
+int vr_render_to_host(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_render_params *prm,
+                      const double *lut_host, const double *table_host, uint8_t *pixels_host, double *premult_host,
+                      double *depth_host, uint64_t *totals_host, void *stream) {
+    if (!vol || !cam || !prm || !lut_host || !pixels_host || !totals_host) return fail(VR_EINVALID, "null pointer");
+    DeviceGuard g(vol->device);
+    configure_pool(vol->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    int classify = prm->mode == VR_MODE_ISO ? VR_CLS_POST : prm->classify;
+    int cells_x, ncells, slots;
+    long long npix;
+    cell_counts(cam, cells_x, ncells, slots, npix);
+    int nblocks = grid ? grid->nblocks : 1;
+    size_t lut_b = sizeof(double) * 4 * (size_t)std::max(prm->nlut, 1);
+    size_t tbl_b = (classify == VR_CLS_PREINT && table_host) ? sizeof(double) * 4 * (size_t)prm->ntbl * prm->ntbl : 0;
+    size_t pix_b = (size_t)npix * 4, pre_b = premult_host ? (size_t)npix * 32 : 0, dep_b = depth_host ? (size_t)npix * 8 : 0;
+    size_t o_lut = 0, o_tbl = o_lut + lut_b, o_pre = (o_tbl + tbl_b + 255) & ~size_t(255);
+    size_t o_dep = o_pre + pre_b, o_tot = (o_dep + dep_b + 255) & ~size_t(255);
+    size_t o_hit = o_tot + 8 * 8, o_pix = (o_hit + nblocks + 255) & ~size_t(255);
+    size_t total = o_pix + pix_b;
+    Scratch mem(s);
+    VR_CUDA(mem.alloc(total));
+    char *base = (char *)mem.p;
+    VR_CUDA(cudaMemcpyAsync(base + o_lut, lut_host, lut_b, cudaMemcpyHostToDevice, s));
+    if (tbl_b) VR_CUDA(cudaMemcpyAsync(base + o_tbl, table_host, tbl_b, cudaMemcpyHostToDevice, s));
+    VR_CUDA(cudaMemsetAsync(base + o_tot, 0, 8 * 8, s));
+    Scratch rgba(s);
+    if (classify == VR_CLS_PRE) {
+        long long nvox = vol->nx * vol->ny * vol->nz;
+        VR_CUDA(rgba.alloc((size_t)nvox * 4));
+        VR_CUDA(vr::launch_preclassify(vol->data, nvox, (const double *)(base + o_lut), prm->nlut, prm->lut_lo,
+                                       (prm->lut_hi - prm->lut_lo) / (double)prm->nlut, (uint8_t *)rgba.p, s));
+    }
+    vr_render_outputs out = {};
+    out.pixels = (uint8_t *)(base + o_pix);
+    out.premult = premult_host ? (double *)(base + o_pre) : nullptr;
+    out.depth = depth_host ? (double *)(base + o_dep) : nullptr;
+    out.blocks_hit = (uint8_t *)(base + o_hit);
+    out.totals = (uint64_t *)(base + o_tot);
+    int rc = render_impl(vol, grid, cam, prm, (const double *)(base + o_lut), tbl_b ? (const double *)(base + o_tbl) : nullptr,
+                         (const uint8_t *)rgba.p, &out, s);
+    if (rc) return rc;
+    VR_CUDA(cudaMemcpyAsync(pixels_host, out.pixels, pix_b, cudaMemcpyDeviceToHost, s));
+    if (premult_host) VR_CUDA(cudaMemcpyAsync(premult_host, out.premult, pre_b, cudaMemcpyDeviceToHost, s));
+    if (depth_host) VR_CUDA(cudaMemcpyAsync(depth_host, out.depth, dep_b, cudaMemcpyDeviceToHost, s));
+    VR_CUDA(cudaMemcpyAsync(totals_host, out.totals, 5 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    VR_CUDA(cudaStreamSynchronize(s));
+    return VR_OK;
+}
+
+int vr_preclassify(const vr_volume *vol, const double *lut, int32_t nbins, double lut_lo, double lut_hi,
+                   uint8_t *rgba_out, void *stream) {
+    if (!vol || !lut || !rgba_out) return fail(VR_EINVALID, "null pointer");
+    int rc = check_lut(nbins, lut_lo, lut_hi);
+    if (rc) return rc;
+    DeviceGuard g(vol->device);
+    VR_CUDA(vr::launch_preclassify(vol->data, vol->nx * vol->ny * vol->nz, lut, nbins, lut_lo,
+                                   (lut_hi - lut_lo) / (double)nbins, rgba_out, (cudaStream_t)stream));
+    return VR_OK;
+}
+
+// ----------------------------------------------------------------- sampling
+
+int vr_sample_points(const vr_volume *vol, const double *pts, int64_t n, int cubic, double *out, void *stream) {
+    if (!vol || (n > 0 && (!pts || !out))) return fail(VR_EINVALID, "null pointer");
+    DeviceGuard g(vol->device);
+    VR_CUDA(vr::launch_sample_points(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, pts, n, cubic, 0, vol->sx,
+                                     vol->sy, vol->sz, out, (cudaStream_t)stream));
+    return VR_OK;
+}
+
+int vr_gradient_points(const vr_volume *vol, const double *pts, int64_t n, int cubic, double *out, void *stream) {
+    if (!vol || (n > 0 && (!pts || !out))) return fail(VR_EINVALID, "null pointer");
+    DeviceGuard g(vol->device);
+    VR_CUDA(vr::launch_sample_points(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, pts, n, cubic, 1, vol->sx,
+                                     vol->sy, vol->sz, out, (cudaStream_t)stream));
+    return VR_OK;
+}
+
+// ---------------------------------------------------------------- measure
+
+int vr_threshold_count(const vr_volume *vol, int32_t thr, uint64_t *count, void *stream) {
+    if (!vol || !count) return fail(VR_EINVALID, "null pointer");
+    DeviceGuard g(vol->device);
+    VR_CUDA(vr::launch_threshold_count(vol->data, vol->nx * vol->ny * vol->nz, thr, (unsigned long long *)count,
+                                       (cudaStream_t)stream));
+    return VR_OK;
+}
+
+int vr_ball_counts(const vr_volume *vol, int32_t thr, const double *centres, const double *radii, int64_t nballs,
+                   uint64_t *counts, uint64_t *faces, void *stream) {
+    if (!vol || (nballs > 0 && (!centres || !radii || !counts))) return fail(VR_EINVALID, "null pointer");
+    if (nballs > (1 << 30)) return fail(VR_EINVALID, "too many balls");
+    DeviceGuard g(vol->device);
+    VR_CUDA(vr::launch_ball_counts(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, vol->sx, vol->sy, vol->sz,
+                                   thr, centres, radii, (int)nballs, (unsigned long long *)counts,
+                                   (unsigned long long *)faces, (cudaStream_t)stream));
+    return VR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,570 @@
+// vr_prep.cu -- K1/K2/K4 kernels and the point sampler (see vr_prep.cuh).
+#include <cfloat>
+#include <climits>
+
+#include "vr_prep.cuh"
+
+namespace vr {
+namespace {
+
+constexpr int kBlock = 256;
+
+VR_D int warp_min(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+VR_D int warp_max(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+VR_D unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+int grid_for(long long n, int block, int cap = 148 * 16) {
+    long long g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    return (int)(g < cap ? g : cap);
+}
+
+// ------------------------------------------------------------ value range
+
+__global__ void init_minmax_kernel(int *out, int count) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) {
+        out[2 * i] = INT_MAX;
+        out[2 * i + 1] = INT_MIN;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) value_range_kernel(const int16_t *__restrict__ v, long long n, int *out) {
+    int lo = INT_MAX, hi = INT_MIN;
+    long long nvec = n / 8;
+    const int4 *v8 = reinterpret_cast<const int4 *>(v);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+        int4 q = __ldg(v8 + i);
+        const int16_t *h = reinterpret_cast<const int16_t *>(&q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            lo = min(lo, (int)h[k]);
+            hi = max(hi, (int)h[k]);
+        }
+    }
+    for (long long i = nvec * 8 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        lo = min(lo, (int)v[i]);
+        hi = max(hi, (int)v[i]);
+    }
+    lo = warp_min(lo);
+    hi = warp_max(hi);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(out, lo);
+        atomicMax(out + 1, hi);
+    }
+}
+
+// --------------------------------------------------------------- phantoms
+
+struct Ellipsoid {
+    double cx, cy, cz, ax, ay, az, s_min, width;
+};
+
+struct PhantomArgs {
+    int kind, nx, ny, nz;
+    Ellipsoid e[4];       // torso: body, spine, blob_l, blob_r
+    double c[3];          // sphere: integer centres d//2; shell: (d-1)/2
+    double radius;        // sphere: min(dims)//2 ; shell: min(dims)/2
+    double r_in, r_out;   // shell: 0.55*radius, 0.80*radius
+};
+
+// phantoms.py:32-42
+VR_D double ellipsoid_blend(const Ellipsoid &E, double x, double y, double z) {
+    double qx = (x - E.cx) / E.ax;
+    double qy = (y - E.cy) / E.ay;
+    double qz = (z - E.cz) / E.az;
+    double e = sqrt((qx * qx + qy * qy) + qz * qz);
+    double v = (1.0 - e) * E.s_min / E.width + 0.5;
+    return fmin(fmax(v, 0.0), 1.0);
+}
+
+__global__ void __launch_bounds__(kBlock) phantom_kernel(const __grid_constant__ PhantomArgs p, int16_t *out) {
+    long long n = (long long)p.nx * p.ny * p.nz;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        int ix = (int)(i % p.nx);
+        long long r = i / p.nx;
+        int iy = (int)(r % p.ny);
+        int iz = (int)(r / p.ny);
+        double x = ix, y = iy, z = iz;
+        double field;
+        if (p.kind == 2) {  // torso, phantoms.py:63-79
+            double body = ellipsoid_blend(p.e[0], x, y, z);
+            double spine = ellipsoid_blend(p.e[1], x, y, z);
+            double bl = ellipsoid_blend(p.e[2], x, y, z);
+            double br = ellipsoid_blend(p.e[3], x, y, z);
+            double bone = fmax(spine, fmax(bl, br));
+            field = (-1000.0 + 1040.0 * body) + 1160.0 * bone;
+        } else {
+            double dx = x - p.c[0], dy = y - p.c[1], dz = z - p.c[2];
+            double rr = sqrt((dx * dx + dy * dy) + dz * dz);
+            if (p.kind == 0) {  // sphere, phantoms.py:45-50
+                double v = 1000.0 - 2000.0 * rr / p.radius;
+                field = fmin(fmax(v, -1000.0), 1000.0);
+            } else {  // shell, phantoms.py:53-60
+                double d = fmax(p.r_in - rr, rr - p.r_out);
+                double band = fmin(fmax(0.5 - d / 1.5, 0.0), 1.0);
+                field = -1000.0 + 1800.0 * band;
+            }
+        }
+        out[i] = (int16_t)rint(field);
+    }
+}
+
+// ------------------------------------------------------------- block minmax
+
+VR_D void block_coords(const Layout &L, int b, int &bi, int &bj, int &bk) {
+    bi = b % L.nb[0];
+    int r = b / L.nb[0];
+    bj = r % L.nb[1];
+    bk = r / L.nb[1];
+}
+
+// one CTA per (block, z-chunk); rows of the block are read x-contiguous
+__global__ void __launch_bounds__(kBlock) block_minmax_kernel(const int16_t *__restrict__ vol, const Layout L,
+                                                              int *vmin, int *vmax) {
+    int b = blockIdx.x;
+    int bi, bj, bk;
+    block_coords(L, b, bi, bj, bk);
+    int ox = block_origin(L, bi), oy = block_origin(L, bj), oz = block_origin(L, bk);
+    int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj), ez = block_extent(L, 2, bk);
+    int z0 = (int)((long long)ez * blockIdx.y / gridDim.y);
+    int z1 = (int)((long long)ez * (blockIdx.y + 1) / gridDim.y);
+    long long cnt = (long long)(z1 - z0) * ey * ex;
+    int lo = INT_MAX, hi = INT_MIN;
+    for (long long i = threadIdx.x; i < cnt; i += blockDim.x) {
+        int x = (int)(i % ex);
+        long long r = i / ex;
+        int y = (int)(r % ey);
+        int z = z0 + (int)(r / ey);
+        int v = __ldg(vol + (long long)(oz + z) * L.pz + (long long)(oy + y) * L.py + ox + x);
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+    lo = warp_min(lo);
+    hi = warp_max(hi);
+    if ((threadIdx.x & 31) == 0 && cnt > 0) {
+        atomicMin(vmin + b, lo);
+        atomicMax(vmax + b, hi);
+    }
+}
+
+__global__ void init_block_minmax_kernel(int *vmin, int *vmax, int n) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        vmin[i] = INT_MAX;
+        vmax[i] = INT_MIN;
+    }
+}
+
+// ------------------------------------------------------------- visibility
+
+// transfer.py:120-125 ClassifiedLUT.bin_index
+VR_D int classified_bin(double s, double lo, double bin_width, int nbins) {
+    double f = floor((s - lo) / bin_width);
+    if (f < 0.0) return 0;
+    if (f > (double)(nbins - 1)) return nbins - 1;
+    return (int)f;
+}
+
+constexpr int kSetupThreads = 1024;
+
+// cull_empty (blocks.py:161-173) + the per-value visibility bitmask that
+// fit_bounding_box (blocks.py:176-199) tests per voxel.
+__global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs v) {
+    extern __shared__ int prefix[];  // nbins + 1
+    __shared__ int chunk_sum[kSetupThreads];
+    __shared__ unsigned int n_empty;
+    const int tid = threadIdx.x;
+    // flags and an exclusive prefix over the bins with nonzero opacity
+    // (ClassifiedLUT.opacity_prefix, transfer.py:131-133)
+    int per = (v.nbins + kSetupThreads - 1) / kSetupThreads;
+    int b0 = tid * per, b1 = min(b0 + per, v.nbins);
+    int s = 0;
+    for (int i = b0; i < b1; ++i) s += (__ldg(v.lut + 4 * i + 3) > 0.0) ? 1 : 0;
+    chunk_sum[tid] = s;
+    if (tid == 0) n_empty = 0;
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int i = 0; i < kSetupThreads; ++i) {
+            int c = chunk_sum[i];
+            chunk_sum[i] = run;
+            run += c;
+        }
+        prefix[v.nbins] = run;
+    }
+    __syncthreads();
+    int run = chunk_sum[tid];
+    for (int i = b0; i < b1; ++i) {
+        prefix[i] = run;
+        run += (__ldg(v.lut + 4 * i + 3) > 0.0) ? 1 : 0;
+    }
+    __syncthreads();
+    // visibility bit per int16 value: lut.rgba[bin_index(v), 3] > 0
+    for (int w = tid; w < 2048; w += kSetupThreads) {
+        unsigned int bits = 0;
+        for (int k = 0; k < 32; ++k) {
+            int val = w * 32 + k - 32768;
+            int bin = classified_bin((double)val, v.lut_lo, v.bin_width, v.nbins);
+            int vis = (prefix[bin + 1] - prefix[bin]) > 0;
+            bits |= (unsigned int)vis << k;
+        }
+        v.visbits[w] = bits;
+    }
+    // interval test per block, sentinel AABB for the fit kernel
+    for (int b = tid; b < v.nblocks; b += kSetupThreads) {
+        int lo = classified_bin((double)v.vmin[b], v.lut_lo, v.bin_width, v.nbins);
+        int hi = classified_bin((double)v.vmax[b], v.lut_lo, v.bin_width, v.nbins);
+        bool visible = (prefix[hi + 1] - prefix[lo]) > 0;
+        v.empty[b] = visible ? 0 : 1;
+        if (!visible) atomicAdd(&n_empty, 1u);
+        int *ab = v.aabb + 6 * b;
+        ab[0] = ab[1] = ab[2] = INT_MAX;
+        ab[3] = ab[4] = ab[5] = -1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        v.counters[0] = n_empty;
+        v.counters[1] = 0;
+    }
+}
+
+// fit_bounding_box (blocks.py:176-199): local min/max of visible voxels
+__global__ void __launch_bounds__(kBlock) aabb_kernel(const int16_t *__restrict__ vol, const Layout L, const VisArgs v) {
+    __shared__ unsigned int bits[2048];
+    int b = blockIdx.x;
+    if (v.empty[b]) return;
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) bits[i] = v.visbits[i];
+    __syncthreads();
+    int bi, bj, bk;
+    block_coords(L, b, bi, bj, bk);
+    int ox = block_origin(L, bi), oy = block_origin(L, bj), oz = block_origin(L, bk);
+    int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj), ez = block_extent(L, 2, bk);
+    int z0 = (int)((long long)ez * blockIdx.y / gridDim.y);
+    int z1 = (int)((long long)ez * (blockIdx.y + 1) / gridDim.y);
+    long long cnt = (long long)(z1 - z0) * ey * ex;
+    int mnx = INT_MAX, mny = INT_MAX, mnz = INT_MAX, mxx = -1, mxy = -1, mxz = -1;
+    for (long long i = threadIdx.x; i < cnt; i += blockDim.x) {
+        int x = (int)(i % ex);
+        long long r = i / ex;
+        int y = (int)(r % ey);
+        int z = z0 + (int)(r / ey);
+        int val = __ldg(vol + (long long)(oz + z) * L.pz + (long long)(oy + y) * L.py + ox + x);
+        unsigned int u = (unsigned int)(val + 32768);
+        if ((bits[u >> 5] >> (u & 31)) & 1u) {
+            mnx = min(mnx, x); mxx = max(mxx, x);
+            mny = min(mny, y); mxy = max(mxy, y);
+            mnz = min(mnz, z); mxz = max(mxz, z);
+        }
+    }
+    mnx = warp_min(mnx); mny = warp_min(mny); mnz = warp_min(mnz);
+    mxx = warp_max(mxx); mxy = warp_max(mxy); mxz = warp_max(mxz);
+    if ((threadIdx.x & 31) == 0 && mxx >= 0) {
+        int *ab = v.aabb + 6 * b;
+        atomicMin(ab + 0, mnx); atomicMin(ab + 1, mny); atomicMin(ab + 2, mnz);
+        atomicMax(ab + 3, mxx); atomicMax(ab + 4, mxy); atomicMax(ab + 5, mxz);
+    }
+}
+
+// dilate by one, clip to the block, globalise (blocks.py:189-198) and apply
+// the render margin (render.py:388-390)
+__global__ void box_kernel(const Layout L, const VisArgs v) {
+    int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= v.nblocks) return;
+    int bi, bj, bk;
+    block_coords(L, b, bi, bj, bk);
+    const int org[3] = {block_origin(L, bi), block_origin(L, bj), block_origin(L, bk)};
+    const int ext[3] = {block_extent(L, 0, bi), block_extent(L, 1, bj), block_extent(L, 2, bk)};
+    const int *ab = v.aabb + 6 * b;
+    bool fitted = !v.empty[b] && ab[3] >= 0;
+    if (!v.empty[b] && !fitted) atomicAdd(v.counters + 1, 1ull);  // reference raises EmptyBlock
+    for (int k = 0; k < 3; ++k) {
+        long long lo, hi;
+        if (fitted) {
+            lo = org[k] + max(ab[k] - 1, 0);
+            hi = org[k] + min(ab[3 + k] + 1, ext[k] - 1);
+        } else {
+            lo = LLONG_MAX / 2;
+            hi = -1;
+        }
+        v.box[6 * b + k] = (double)lo - v.margin;
+        v.box[6 * b + 3 + k] = (double)hi + v.margin;
+        if (v.aabb_global) {
+            v.aabb_global[6 * b + k] = lo;
+            v.aabb_global[6 * b + 3 + k] = hi;
+        }
+    }
+}
+
+__global__ void count_hits_kernel(const uint8_t *hits, int n, unsigned long long *out) {
+    unsigned long long c = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c += hits[i] ? 1 : 0;
+    c = warp_sum(c);
+    __shared__ unsigned long long part[32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
+        *out = s;
+    }
+}
+
+// --------------------------------------------------------- preclassify
+
+__global__ void __launch_bounds__(kBlock) preclassify_kernel(const int16_t *__restrict__ vol, long long n,
+                                                             const double *__restrict__ lut, int nbins,
+                                                             double lo, double bw, uint8_t *rgba) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        int k = classified_bin((double)vol[i], lo, bw, nbins);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) rgba[c * n + i] = (uint8_t)rint(__ldg(lut + 4 * k + c) * 255.0);
+    }
+}
+
+// ------------------------------------------------------- point sampling
+
+__global__ void __launch_bounds__(kBlock) sample_points_kernel(const int16_t *vol, int nx, int ny, int nz,
+                                                               const double *pts, long long n, int cubic,
+                                                               int gradient, double sx, double sy, double sz,
+                                                               double *out) {
+    long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Brick<int16_t> b;
+    b.base = vol;
+    b.py = nx;
+    b.pz = (long long)nx * ny;
+    b.ex = nx;
+    b.ey = ny;
+    b.ez = nz;
+    double x = pts[3 * i], y = pts[3 * i + 1], z = pts[3 * i + 2];
+    bool c = cubic != 0;
+    if (!gradient) {
+        out[i] = sample(b, x, y, z, c);
+        return;
+    }
+    const double h = 0.5;  // _kernels.py:153-166
+    double gx = sample(b, x + h, y, z, c) - sample(b, x - h, y, z, c);
+    double gy = sample(b, x, y + h, z, c) - sample(b, x, y - h, z, c);
+    double gz = sample(b, x, y, z + h, c) - sample(b, x, y, z - h, c);
+    out[3 * i] = gx / sx;
+    out[3 * i + 1] = gy / sy;
+    out[3 * i + 2] = gz / sz;
+}
+
+// ---------------------------------------------------------- K4 measure
+
+__global__ void __launch_bounds__(kBlock) threshold_kernel(const int16_t *__restrict__ v, long long n, int thr,
+                                                           unsigned long long *count) {
+    unsigned long long c = 0;
+    long long nvec = n / 8;
+    const int4 *v8 = reinterpret_cast<const int4 *>(v);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+        int4 q = __ldg(v8 + i);
+        const int16_t *h = reinterpret_cast<const int16_t *>(&q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c += (h[k] >= thr) ? 1 : 0;
+    }
+    for (long long i = nvec * 8 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        c += (v[i] >= thr) ? 1 : 0;
+    c = warp_sum(c);
+    __shared__ unsigned long long part[kBlock / 32];
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int w = 0; w < kBlock / 32; ++w) s += part[w];
+        if (s) atomicAdd(count, s);
+    }
+}
+
+// one CTA per ball; voxels of the ball's bounding box, exact membership test
+__global__ void __launch_bounds__(kBlock) ball_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
+                                                      double sx, double sy, double sz, int thr,
+                                                      const double *centres, const double *radii,
+                                                      unsigned long long *counts, unsigned long long *faces) {
+    int q = blockIdx.x;
+    double cx = centres[3 * q], cy = centres[3 * q + 1], cz = centres[3 * q + 2];
+    double rad = radii[q];
+    double r2 = rad * rad;
+    // conservative index bounds (one voxel of slack each side)
+    int i0 = max(0, (int)floor((cx - rad) / sx) - 1), i1 = min(nx - 1, (int)ceil((cx + rad) / sx) + 1);
+    int j0 = max(0, (int)floor((cy - rad) / sy) - 1), j1 = min(ny - 1, (int)ceil((cy + rad) / sy) + 1);
+    int k0 = max(0, (int)floor((cz - rad) / sz) - 1), k1 = min(nz - 1, (int)ceil((cz + rad) / sz) + 1);
+    unsigned long long c = 0, f = 0;
+    if (i0 <= i1 && j0 <= j1 && k0 <= k1) {
+        int wx = i1 - i0 + 1, wy = j1 - j0 + 1;
+        long long cnt = (long long)wx * wy * (k1 - k0 + 1);
+        long long py = nx, pz = (long long)nx * ny;
+        for (long long t = threadIdx.x; t < cnt; t += blockDim.x) {
+            int i = i0 + (int)(t % wx);
+            long long r = t / wx;
+            int j = j0 + (int)(r % wy);
+            int k = k0 + (int)(r / wy);
+            double dx = (double)i * sx - cx, dy = (double)j * sy - cy, dz = (double)k * sz - cz;
+            if ((dx * dx + dy * dy) + dz * dz > r2) continue;
+            const int16_t *p = vol + k * pz + j * py + i;
+            if (__ldg(p) < thr) continue;
+            c += 1;
+            if (faces) {
+                f += (i == 0 || __ldg(p - 1) < thr) ? 1 : 0;
+                f += (i == nx - 1 || __ldg(p + 1) < thr) ? 1 : 0;
+                f += (j == 0 || __ldg(p - py) < thr) ? 1 : 0;
+                f += (j == ny - 1 || __ldg(p + py) < thr) ? 1 : 0;
+                f += (k == 0 || __ldg(p - pz) < thr) ? 1 : 0;
+                f += (k == nz - 1 || __ldg(p + pz) < thr) ? 1 : 0;
+            }
+        }
+    }
+    c = warp_sum(c);
+    f = warp_sum(f);
+    __shared__ unsigned long long pc[kBlock / 32], pf[kBlock / 32];
+    if ((threadIdx.x & 31) == 0) {
+        pc[threadIdx.x >> 5] = c;
+        pf[threadIdx.x >> 5] = f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long sc = 0, sf = 0;
+        for (int w = 0; w < kBlock / 32; ++w) {
+            sc += pc[w];
+            sf += pf[w];
+        }
+        counts[q] = sc;
+        if (faces) faces[q] = sf;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_value_range(const int16_t *vol, long long n, int *out, cudaStream_t s) {
+    init_minmax_kernel<<<1, 32, 0, s>>>(out, 1);
+    value_range_kernel<<<grid_for(n / 8 + 1, kBlock), kBlock, 0, s>>>(vol, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_phantom(int kind, int nx, int ny, int nz, int16_t *out, cudaStream_t s) {
+    PhantomArgs p = {};
+    p.kind = kind;
+    p.nx = nx;
+    p.ny = ny;
+    p.nz = nz;
+    if (kind == 2) {
+        // phantoms.py:63-79: c(f) = f * n, s(f) = f * n in float64
+        const double C[4][3] = {{0.50, 0.63, 0.63}, {0.50, 0.63, 0.71}, {0.34, 0.60, 0.55}, {0.68, 0.66, 0.56}};
+        const double S[4][3] = {{0.46, 0.29, 0.29}, {0.40, 0.065, 0.065}, {0.17, 0.10, 0.08}, {0.12, 0.11, 0.09}};
+        const double W[4] = {2.0, 1.5, 1.5, 1.5};
+        for (int k = 0; k < 4; ++k) {
+            Ellipsoid &e = p.e[k];
+            e.cx = C[k][0] * nx;
+            e.cy = C[k][1] * ny;
+            e.cz = C[k][2] * nz;
+            e.ax = S[k][0] * nx;
+            e.ay = S[k][1] * ny;
+            e.az = S[k][2] * nz;
+            double m = e.ax;  // min(ax, ay, az)
+            if (e.ay < m) m = e.ay;
+            if (e.az < m) m = e.az;
+            e.s_min = m;
+            e.width = W[k];
+        }
+    } else if (kind == 0) {
+        p.c[0] = nx / 2;
+        p.c[1] = ny / 2;
+        p.c[2] = nz / 2;
+        int m = nx < ny ? nx : ny;
+        m = m < nz ? m : nz;
+        p.radius = (double)(m / 2);
+    } else {
+        p.c[0] = (nx - 1) / 2.0;
+        p.c[1] = (ny - 1) / 2.0;
+        p.c[2] = (nz - 1) / 2.0;
+        int m = nx < ny ? nx : ny;
+        m = m < nz ? m : nz;
+        p.radius = m / 2.0;
+        p.r_in = 0.55 * p.radius;
+        p.r_out = 0.80 * p.radius;
+    }
+    long long n = (long long)nx * ny * nz;
+    phantom_kernel<<<grid_for(n, kBlock, 148 * 64), kBlock, 0, s>>>(p, out);
+    return cudaGetLastError();
+}
+
+static int zsplit_for(const Layout &L) {
+    long long nblocks = (long long)L.nb[0] * L.nb[1] * L.nb[2];
+    // aim for ~4 CTAs per SM worth of (block, z-chunk) work items
+    long long want = (148 * 8 + nblocks - 1) / nblocks;
+    int bz = L.bsize < L.n[2] ? L.bsize : L.n[2];
+    if (want > bz) want = bz;
+    if (want < 1) want = 1;
+    return (int)want;
+}
+
+cudaError_t launch_block_minmax(const int16_t *vol, const Layout &L, int *vmin, int *vmax, cudaStream_t s) {
+    int nblocks = L.nb[0] * L.nb[1] * L.nb[2];
+    init_block_minmax_kernel<<<(nblocks + 255) / 256, 256, 0, s>>>(vmin, vmax, nblocks);
+    dim3 grid(nblocks, zsplit_for(L));
+    block_minmax_kernel<<<grid, kBlock, 0, s>>>(vol, L, vmin, vmax);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v, cudaStream_t s) {
+    size_t smem = (size_t)(v.nbins + 1) * sizeof(int);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(vis_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    vis_setup_kernel<<<1, kSetupThreads, smem, s>>>(v);
+    dim3 grid(v.nblocks, zsplit_for(L));
+    aabb_kernel<<<grid, kBlock, 0, s>>>(vol, L, v);
+    box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out, cudaStream_t s) {
+    count_hits_kernel<<<1, 1024, 0, s>>>(hits, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_preclassify(const int16_t *vol, long long n, const double *lut, int nbins, double lut_lo,
+                               double bin_width, uint8_t *rgba, cudaStream_t s) {
+    preclassify_kernel<<<grid_for(n, kBlock, 148 * 64), kBlock, 0, s>>>(vol, n, lut, nbins, lut_lo, bin_width, rgba);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sample_points(const int16_t *vol, int nx, int ny, int nz, const double *pts, long long n,
+                                 int cubic, int gradient, double sx, double sy, double sz, double *out,
+                                 cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    long long g = (n + kBlock - 1) / kBlock;
+    sample_points_kernel<<<(unsigned)g, kBlock, 0, s>>>(vol, nx, ny, nz, pts, n, cubic, gradient, sx, sy, sz, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_threshold_count(const int16_t *vol, long long n, int thr, unsigned long long *count,
+                                   cudaStream_t s) {
+    threshold_kernel<<<grid_for(n / 8 + 1, kBlock, 148 * 8), kBlock, 0, s>>>(vol, n, thr, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ball_counts(const int16_t *vol, int nx, int ny, int nz, double sx, double sy, double sz,
+                               int thr, const double *centres, const double *radii, int nballs,
+                               unsigned long long *counts, unsigned long long *faces, cudaStream_t s) {
+    if (nballs <= 0) return cudaSuccess;
+    ball_kernel<<<nballs, kBlock, 0, s>>>(vol, nx, ny, nz, sx, sy, sz, thr, centres, radii, counts, faces);
+    return cudaGetLastError();
+}
+
+}  // namespace vr

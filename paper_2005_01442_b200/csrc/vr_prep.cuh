@@ -1,0 +1,60 @@
+// vr_prep.cuh -- K1/K2 kernels: volume statistics, synthetic phantoms, block
+// min/max (decompose), transfer-function visibility (cull_empty +
+// fit_bounding_box), preclassification, point sampling and the K4 volume
+// measure.  Launchers return the launch error; all work is stream-ordered.
+#pragma once
+#include "vr_common.cuh"
+
+namespace vr {
+
+// value range of the whole volume (make_volume, volume.py:74-79); out[0]=min, out[1]=max
+cudaError_t launch_value_range(const int16_t *vol, long long n, int *out, cudaStream_t s);
+
+// phantoms.py:98-111 on the device
+cudaError_t launch_phantom(int kind, int nx, int ny, int nz, int16_t *out, cudaStream_t s);
+
+// decompose() min/max (blocks.py:133-145); vmin/vmax int32 [nblocks]
+cudaError_t launch_block_minmax(const int16_t *vol, const Layout &L, int *vmin, int *vmax,
+                                cudaStream_t s);
+
+// Visibility state for one LUT (blocks.py:161-220).
+struct VisArgs {
+    const double *lut;  // (nbins, 4)
+    int nbins;
+    double lut_lo, bin_width;
+    const int *vmin, *vmax;
+    int nblocks;
+    // outputs
+    unsigned int *visbits;   // 65536 bits: int16 value v visible <=> bit (v + 32768)
+    uint8_t *empty;          // nblocks
+    int *aabb;               // nblocks x 6 local min/max (x,y,z) of visible voxels
+    double *box;             // nblocks x 6 render box (global, +- margin)
+    long long *aabb_global;  // optional nblocks x 6 int64 inclusive global aabb (lo xyz, hi xyz)
+    unsigned long long *counters;  // [0] empty blocks, [1] non-empty blocks without a visible voxel
+    double margin;
+};
+cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,
+                              cudaStream_t s);
+
+// blocks_visited = sum(blocks_hit) -> *out (render.py:467)
+cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out, cudaStream_t s);
+
+// preclassify_volume (transfer.py:142-145): 4 planar uint8 channels
+cudaError_t launch_preclassify(const int16_t *vol, long long n, const double *lut, int nbins,
+                               double lut_lo, double bin_width, uint8_t *rgba, cudaStream_t s);
+
+// sample_points / gradient_points (_kernels.py:169-187)
+cudaError_t launch_sample_points(const int16_t *vol, int nx, int ny, int nz, const double *pts,
+                                 long long n, int cubic, int gradient, double sx, double sy,
+                                 double sz, double *out, cudaStream_t s);
+
+// K4: voxels >= thr
+cudaError_t launch_threshold_count(const int16_t *vol, long long n, int thr,
+                                   unsigned long long *count, cudaStream_t s);
+// K4 ball form
+cudaError_t launch_ball_counts(const int16_t *vol, int nx, int ny, int nz, double sx, double sy,
+                               double sz, int thr, const double *centres, const double *radii,
+                               int nballs, unsigned long long *counts, unsigned long long *faces,
+                               cudaStream_t s);
+
+}  // namespace vr

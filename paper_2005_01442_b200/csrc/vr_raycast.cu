@@ -1,0 +1,506 @@
+// vr_raycast.cu -- K3: ray generation, box clipping, empty-space leaping,
+// Catmull-Rom / trilinear sampling, classification, headlight shading and
+// front-to-back compositing with early ray termination, fused with the
+// straight-alpha uint8 epilogue and the stats reduction.
+//
+// Follows _kernels.march (/root/reference/pkg/src/voxelray/_kernels.py:279-594)
+// sample for sample: the n-th sample of a ray sits at t = t0 + (n + 0.5)*step,
+// block attribution is floor((x - 1)/stride), and every taken sample is
+// classified and composited with the reference's float64 operation order.
+// What differs is how skipped samples are found: instead of testing the skip
+// predicate at every step (_kernels.py:377-399), a ray in a skippable region
+// leaps to the last sample that is provably still inside it (cell exit or box
+// entry, shrunk by a 1e-6-voxel guard and one sample), then re-evaluates the
+// exact predicate there.  samples_taken / samples_skipped therefore match the
+// reference exactly while the work per ray is O(cells crossed).
+#include <cfloat>
+#include <climits>
+
+#include "vr_raycast.cuh"
+
+namespace vr {
+namespace {
+
+struct Ray {
+    double ox, oy, oz, dx, dy, dz;
+};
+
+// render.py:125-144 (pinhole) per pixel, or the orthographic variant.
+VR_D Ray make_ray(const RenderArgs &a, int px, int py) {
+    Ray r;
+    double v = (1.0 - 2.0 * ((double)py + 0.5) / (double)a.H) * a.half_h;
+    double u = (2.0 * ((double)px + 0.5) / (double)a.W - 1.0) * a.half_w;
+    if (a.projection == 0) {
+        double d0 = (a.fwd[0] + u * a.right[0]) + v * a.up[0];
+        double d1 = (a.fwd[1] + u * a.right[1]) + v * a.up[1];
+        double d2 = (a.fwd[2] + u * a.right[2]) + v * a.up[2];
+        double nrm = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+        r.dx = d0 / nrm;
+        r.dy = d1 / nrm;
+        r.dz = d2 / nrm;
+        r.ox = a.pos[0];
+        r.oy = a.pos[1];
+        r.oz = a.pos[2];
+    } else {
+        r.ox = (a.pos[0] + u * a.right[0]) + v * a.up[0];
+        r.oy = (a.pos[1] + u * a.right[1]) + v * a.up[1];
+        r.oz = (a.pos[2] + u * a.right[2]) + v * a.up[2];
+        r.dx = a.fwd[0];
+        r.dy = a.fwd[1];
+        r.dz = a.fwd[2];
+    }
+    return r;
+}
+
+// render.py:147-156
+VR_D void clip_to_bounds(const Ray &r, const double ext[3], double &tmin, double &tmax) {
+    const double tiny = 1e-300;
+    double o[3] = {r.ox, r.oy, r.oz};
+    double d[3] = {r.dx, r.dy, r.dz};
+    double lo_max = 0.0, hi_min = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double dd = d[k];
+        if (fabs(dd) < tiny) dd = (dd < 0) ? -tiny : tiny;
+        double lo = (0.0 - o[k]) / dd;
+        double hi = (ext[k] - o[k]) / dd;
+        double mn = lo < hi ? lo : hi;
+        double mx = lo > hi ? lo : hi;
+        if (k == 0 || mn > lo_max) lo_max = mn;
+        if (k == 0 || mx < hi_min) hi_min = mx;
+    }
+    tmin = lo_max > 0.0 ? lo_max : 0.0;
+    tmax = hi_min;
+}
+
+VR_D Brick<int16_t> brick_of(const RenderArgs &a, int bi, int bj, int bk) {
+    int ox = block_origin(a.L, bi), oy = block_origin(a.L, bj), oz = block_origin(a.L, bk);
+    Brick<int16_t> b;
+    b.base = a.vol + (long long)oz * a.L.pz + (long long)oy * a.L.py + ox;
+    b.pz = a.L.pz;
+    b.py = a.L.py;
+    b.ex = block_extent(a.L, 0, bi);
+    b.ey = block_extent(a.L, 1, bj);
+    b.ez = block_extent(a.L, 2, bk);
+    return b;
+}
+
+VR_D int owner_x(const RenderArgs &a, double x) { return owner_block(x, a.L.strided, a.L.inv_stride, a.L.nb[0]); }
+VR_D int owner_y(const RenderArgs &a, double y) { return owner_block(y, a.L.strided, a.L.inv_stride, a.L.nb[1]); }
+VR_D int owner_z(const RenderArgs &a, double z) { return owner_block(z, a.L.strided, a.L.inv_stride, a.L.nb[2]); }
+
+// _attr_sample (_kernels.py:211-233) with the owning block already known.
+VR_D double sample_block(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z) {
+    Brick<int16_t> b = brick_of(a, bi, bj, bk);
+    return sample(b, x - (double)block_origin(a.L, bi), y - (double)block_origin(a.L, bj),
+                  z - (double)block_origin(a.L, bk), a.cubic != 0);
+}
+
+VR_D double attr_sample(const RenderArgs &a, double x, double y, double z) {
+    return sample_block(a, owner_x(a, x), owner_y(a, y), owner_z(a, z), x, y, z);
+}
+
+// _attr_grad (_kernels.py:236-253): each of the six taps attributed to its own
+// block; only the displaced axis can change owner.
+VR_D void attr_grad(const RenderArgs &a, double x, double y, double z, int bi, int bj, int bk,
+                    double &gx, double &gy, double &gz) {
+    const double h = 0.5;
+    double xp = x + h, xm = x - h, yp = y + h, ym = y - h, zp = z + h, zm = z - h;
+    gx = sample_block(a, owner_x(a, xp), bj, bk, xp, y, z) - sample_block(a, owner_x(a, xm), bj, bk, xm, y, z);
+    gy = sample_block(a, bi, owner_y(a, yp), bk, x, yp, z) - sample_block(a, bi, owner_y(a, ym), bk, x, ym, z);
+    gz = sample_block(a, bi, bj, owner_z(a, zp), x, y, zp) - sample_block(a, bi, bj, owner_z(a, zm), x, y, zm);
+    gx = divide(gx, a.dsx);
+    gy = divide(gy, a.dsy);
+    gz = divide(gz, a.dsz);
+}
+
+// _attr_rgba (_kernels.py:256-276)
+VR_D double attr_rgba(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z, int ch) {
+    int ox = block_origin(a.L, bi), oy = block_origin(a.L, bj), oz = block_origin(a.L, bk);
+    Brick<uint8_t> b;
+    b.base = a.rgba + (long long)ch * a.rgba_plane + (long long)oz * a.L.pz + (long long)oy * a.L.py + ox;
+    b.pz = a.L.pz;
+    b.py = a.L.py;
+    b.ex = block_extent(a.L, 0, bi);
+    b.ey = block_extent(a.L, 1, bj);
+    b.ez = block_extent(a.L, 2, bk);
+    double v = sample(b, x - (double)ox, y - (double)oy, z - (double)oz, a.cubic != 0);
+    return clampf(v / 255.0, 0.0, 1.0);
+}
+
+// _kernels.py:190-192
+VR_D int lut_bin(double s, double lo, double inv_w, int nbins) {
+    double q = (s - lo) * inv_w;
+    // int() truncates toward zero; clamp in the float domain to stay in range
+    if (q <= -1.0) return 0;
+    if (q >= (double)nbins) return nbins - 1;
+    return clampi((int)q, 0, nbins - 1);
+}
+
+// _kernels.py:195-208
+VR_D void shade(const RenderArgs &a, double &r, double &g, double &b, double nx, double ny, double nz,
+                double lx, double ly, double lz) {
+    double ndl = (nx * lx + ny * ly) + nz * lz;
+    double diff = a.kd * pymax0(ndl);
+    double rv = 2.0 * ndl * ndl - 1.0;
+    double spec = a.ks * vr_pow(pymax0(rv), a.shin);
+    r = clampf(r * (a.ka + diff) + spec, 0.0, 1.0);
+    g = clampf(g * (a.ka + diff) + spec, 0.0, 1.0);
+    b = clampf(b * (a.ka + diff) + spec, 0.0, 1.0);
+}
+
+VR_D double dmin(double a, double b) { return a < b ? a : b; }
+VR_D double dmax(double a, double b) { return a > b ? a : b; }
+
+// Number k >= 1 of samples, starting at n, that are guaranteed skippable:
+// every sample strictly before the safe parameter t_safe lies (in exact
+// arithmetic) at least 1e-6 voxel inside the current ownership cell and, for
+// a non-empty block, at least 1e-6 voxel outside its visibility box, so the
+// computed positions give the same skip verdict; one extra sample of slack
+// absorbs the rounding of t itself.
+VR_D long long leap_count(const RenderArgs &a, const Ray &r, double t0, long long n, double t,
+                          const double p[3], const int bidx[3], int b, bool cell_only) {
+    const double delta = 1e-6;
+    const double d[3] = {r.dx, r.dy, r.dz};
+    const double o[3] = {r.ox, r.oy, r.oz};
+    const double s[3] = {a.dsx.s, a.dsy.s, a.dsz.s};
+    double t_safe = DBL_MAX;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (d[k] > 0.0 && bidx[k] < a.L.nb[k] - 1) {
+            double X = (1.0 + (double)((bidx[k] + 1) * a.L.stride)) - delta;
+            t_safe = dmin(t_safe, (X * s[k] - o[k]) / d[k]);
+        } else if (d[k] < 0.0 && bidx[k] > 0) {
+            double X = (1.0 + (double)(bidx[k] * a.L.stride)) + delta;
+            t_safe = dmin(t_safe, (X * s[k] - o[k]) / d[k]);
+        }
+    }
+    if (!cell_only) {
+        const double *bx = a.box + 6 * (long long)b;
+        double tin = -DBL_MAX, tout = DBL_MAX;
+        bool never = false;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            double lo = __ldg(bx + k), hi = __ldg(bx + 3 + k);
+            if (d[k] == 0.0) {
+                // the coordinate is exactly constant along the ray
+                if (p[k] < lo || p[k] > hi) never = true;
+            } else {
+                double ta = ((lo - delta) * s[k] - o[k]) / d[k];
+                double tb = ((hi + delta) * s[k] - o[k]) / d[k];
+                tin = dmax(tin, dmin(ta, tb));
+                tout = dmin(tout, dmax(ta, tb));
+            }
+        }
+        if (!never && tin <= tout && tout >= t) t_safe = (tin > t) ? dmin(t_safe, tin) : t;
+    }
+    if (!(t_safe > t)) return 1;
+    double q = (t_safe - t0) / a.step - 0.5;
+    if (q > 4.0e15) return LLONG_MAX / 4;
+    long long m = (long long)floor(q) - 1;
+    long long k = m - n + 1;
+    return k < 1 ? 1 : k;
+}
+
+struct RayResult {
+    double r, g, b, a;
+    double depth;
+    long long taken, skipped, shaded;
+};
+
+// One pixel of _kernels.march (:343-594).
+VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
+    RayResult res;
+    double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
+    long long n_taken = 0, n_skip = 0, n_shaded = 0;
+    double depth = __longlong_as_double(0x7ff8000000000000LL);  // NaN
+    if (t1 >= t0) {
+        const double step = a.step;
+        long long nsteps = (long long)ceil((t1 - t0) / step);
+        if (nsteps < 1) nsteps = 1;
+        // the reference breaks at the first t > t1; t(n) is monotone in n, so
+        // the samples it visits are exactly the prefix [0, N)
+        long long N = nsteps;
+        while (N > 0 && (t0 + ((double)(N - 1) + 0.5) * step) > t1) --N;
+        const int nbx = a.L.nb[0], nby = a.L.nb[1];
+        const bool iso = a.mode == 1;
+        double prev_s = 0.0;
+        bool prev_valid = false, prev_skippable = false;
+        int last_hit = -1;
+        long long n = 0;
+        while (n < N) {
+            double t = t0 + ((double)n + 0.5) * step;
+            double x = divide(r.ox + t * r.dx, a.dsx);
+            double y = divide(r.oy + t * r.dy, a.dsy);
+            double z = divide(r.oz + t * r.dz, a.dsz);
+            int bi = owner_x(a, x), bj = owner_y(a, y), bk = owner_z(a, z);
+            int b = (bk * nby + bj) * nbx + bi;
+
+            bool skippable = false;
+            bool cell_only = true;
+            if (a.skip_empty) {
+                if (iso) {
+                    skippable = (double)__ldg(a.vmax + b) < a.isovalue || (double)__ldg(a.vmin + b) > a.isovalue;
+                } else if (__ldg(a.empty + b) == 1) {
+                    skippable = true;
+                } else {
+                    const double *bx = a.box + 6 * (long long)b;
+                    skippable = x < __ldg(bx) || x > __ldg(bx + 3) || y < __ldg(bx + 1) ||
+                                y > __ldg(bx + 4) || z < __ldg(bx + 2) || z > __ldg(bx + 5);
+                    cell_only = false;
+                }
+            }
+            if (skippable && (prev_skippable || !a.chained)) {
+                const double p[3] = {x, y, z};
+                const int bidx[3] = {bi, bj, bk};
+                long long k = leap_count(a, r, t0, n, t, p, bidx, b, cell_only);
+                long long m = (N - n < k) ? N : n + k;
+                n_skip += m - n;
+                n = m;
+                prev_valid = false;
+                prev_skippable = true;
+                continue;
+            }
+            prev_skippable = skippable;
+            if (b != last_hit) {
+                if (a.blocks_hit) a.blocks_hit[b] = 1;
+                last_hit = b;
+            }
+            n_taken += 1;
+
+            if (iso) {
+                // _kernels.py:405-468
+                double s = sample_block(a, bi, bj, bk, x, y, z);
+                if (!prev_valid && n > 0) {
+                    double tp = t - step;
+                    prev_s = attr_sample(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
+                                         divide(r.oz + tp * r.dz, a.dsz));
+                    prev_valid = true;
+                }
+                bool hit = false;
+                double t_hit = t;
+                if (prev_valid && (prev_s - a.isovalue) * (s - a.isovalue) < 0.0) {
+                    double lo_t = t - step, hi_t = t, lo_s = prev_s;
+                    for (int it = 0; it < 8; ++it) {
+                        double mid = 0.5 * (lo_t + hi_t);
+                        double ms = attr_sample(a, divide(r.ox + mid * r.dx, a.dsx),
+                                                divide(r.oy + mid * r.dy, a.dsy),
+                                                divide(r.oz + mid * r.dz, a.dsz));
+                        if ((lo_s - a.isovalue) * (ms - a.isovalue) <= 0.0) {
+                            hi_t = mid;
+                        } else {
+                            lo_t = mid;
+                            lo_s = ms;
+                        }
+                    }
+                    t_hit = 0.5 * (lo_t + hi_t);
+                    hit = true;
+                } else if (s == a.isovalue) {
+                    hit = true;
+                }
+                if (hit) {
+                    double hx = divide(r.ox + t_hit * r.dx, a.dsx);
+                    double hy = divide(r.oy + t_hit * r.dy, a.dsy);
+                    double hz = divide(r.oz + t_hit * r.dz, a.dsz);
+                    int ib = lut_bin(a.isovalue, a.lut_lo, a.lut_inv_w, a.nlut);
+                    double cr = __ldg(a.lut + 4 * ib), cg = __ldg(a.lut + 4 * ib + 1), cb = __ldg(a.lut + 4 * ib + 2);
+                    double gx, gy, gz;
+                    attr_grad(a, hx, hy, hz, owner_x(a, hx), owner_y(a, hy), owner_z(a, hz), gx, gy, gz);
+                    n_shaded += 1;
+                    double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                    if (a.lighting && norm > 1e-12)
+                        shade(a, cr, cg, cb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                    acc_r = cr;
+                    acc_g = cg;
+                    acc_b = cb;
+                    acc_a = 1.0;
+                    depth = t_hit;
+                    break;
+                }
+                prev_s = s;
+                prev_valid = true;
+                ++n;
+                continue;
+            }
+
+            if (a.classify == 1) {
+                // pre-classified (_kernels.py:471-507)
+                double sa = attr_rgba(a, bi, bj, bk, x, y, z, 3);
+                if (sa > 0.0) {
+                    double sr = attr_rgba(a, bi, bj, bk, x, y, z, 0);
+                    double sg = attr_rgba(a, bi, bj, bk, x, y, z, 1);
+                    double sb = attr_rgba(a, bi, bj, bk, x, y, z, 2);
+                    double ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
+                    if (a.lighting) {
+                        double gx, gy, gz;
+                        attr_grad(a, x, y, z, bi, bj, bk, gx, gy, gz);
+                        n_shaded += 1;
+                        double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                        if (norm > 1e-12)
+                            shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                    }
+                    double w = (1.0 - acc_a) * ahat;
+                    acc_r += w * sr;
+                    acc_g += w * sg;
+                    acc_b += w * sb;
+                    acc_a += w;
+                    if (acc_a >= a.term_alpha) break;
+                }
+            } else if (a.classify == 0) {
+                // post-classified (_kernels.py:508-537)
+                double s = sample_block(a, bi, bj, bk, x, y, z);
+                int sbin = lut_bin(s, a.lut_lo, a.lut_inv_w, a.nlut);
+                double sa = __ldg(a.lut + 4 * sbin + 3);
+                if (sa > 0.0) {
+                    double sr = __ldg(a.lut + 4 * sbin), sg = __ldg(a.lut + 4 * sbin + 1), sb = __ldg(a.lut + 4 * sbin + 2);
+                    double ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
+                    if (a.lighting) {
+                        double gx, gy, gz;
+                        attr_grad(a, x, y, z, bi, bj, bk, gx, gy, gz);
+                        n_shaded += 1;
+                        double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                        if (norm > 1e-12)
+                            shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                    }
+                    double w = (1.0 - acc_a) * ahat;
+                    acc_r += w * sr;
+                    acc_g += w * sg;
+                    acc_b += w * sb;
+                    acc_a += w;
+                    if (acc_a >= a.term_alpha) break;
+                }
+            } else {
+                // pre-integrated (_kernels.py:538-581)
+                double s = sample_block(a, bi, bj, bk, x, y, z);
+                if (!prev_valid && n > 0) {
+                    double tp = t - step;
+                    prev_s = attr_sample(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
+                                         divide(r.oz + tp * r.dz, a.dsz));
+                    prev_valid = true;
+                }
+                double sf = prev_valid ? prev_s : s;
+                int fbin = lut_bin(sf, a.tbl_lo, a.tbl_inv_w, a.ntbl);
+                int bbin = lut_bin(s, a.tbl_lo, a.tbl_inv_w, a.ntbl);
+                const double *cell = a.table + 4 * ((long long)fbin * a.ntbl + bbin);
+                double seg_a = __ldg(cell + 3);
+                if (seg_a > 0.0) {
+                    double seg_r = __ldg(cell), seg_g = __ldg(cell + 1), seg_b = __ldg(cell + 2);
+                    if (a.lighting) {
+                        double gx, gy, gz;
+                        attr_grad(a, x, y, z, bi, bj, bk, gx, gy, gz);
+                        n_shaded += 1;
+                        double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                        if (norm > 1e-12) {
+                            double ndl = fabs(((gx * -r.dx + gy * -r.dy) + gz * -r.dz) / norm);
+                            double scale = a.ka + a.kd * ndl;
+                            double spec = a.ks * vr_pow(ndl, a.shin) * seg_a;
+                            seg_r = clampf(scale * seg_r + spec, 0.0, 1.0);
+                            seg_g = clampf(scale * seg_g + spec, 0.0, 1.0);
+                            seg_b = clampf(scale * seg_b + spec, 0.0, 1.0);
+                        }
+                    }
+                    double w = 1.0 - acc_a;
+                    acc_r += w * seg_r;
+                    acc_g += w * seg_g;
+                    acc_b += w * seg_b;
+                    acc_a += w * seg_a;
+                    if (acc_a >= a.term_alpha) break;
+                }
+                prev_s = s;
+                prev_valid = true;
+            }
+            ++n;
+        }
+    }
+    // composite over the background (_kernels.py:583-588)
+    double w = 1.0 - acc_a;
+    acc_r += w * a.bg[0] * a.bg[3];
+    acc_g += w * a.bg[1] * a.bg[3];
+    acc_b += w * a.bg[2] * a.bg[3];
+    acc_a += w * a.bg[3];
+    res.r = acc_r;
+    res.g = acc_g;
+    res.b = acc_b;
+    res.a = acc_a;
+    res.depth = depth;
+    res.taken = n_taken;
+    res.skipped = n_skip;
+    res.shaded = n_shaded;
+    return res;
+}
+
+// render.py:454-459: straight = premult / max(alpha, 1e-12) where alpha > 0,
+// rint(clip(.,0,1) * 255) with round-half-even.
+VR_D unsigned char to_u8(double v) { return (unsigned char)rint(clampf(v, 0.0, 1.0) * 255.0); }
+
+VR_D unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(kThreads) raycast_kernel(const __grid_constant__ RenderArgs a) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lx = (warp & 1) * 8 + (lane & 7);   // 0..15 inside the cell
+    const int ly = (warp >> 1) * 4 + (lane >> 3);  // 0..7
+    const int slot = blockIdx.x;
+    const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
+    const int cx = (cell % a.cells_x) * kTileW + lx;
+    const int cy = (cell / a.cells_x) * kTileH + ly;
+    const bool active = cell < a.ncells && cx < a.tw && cy < a.th;
+    unsigned long long taken = 0, skipped = 0, shaded = 0;
+    if (active) {
+        Ray r = make_ray(a, a.tx + cx, a.ty + cy);
+        double t0, t1;
+        clip_to_bounds(r, a.ext_mm, t0, t1);
+        RayResult res = march(a, r, t0, t1);
+        const long long p = a.il_n > 1 ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx
+                                        : (long long)cy * a.tw + cx;
+        if (a.premult) {
+            double4 *o = reinterpret_cast<double4 *>(a.premult) + p;
+            o->x = res.r;
+            o->y = res.g;
+            o->z = res.b;
+            o->w = res.a;
+        }
+        if (a.pixels) {
+            double alpha = res.a;
+            double r0 = 0.0, g0 = 0.0, b0 = 0.0;
+            if (alpha > 0.0) {
+                double den = alpha > 1e-12 ? alpha : 1e-12;
+                r0 = res.r / den;
+                g0 = res.g / den;
+                b0 = res.b / den;
+            }
+            uchar4 px = make_uchar4(to_u8(r0), to_u8(g0), to_u8(b0), to_u8(alpha));
+            reinterpret_cast<uchar4 *>(a.pixels)[p] = px;
+        }
+        if (a.depth) a.depth[p] = res.depth;
+        if (a.taken) a.taken[p] = res.taken;
+        if (a.skipped) a.skipped[p] = res.skipped;
+        taken = (unsigned long long)res.taken;
+        skipped = (unsigned long long)res.skipped;
+        shaded = (unsigned long long)res.shaded;
+    }
+    taken = warp_sum(taken);
+    skipped = warp_sum(skipped);
+    shaded = warp_sum(shaded);
+    if (lane == 0) {
+        if (a.totals && (taken | skipped)) {
+            atomicAdd(a.totals, taken);
+            atomicAdd(a.totals + 1, skipped);
+        }
+        if (a.shaded && shaded) atomicAdd(a.shaded, shaded);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
+    if (a.tw <= 0 || a.th <= 0) return cudaSuccess;
+    if (a.slots <= 0) return cudaSuccess;
+    raycast_kernel<<<a.slots, kThreads, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace vr

@@ -1,0 +1,61 @@
+// vr_raycast.cuh -- arguments of the K3 ray-cast kernel (host + device view).
+#pragma once
+#include "vr_common.cuh"
+
+namespace vr {
+
+struct RenderArgs {
+    // volume and its block layout (monolithic = one block spanning the volume)
+    const int16_t *vol;
+    Layout L;
+    Divisor dsx, dsy, dsz;  // spacing divisors (x = (o + t*d) / s)
+    double ext_mm[3];       // (n-1)*s, volume.py:62-67
+
+    // camera (render.py:125-156 or the orthographic variant)
+    int projection, W, H, tx, ty, tw, th;
+    int il_n, il_k;        // sort-first interleave: render cells c % il_n == il_k
+    int cells_x, ncells;   // 16x8 cells across the rectangle, total
+    int slots;             // CTAs launched (cells rendered by this call)
+    double pos[3], fwd[3], right[3], up[3];
+    double half_w, half_h;
+
+    // settings (render.py:361-425 resolved)
+    double step, ref_step;
+    PowSpec corr, shin;
+    int mode, cubic, lighting, classify, skip_empty, chained;
+    double isovalue, term_alpha, ka, kd, ks;
+    double bg[4];
+    const double *lut;
+    int nlut;
+    double lut_lo, lut_inv_w;
+    const double *table;
+    int ntbl;
+    double tbl_lo, tbl_inv_w;
+    const uint8_t *rgba;     // 4 planar (nz,ny,nx) uint8 channels (pre-classification)
+    long long rgba_plane;    // elements per channel plane
+
+    // block classification (K2 outputs; unused when skip_empty == 0)
+    const uint8_t *empty;    // nblocks
+    const double *box;       // nblocks x 6: lo xyz (aabb_lo - margin), hi xyz (aabb_hi + margin)
+    const int *vmin, *vmax;  // nblocks (iso skip predicate)
+
+    // outputs (all optional)
+    uint8_t *pixels;
+    double *premult;
+    double *depth;
+    long long *taken, *skipped;
+    uint8_t *blocks_hit;
+    unsigned long long *totals;  // [0] taken, [1] skipped
+    unsigned long long *shaded;  // [0] gradient evaluations
+};
+
+// CTA = 16 x 8 pixels, four warps, each warp an 8 x 4 screen tile so that the
+// rays of a warp stay spatially coherent (SIMT efficiency 0.80 for
+// 8x4 tiles vs 0.59 for row-major warps).
+constexpr int kTileW = 16;
+constexpr int kTileH = 8;
+constexpr int kThreads = 128;
+
+cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream);
+
+}  // namespace vr

@@ -1,0 +1,118 @@
+"""Sort-first multi-GPU rendering: interleaved 16x8 cells per rank, one gather.
+
+The frame is cut into 16x8-pixel cells numbered row-major; rank k of n renders
+cells c with c % n == k (the kernel's interleave mode, include/voxelray_b200.h)
+into a packed buffer of ceil(ncells / n) cells, identical in size on every
+rank.  The volume is replicated (one copy per GPU; 1 GiB at the largest
+config vs 180 GB of HBM).  The only exchange is the gather of the packed
+uint8 cells to rank 0 (NCCL over NVLink on the GPU box, gloo in the CPU
+tests), where ``unpack_cells`` restores the row-major frame.  Pixels are
+independent (reference SPEC.md:354, _kernels.py:13-14), so the gathered frame
+equals the single-GPU frame bit for bit.
+"""
+
+from __future__ import annotations
+
+import math
+
+CELL_W, CELL_H = 16, 8
+
+
+def cell_grid(width: int, height: int):
+    """(cells_x, cells_y) covering a width x height rectangle."""
+    return math.ceil(width / CELL_W), math.ceil(height / CELL_H)
+
+
+def cells_per_rank(width: int, height: int, n: int) -> int:
+    cx, cy = cell_grid(width, height)
+    return math.ceil(cx * cy / n)
+
+
+def rank_cells(width: int, height: int, n: int, k: int) -> list[int]:
+    """Cell indices rendered by rank k of n, in packed order."""
+    cx, cy = cell_grid(width, height)
+    return list(range(k, cx * cy, n))
+
+
+def cell_rect(width: int, height: int, c: int):
+    """(x0, y0, w, h) of cell c clipped to the frame."""
+    cx, _ = cell_grid(width, height)
+    x0, y0 = (c % cx) * CELL_W, (c // cx) * CELL_H
+    return x0, y0, min(CELL_W, width - x0), min(CELL_H, height - y0)
+
+
+def pack_cells(frame, n: int, k: int):
+    """What rank k's packed buffer holds for a (H, W, C) frame (torch or numpy):
+    shape (cells_per_rank * 128, C), cells beyond the frame left zero."""
+    H, W, C = frame.shape
+    slots = cells_per_rank(W, H, n)
+    out = frame.new_zeros((slots * CELL_H * CELL_W, C)) if hasattr(frame, "new_zeros") else \
+        __import__("numpy").zeros((slots * CELL_H * CELL_W, C), dtype=frame.dtype)
+    for s, c in enumerate(rank_cells(W, H, n, k)):
+        x0, y0, w, h = cell_rect(W, H, c)
+        block = out[s * 128:(s + 1) * 128].reshape(CELL_H, CELL_W, C)
+        block[:h, :w] = frame[y0:y0 + h, x0:x0 + w]
+    return out
+
+
+def unpack_cells(gathered, width: int, height: int):
+    """Reassemble the frame from the n packed rank buffers.
+
+    gathered: torch tensor (n, slots * 128, C) in rank order.  Returns (H, W, C).
+    """
+    n, per, C = gathered.shape
+    slots = per // (CELL_W * CELL_H)
+    cx, cy = cell_grid(width, height)
+    # slot s of rank k holds cell s * n + k
+    cells = gathered.reshape(n, slots, CELL_H, CELL_W, C).transpose(0, 1).reshape(n * slots, CELL_H, CELL_W, C)
+    cells = cells[: cx * cy].reshape(cy, cx, CELL_H, CELL_W, C)
+    frame = cells.permute(0, 2, 1, 3, 4).reshape(cy * CELL_H, cx * CELL_W, C)
+    return frame[:height, :width]
+
+
+def gather_frame(packed, width: int, height: int, group=None):
+    """Gather every rank's packed cells to rank 0 and unpack there.
+
+    packed: (slots * 128, C) tensor on this rank's device (CUDA for NCCL, CPU
+    for gloo).  Returns the (H, W, C) frame on rank 0, None elsewhere.
+    """
+    import torch
+    import torch.distributed as dist
+
+    n = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if n == 1:
+        return unpack_cells(packed.unsqueeze(0), width, height)
+    if rank == 0:
+        bufs = [torch.empty_like(packed) for _ in range(n)]
+        dist.gather(packed, gather_list=bufs, dst=0, group=group)
+        return unpack_cells(torch.stack(bufs), width, height)
+    dist.gather(packed, gather_list=None, dst=0, group=group)
+    return None
+
+
+def render_sharded(volume, camera, tf, settings, *, group=None, device=None):
+    """Multi-GPU render of one frame: every rank calls this with the same
+    arguments; rank 0 returns the (H, W, 4) uint8 frame as a host array and
+    the summed stats, other ranks return (None, stats)."""
+    import torch
+    import torch.distributed as dist
+
+    from .render import Renderer
+
+    n = dist.get_world_size(group) if dist.is_initialized() else 1
+    k = dist.get_rank(group) if dist.is_initialized() else 0
+    dev = torch.cuda.current_device() if device is None else device
+    r = Renderer(volume, camera, tf, settings, device=dev, interleave=(n, k) if n > 1 else None)
+    r.render_async()
+    packed = r.pixels.reshape(-1, 4)
+    totals = r.totals[:2].clone()
+    if n > 1:
+        dist.all_reduce(totals, group=group)
+        frame = gather_frame(packed, camera.width, camera.height, group)
+    else:
+        frame = r.pixels
+    stats = totals.cpu().tolist()
+    if frame is None:
+        return None, stats
+    return frame.cpu().numpy(), stats
