@@ -376,7 +376,8 @@ struct VisScratch {
         off_box = (off_box + 15) & ~size_t(15);
         size_t off_glob = off_box + (size_t)nb * 6 * 8;
         size_t off_cnt = off_glob + (want_global ? (size_t)nb * 6 * 8 : 0);
-        size_t total = off_cnt + 2 * 8;
+        size_t off_uni = off_cnt + 2 * 8;
+        size_t total = off_uni + 6 * 4;
         cudaError_t e = mem.alloc(total);
         if (e != cudaSuccess) return e;
         char *base = (char *)mem.p;
@@ -393,6 +394,7 @@ struct VisScratch {
         v.box = (double *)(base + off_box);
         v.aabb_global = want_global ? (long long *)(base + off_glob) : nullptr;
         v.counters = (unsigned long long *)(base + off_cnt);
+        v.uni = (int *)(base + off_uni);
         v.margin = margin;
         return cudaSuccess;
     }
@@ -511,6 +513,8 @@ static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
     a.tbl_inv_w = (double)a.ntbl / (prm->lut_hi - prm->lut_lo);  // render.py:425
     a.rgba = rgba;
     a.rgba_plane = vol->nx * vol->ny * vol->nz;
+    a.margin = prm->margin;
+    a.inv_step = 1.0 / prm->step;
     return VR_OK;
 }
 
@@ -539,6 +543,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.box = vs.v.box;
         a.vmin = grid->vmin;
         a.vmax = grid->vmax;
+        a.uni = vs.v.uni;
     }
     if (out->ev_start) VR_CUDA(cudaEventRecord((cudaEvent_t)out->ev_start, s));
     VR_CUDA(vr::launch_raycast(a, s));

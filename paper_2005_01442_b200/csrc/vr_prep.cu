@@ -139,22 +139,23 @@ __global__ void __launch_bounds__(kBlock) block_minmax_kernel(const int16_t *__r
     block_coords(L, b, bi, bj, bk);
     int ox = block_origin(L, bi), oy = block_origin(L, bj), oz = block_origin(L, bk);
     int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj), ez = block_extent(L, 2, bk);
-    int z0 = (int)((long long)ez * blockIdx.y / gridDim.y);
-    int z1 = (int)((long long)ez * (blockIdx.y + 1) / gridDim.y);
-    long long cnt = (long long)(z1 - z0) * ey * ex;
     int lo = INT_MAX, hi = INT_MIN;
-    for (long long i = threadIdx.x; i < cnt; i += blockDim.x) {
-        int x = (int)(i % ex);
-        long long r = i / ex;
-        int y = (int)(r % ey);
-        int z = z0 + (int)(r / ey);
-        int v = __ldg(vol + (long long)(oz + z) * L.pz + (long long)(oy + y) * L.py + ox + x);
-        lo = min(lo, v);
-        hi = max(hi, v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // one z-slice per CTA row of the grid; each warp walks rows x-contiguously
+    for (int z = blockIdx.y; z < ez; z += gridDim.y) {
+        const int16_t *plane = vol + (long long)(oz + z) * L.pz + (long long)oy * L.py + ox;
+        for (int y = wid; y < ey; y += nw) {
+            const int16_t *row = plane + (long long)y * L.py;
+            for (int x = lane; x < ex; x += 32) {
+                int v = __ldg(row + x);
+                lo = min(lo, v);
+                hi = max(hi, v);
+            }
+        }
     }
     lo = warp_min(lo);
     hi = warp_max(hi);
-    if ((threadIdx.x & 31) == 0 && cnt > 0) {
+    if (lane == 0 && lo <= hi) {
         atomicMin(vmin + b, lo);
         atomicMax(vmax + b, hi);
     }
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
         v.counters[0] = n_empty;
         v.counters[1] = 0;
     }
+    if (tid < 6) v.uni[tid] = tid < 3 ? INT_MAX : INT_MIN;
 }
 
 // fit_bounding_box (blocks.py:176-199): local min/max of visible voxels
@@ -252,21 +254,20 @@ __global__ void __launch_bounds__(kBlock) aabb_kernel(const int16_t *__restrict_
     block_coords(L, b, bi, bj, bk);
     int ox = block_origin(L, bi), oy = block_origin(L, bj), oz = block_origin(L, bk);
     int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj), ez = block_extent(L, 2, bk);
-    int z0 = (int)((long long)ez * blockIdx.y / gridDim.y);
-    int z1 = (int)((long long)ez * (blockIdx.y + 1) / gridDim.y);
-    long long cnt = (long long)(z1 - z0) * ey * ex;
     int mnx = INT_MAX, mny = INT_MAX, mnz = INT_MAX, mxx = -1, mxy = -1, mxz = -1;
-    for (long long i = threadIdx.x; i < cnt; i += blockDim.x) {
-        int x = (int)(i % ex);
-        long long r = i / ex;
-        int y = (int)(r % ey);
-        int z = z0 + (int)(r / ey);
-        int val = __ldg(vol + (long long)(oz + z) * L.pz + (long long)(oy + y) * L.py + ox + x);
-        unsigned int u = (unsigned int)(val + 32768);
-        if ((bits[u >> 5] >> (u & 31)) & 1u) {
-            mnx = min(mnx, x); mxx = max(mxx, x);
-            mny = min(mny, y); mxy = max(mxy, y);
-            mnz = min(mnz, z); mxz = max(mxz, z);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int z = blockIdx.y; z < ez; z += gridDim.y) {
+        const int16_t *plane = vol + (long long)(oz + z) * L.pz + (long long)oy * L.py + ox;
+        for (int y = wid; y < ey; y += nw) {
+            const int16_t *row = plane + (long long)y * L.py;
+            for (int x = lane; x < ex; x += 32) {
+                unsigned int u = (unsigned int)(__ldg(row + x) + 32768);
+                if ((bits[u >> 5] >> (u & 31)) & 1u) {
+                    mnx = min(mnx, x); mxx = max(mxx, x);
+                    mny = min(mny, y); mxy = max(mxy, y);
+                    mnz = min(mnz, z); mxz = max(mxz, z);
+                }
+            }
         }
     }
     mnx = warp_min(mnx); mny = warp_min(mny); mnz = warp_min(mnz);
@@ -304,6 +305,10 @@ __global__ void box_kernel(const Layout L, const VisArgs v) {
         if (v.aabb_global) {
             v.aabb_global[6 * b + k] = lo;
             v.aabb_global[6 * b + 3 + k] = hi;
+        }
+        if (fitted) {
+            atomicMin(v.uni + k, (int)lo);
+            atomicMax(v.uni + 3 + k, (int)hi);
         }
     }
 }
@@ -503,13 +508,9 @@ cudaError_t launch_phantom(int kind, int nx, int ny, int nz, int16_t *out, cudaS
 }
 
 static int zsplit_for(const Layout &L) {
-    long long nblocks = (long long)L.nb[0] * L.nb[1] * L.nb[2];
-    // aim for ~4 CTAs per SM worth of (block, z-chunk) work items
-    long long want = (148 * 8 + nblocks - 1) / nblocks;
+    // one z-slice of a block per CTA (blocks skipped by the kernel exit at once)
     int bz = L.bsize < L.n[2] ? L.bsize : L.n[2];
-    if (want > bz) want = bz;
-    if (want < 1) want = 1;
-    return (int)want;
+    return bz < 1 ? 1 : (bz > 65535 ? 65535 : bz);
 }
 
 cudaError_t launch_block_minmax(const int16_t *vol, const Layout &L, int *vmin, int *vmax, cudaStream_t s) {

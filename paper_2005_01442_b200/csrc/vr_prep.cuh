@@ -31,6 +31,7 @@ struct VisArgs {
     double *box;             // nblocks x 6 render box (global, +- margin)
     long long *aabb_global;  // optional nblocks x 6 int64 inclusive global aabb (lo xyz, hi xyz)
     unsigned long long *counters;  // [0] empty blocks, [1] non-empty blocks without a visible voxel
+    int *uni;                // 6: union of the fitted global AABBs (lo xyz, hi xyz)
     double margin;
 };
 cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,

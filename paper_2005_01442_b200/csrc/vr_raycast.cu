@@ -9,10 +9,17 @@
 // classified and composited with the reference's float64 operation order.
 // What differs is how skipped samples are found: instead of testing the skip
 // predicate at every step (_kernels.py:377-399), a ray in a skippable region
-// leaps to the last sample that is provably still inside it (cell exit or box
-// entry, shrunk by a 1e-6-voxel guard and one sample), then re-evaluates the
-// exact predicate there.  samples_taken / samples_skipped therefore match the
-// reference exactly while the work per ray is O(cells crossed).
+// leaps to the last sample that is provably still inside it -- the exit of its
+// ownership cell, the entry of the block's visibility box, or the entry of the
+// union of all visibility boxes, each shrunk by a 1e-6-voxel guard and one
+// sample -- then re-evaluates the exact predicate there.  samples_taken /
+// samples_skipped therefore match the reference exactly while the work per
+// ray is O(cells crossed near visible matter).
+//
+// The kernel is specialised per (mode/classification, interpolation,
+// lighting, leaping) so each instantiation carries only its own path: one
+// kernel holding every branch spilled the instruction cache (ncu: 16% of warp
+// samples stalled on no_instructions) and needed 154 registers.
 #include <cfloat>
 #include <climits>
 
@@ -20,6 +27,8 @@
 
 namespace vr {
 namespace {
+
+enum Kind { kPost = 0, kPre = 1, kPreint = 2, kIso = 3 };
 
 struct Ray {
     double ox, oy, oz, dx, dy, dz;
@@ -55,8 +64,8 @@ VR_D Ray make_ray(const RenderArgs &a, int px, int py) {
 // render.py:147-156
 VR_D void clip_to_bounds(const Ray &r, const double ext[3], double &tmin, double &tmax) {
     const double tiny = 1e-300;
-    double o[3] = {r.ox, r.oy, r.oz};
-    double d[3] = {r.dx, r.dy, r.dz};
+    const double o[3] = {r.ox, r.oy, r.oz};
+    const double d[3] = {r.dx, r.dy, r.dz};
     double lo_max = 0.0, hi_min = 0.0;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -73,58 +82,69 @@ VR_D void clip_to_bounds(const Ray &r, const double ext[3], double &tmin, double
     tmax = hi_min;
 }
 
-VR_D Brick<int16_t> brick_of(const RenderArgs &a, int bi, int bj, int bk) {
-    int ox = block_origin(a.L, bi), oy = block_origin(a.L, bj), oz = block_origin(a.L, bk);
-    Brick<int16_t> b;
-    b.base = a.vol + (long long)oz * a.L.pz + (long long)oy * a.L.py + ox;
+VR_D int owner(const RenderArgs &a, int axis, double v) {
+    return owner_block(v, a.L.strided, a.L.inv_stride, a.L.nb[axis]);
+}
+
+// _attr_sample (_kernels.py:211-233) with the owning block already known:
+// local coordinates x - origin, taps clamped to the block, voxels read in
+// place from the volume (the atlas copy holds the same voxels).
+template <bool CUBIC, class T>
+VR_D double sample_in(const T *vol, const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z) {
+    const int ox = block_origin(a.L, bi), oy = block_origin(a.L, bj), oz = block_origin(a.L, bk);
+    Brick<T> b;
+    b.base = vol + (long long)oz * a.L.pz + (long long)oy * a.L.py + ox;
     b.pz = a.L.pz;
     b.py = a.L.py;
     b.ex = block_extent(a.L, 0, bi);
     b.ey = block_extent(a.L, 1, bj);
     b.ez = block_extent(a.L, 2, bk);
-    return b;
+    const double lx = x - (double)ox, ly = y - (double)oy, lz = z - (double)oz;
+    return CUBIC ? cub_sample(b, lx, ly, lz) : tri_sample(b, lx, ly, lz);
 }
 
-VR_D int owner_x(const RenderArgs &a, double x) { return owner_block(x, a.L.strided, a.L.inv_stride, a.L.nb[0]); }
-VR_D int owner_y(const RenderArgs &a, double y) { return owner_block(y, a.L.strided, a.L.inv_stride, a.L.nb[1]); }
-VR_D int owner_z(const RenderArgs &a, double z) { return owner_block(z, a.L.strided, a.L.inv_stride, a.L.nb[2]); }
-
-// _attr_sample (_kernels.py:211-233) with the owning block already known.
-VR_D double sample_block(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z) {
-    Brick<int16_t> b = brick_of(a, bi, bj, bk);
-    return sample(b, x - (double)block_origin(a.L, bi), y - (double)block_origin(a.L, bj),
-                  z - (double)block_origin(a.L, bk), a.cubic != 0);
-}
-
+template <bool CUBIC>
 VR_D double attr_sample(const RenderArgs &a, double x, double y, double z) {
-    return sample_block(a, owner_x(a, x), owner_y(a, y), owner_z(a, z), x, y, z);
+    return sample_in<CUBIC>(a.vol, a, owner(a, 0, x), owner(a, 1, y), owner(a, 2, z), x, y, z);
 }
 
-// _attr_grad (_kernels.py:236-253): each of the six taps attributed to its own
-// block; only the displaced axis can change owner.
-VR_D void attr_grad(const RenderArgs &a, double x, double y, double z, int bi, int bj, int bk,
-                    double &gx, double &gy, double &gz) {
-    const double h = 0.5;
-    double xp = x + h, xm = x - h, yp = y + h, ym = y - h, zp = z + h, zm = z - h;
-    gx = sample_block(a, owner_x(a, xp), bj, bk, xp, y, z) - sample_block(a, owner_x(a, xm), bj, bk, xm, y, z);
-    gy = sample_block(a, bi, owner_y(a, yp), bk, x, yp, z) - sample_block(a, bi, owner_y(a, ym), bk, x, ym, z);
-    gz = sample_block(a, bi, bj, owner_z(a, zp), x, y, zp) - sample_block(a, bi, bj, owner_z(a, zm), x, y, zm);
-    gx = divide(gx, a.dsx);
-    gy = divide(gy, a.dsy);
-    gz = divide(gz, a.dsz);
+// _attr_grad (_kernels.py:236-253): six taps at +-0.5 voxel, each attributed
+// to its own block (only the displaced axis can change owner), then / spacing.
+// One loop body so the interpolant is instantiated once for all six.
+template <bool CUBIC>
+VR_D void attr_grad(const RenderArgs &a, double x, double y, double z, int bi, int bj, int bk, double g[3]) {
+    double plus = 0.0;
+#pragma unroll 1
+    for (int q = 0; q < 6; ++q) {
+        const int axis = q >> 1;
+        const double h = (q & 1) ? -0.5 : 0.5;
+        double px = x, py = y, pz = z;
+        int qi = bi, qj = bj, qk = bk;
+        if (axis == 0) {
+            px = x + h;
+            qi = owner(a, 0, px);
+        } else if (axis == 1) {
+            py = y + h;
+            qj = owner(a, 1, py);
+        } else {
+            pz = z + h;
+            qk = owner(a, 2, pz);
+        }
+        double s = sample_in<CUBIC>(a.vol, a, qi, qj, qk, px, py, pz);
+        if (q & 1)
+            g[axis] = plus - s;
+        else
+            plus = s;
+    }
+    g[0] = divide(g[0], a.dsx);
+    g[1] = divide(g[1], a.dsy);
+    g[2] = divide(g[2], a.dsz);
 }
 
 // _attr_rgba (_kernels.py:256-276)
+template <bool CUBIC>
 VR_D double attr_rgba(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z, int ch) {
-    int ox = block_origin(a.L, bi), oy = block_origin(a.L, bj), oz = block_origin(a.L, bk);
-    Brick<uint8_t> b;
-    b.base = a.rgba + (long long)ch * a.rgba_plane + (long long)oz * a.L.pz + (long long)oy * a.L.py + ox;
-    b.pz = a.L.pz;
-    b.py = a.L.py;
-    b.ex = block_extent(a.L, 0, bi);
-    b.ey = block_extent(a.L, 1, bj);
-    b.ez = block_extent(a.L, 2, bk);
-    double v = sample(b, x - (double)ox, y - (double)oy, z - (double)oz, a.cubic != 0);
+    double v = sample_in<CUBIC>(a.rgba + (long long)ch * a.rgba_plane, a, bi, bj, bk, x, y, z);
     return clampf(v / 255.0, 0.0, 1.0);
 }
 
@@ -152,14 +172,39 @@ VR_D void shade(const RenderArgs &a, double &r, double &g, double &b, double nx,
 VR_D double dmin(double a, double b) { return a < b ? a : b; }
 VR_D double dmax(double a, double b) { return a > b ? a : b; }
 
-// Number k >= 1 of samples, starting at n, that are guaranteed skippable:
-// every sample strictly before the safe parameter t_safe lies (in exact
-// arithmetic) at least 1e-6 voxel inside the current ownership cell and, for
-// a non-empty block, at least 1e-6 voxel outside its visibility box, so the
-// computed positions give the same skip verdict; one extra sample of slack
-// absorbs the rounding of t itself.
-VR_D long long leap_count(const RenderArgs &a, const Ray &r, double t0, long long n, double t,
-                          const double p[3], const int bidx[3], int b, bool cell_only) {
+// Parameter interval in which the (exact) ray lies inside the box [lo, hi]
+// expanded by delta on every side; returns false when it never does.  For an
+// axis the ray does not move along, the computed coordinate is exactly
+// constant, so the test uses the unexpanded bounds on it.
+VR_D bool slab(const double o[3], const double d[3], const double inv[3], const double s[3], const double p[3],
+               const double lo[3], const double hi[3], double delta, double &tin, double &tout) {
+    tin = -DBL_MAX;
+    tout = DBL_MAX;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (d[k] == 0.0) {
+            if (p[k] < lo[k] || p[k] > hi[k]) return false;
+        } else {
+            double ta = ((lo[k] - delta) * s[k] - o[k]) * inv[k];
+            double tb = ((hi[k] + delta) * s[k] - o[k]) * inv[k];
+            tin = dmax(tin, dmin(ta, tb));
+            tout = dmin(tout, dmax(ta, tb));
+        }
+    }
+    return tin <= tout;
+}
+
+// Number k >= 1 of samples, starting at the skippable sample n (parameter t,
+// computed position p, owner block (bidx, b)), that are guaranteed skippable.
+// Every sample strictly before the returned safe parameter lies, in exact
+// arithmetic, at least `delta` voxel inside the current ownership cell and
+// outside the block's box (when it is non-empty), or outside the union of
+// all visibility boxes; computed positions err by < 1e-11 voxel, so they give
+// the same verdict.  One sample of slack absorbs the rounding of t itself;
+// reciprocal multiplies stand in for divisions for the same reason.
+template <int KIND>
+VR_D long long leap_count(const RenderArgs &a, const Ray &r, const double inv[3], double t0, long long n,
+                          double t, const double p[3], const int bidx[3], int b, bool cell_only) {
     const double delta = 1e-6;
     const double d[3] = {r.dx, r.dy, r.dz};
     const double o[3] = {r.ox, r.oy, r.oz};
@@ -169,33 +214,40 @@ VR_D long long leap_count(const RenderArgs &a, const Ray &r, double t0, long lon
     for (int k = 0; k < 3; ++k) {
         if (d[k] > 0.0 && bidx[k] < a.L.nb[k] - 1) {
             double X = (1.0 + (double)((bidx[k] + 1) * a.L.stride)) - delta;
-            t_safe = dmin(t_safe, (X * s[k] - o[k]) / d[k]);
+            t_safe = dmin(t_safe, (X * s[k] - o[k]) * inv[k]);
         } else if (d[k] < 0.0 && bidx[k] > 0) {
             double X = (1.0 + (double)(bidx[k] * a.L.stride)) + delta;
-            t_safe = dmin(t_safe, (X * s[k] - o[k]) / d[k]);
+            t_safe = dmin(t_safe, (X * s[k] - o[k]) * inv[k]);
         }
     }
-    if (!cell_only) {
-        const double *bx = a.box + 6 * (long long)b;
-        double tin = -DBL_MAX, tout = DBL_MAX;
-        bool never = false;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            double lo = __ldg(bx + k), hi = __ldg(bx + 3 + k);
-            if (d[k] == 0.0) {
-                // the coordinate is exactly constant along the ray
-                if (p[k] < lo || p[k] > hi) never = true;
-            } else {
-                double ta = ((lo - delta) * s[k] - o[k]) / d[k];
-                double tb = ((hi + delta) * s[k] - o[k]) / d[k];
-                tin = dmax(tin, dmin(ta, tb));
-                tout = dmin(tout, dmax(ta, tb));
-            }
+    if (KIND != kIso) {
+        if (!cell_only) {
+            const double *bx = a.box + 6 * (long long)b;
+            const double lo[3] = {__ldg(bx), __ldg(bx + 1), __ldg(bx + 2)};
+            const double hi[3] = {__ldg(bx + 3), __ldg(bx + 4), __ldg(bx + 5)};
+            double tin, tout;
+            if (slab(o, d, inv, s, p, lo, hi, delta, tin, tout) && tout >= t)
+                t_safe = (tin > t) ? dmin(t_safe, tin) : t;
         }
-        if (!never && tin <= tout && tout >= t) t_safe = (tin > t) ? dmin(t_safe, tin) : t;
+        // union of every non-empty block's box: outside it nothing is visible
+        double tin, tout;
+        double ut;
+        const int u0 = __ldg(a.uni), u3 = __ldg(a.uni + 3);
+        const double ulo[3] = {(double)u0 - a.margin, (double)__ldg(a.uni + 1) - a.margin,
+                               (double)__ldg(a.uni + 2) - a.margin};
+        const double uhi[3] = {(double)u3 + a.margin, (double)__ldg(a.uni + 4) + a.margin,
+                               (double)__ldg(a.uni + 5) + a.margin};
+        if (u0 > u3) {
+            ut = DBL_MAX;  // no visible block at all
+        } else if (!slab(o, d, inv, s, p, ulo, uhi, delta, tin, tout) || tout < t) {
+            ut = DBL_MAX;
+        } else {
+            ut = tin > t ? tin : t;
+        }
+        t_safe = dmax(t_safe, ut);
     }
     if (!(t_safe > t)) return 1;
-    double q = (t_safe - t0) / a.step - 0.5;
+    double q = (t_safe - t0) * a.inv_step - 0.5;
     if (q > 4.0e15) return LLONG_MAX / 4;
     long long m = (long long)floor(q) - 1;
     long long k = m - n + 1;
@@ -209,7 +261,9 @@ struct RayResult {
 };
 
 // One pixel of _kernels.march (:343-594).
+template <int KIND, bool CUBIC, bool LIGHT, bool SKIP>
 VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
+    constexpr bool chained = (KIND == kIso) || (KIND == kPreint);  // _kernels.py:341
     RayResult res;
     double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
     long long n_taken = 0, n_skip = 0, n_shaded = 0;
@@ -223,23 +277,27 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
         long long N = nsteps;
         while (N > 0 && (t0 + ((double)(N - 1) + 0.5) * step) > t1) --N;
         const int nbx = a.L.nb[0], nby = a.L.nb[1];
-        const bool iso = a.mode == 1;
+        double inv[3] = {0.0, 0.0, 0.0};
+        if (SKIP) {
+            inv[0] = r.dx != 0.0 ? 1.0 / r.dx : 0.0;
+            inv[1] = r.dy != 0.0 ? 1.0 / r.dy : 0.0;
+            inv[2] = r.dz != 0.0 ? 1.0 / r.dz : 0.0;
+        }
         double prev_s = 0.0;
         bool prev_valid = false, prev_skippable = false;
         int last_hit = -1;
         long long n = 0;
         while (n < N) {
-            double t = t0 + ((double)n + 0.5) * step;
-            double x = divide(r.ox + t * r.dx, a.dsx);
-            double y = divide(r.oy + t * r.dy, a.dsy);
-            double z = divide(r.oz + t * r.dz, a.dsz);
-            int bi = owner_x(a, x), bj = owner_y(a, y), bk = owner_z(a, z);
-            int b = (bk * nby + bj) * nbx + bi;
+            const double t = t0 + ((double)n + 0.5) * step;
+            const double x = divide(r.ox + t * r.dx, a.dsx);
+            const double y = divide(r.oy + t * r.dy, a.dsy);
+            const double z = divide(r.oz + t * r.dz, a.dsz);
+            const int bi = owner(a, 0, x), bj = owner(a, 1, y), bk = owner(a, 2, z);
+            const int b = (bk * nby + bj) * nbx + bi;
 
-            bool skippable = false;
-            bool cell_only = true;
-            if (a.skip_empty) {
-                if (iso) {
+            if (SKIP) {
+                bool skippable, cell_only = true;
+                if (KIND == kIso) {
                     skippable = (double)__ldg(a.vmax + b) < a.isovalue || (double)__ldg(a.vmin + b) > a.isovalue;
                 } else if (__ldg(a.empty + b) == 1) {
                     skippable = true;
@@ -249,43 +307,44 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                                 y > __ldg(bx + 4) || z < __ldg(bx + 2) || z > __ldg(bx + 5);
                     cell_only = false;
                 }
+                if (skippable && (prev_skippable || !chained)) {
+                    const double p[3] = {x, y, z};
+                    const int bidx[3] = {bi, bj, bk};
+                    long long k = leap_count<KIND>(a, r, inv, t0, n, t, p, bidx, b, cell_only);
+                    long long m = (N - n < k) ? N : n + k;
+                    n_skip += m - n;
+                    n = m;
+                    prev_valid = false;
+                    prev_skippable = true;
+                    continue;
+                }
+                prev_skippable = skippable;
             }
-            if (skippable && (prev_skippable || !a.chained)) {
-                const double p[3] = {x, y, z};
-                const int bidx[3] = {bi, bj, bk};
-                long long k = leap_count(a, r, t0, n, t, p, bidx, b, cell_only);
-                long long m = (N - n < k) ? N : n + k;
-                n_skip += m - n;
-                n = m;
-                prev_valid = false;
-                prev_skippable = true;
-                continue;
-            }
-            prev_skippable = skippable;
             if (b != last_hit) {
                 if (a.blocks_hit) a.blocks_hit[b] = 1;
                 last_hit = b;
             }
             n_taken += 1;
 
-            if (iso) {
+            if (KIND == kIso) {
                 // _kernels.py:405-468
-                double s = sample_block(a, bi, bj, bk, x, y, z);
+                double s = sample_in<CUBIC>(a.vol, a, bi, bj, bk, x, y, z);
                 if (!prev_valid && n > 0) {
                     double tp = t - step;
-                    prev_s = attr_sample(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
-                                         divide(r.oz + tp * r.dz, a.dsz));
+                    prev_s = attr_sample<CUBIC>(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
+                                                divide(r.oz + tp * r.dz, a.dsz));
                     prev_valid = true;
                 }
                 bool hit = false;
                 double t_hit = t;
                 if (prev_valid && (prev_s - a.isovalue) * (s - a.isovalue) < 0.0) {
                     double lo_t = t - step, hi_t = t, lo_s = prev_s;
+#pragma unroll 1
                     for (int it = 0; it < 8; ++it) {
                         double mid = 0.5 * (lo_t + hi_t);
-                        double ms = attr_sample(a, divide(r.ox + mid * r.dx, a.dsx),
-                                                divide(r.oy + mid * r.dy, a.dsy),
-                                                divide(r.oz + mid * r.dz, a.dsz));
+                        double ms = attr_sample<CUBIC>(a, divide(r.ox + mid * r.dx, a.dsx),
+                                                       divide(r.oy + mid * r.dy, a.dsy),
+                                                       divide(r.oz + mid * r.dz, a.dsz));
                         if ((lo_s - a.isovalue) * (ms - a.isovalue) <= 0.0) {
                             hi_t = mid;
                         } else {
@@ -304,12 +363,12 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                     double hz = divide(r.oz + t_hit * r.dz, a.dsz);
                     int ib = lut_bin(a.isovalue, a.lut_lo, a.lut_inv_w, a.nlut);
                     double cr = __ldg(a.lut + 4 * ib), cg = __ldg(a.lut + 4 * ib + 1), cb = __ldg(a.lut + 4 * ib + 2);
-                    double gx, gy, gz;
-                    attr_grad(a, hx, hy, hz, owner_x(a, hx), owner_y(a, hy), owner_z(a, hz), gx, gy, gz);
+                    double g[3];
+                    attr_grad<CUBIC>(a, hx, hy, hz, owner(a, 0, hx), owner(a, 1, hy), owner(a, 2, hz), g);
                     n_shaded += 1;
-                    double norm = sqrt((gx * gx + gy * gy) + gz * gz);
-                    if (a.lighting && norm > 1e-12)
-                        shade(a, cr, cg, cb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                    double norm = sqrt((g[0] * g[0] + g[1] * g[1]) + g[2] * g[2]);
+                    if (LIGHT && norm > 1e-12)
+                        shade(a, cr, cg, cb, -g[0] / norm, -g[1] / norm, -g[2] / norm, -r.dx, -r.dy, -r.dz);
                     acc_r = cr;
                     acc_g = cg;
                     acc_b = cb;
@@ -319,25 +378,21 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 }
                 prev_s = s;
                 prev_valid = true;
-                ++n;
-                continue;
-            }
-
-            if (a.classify == 1) {
+            } else if (KIND == kPre) {
                 // pre-classified (_kernels.py:471-507)
-                double sa = attr_rgba(a, bi, bj, bk, x, y, z, 3);
+                double sa = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 3);
                 if (sa > 0.0) {
-                    double sr = attr_rgba(a, bi, bj, bk, x, y, z, 0);
-                    double sg = attr_rgba(a, bi, bj, bk, x, y, z, 1);
-                    double sb = attr_rgba(a, bi, bj, bk, x, y, z, 2);
+                    double sr = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 0);
+                    double sg = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 1);
+                    double sb = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 2);
                     double ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
-                    if (a.lighting) {
-                        double gx, gy, gz;
-                        attr_grad(a, x, y, z, bi, bj, bk, gx, gy, gz);
+                    if (LIGHT) {
+                        double g[3];
+                        attr_grad<CUBIC>(a, x, y, z, bi, bj, bk, g);
                         n_shaded += 1;
-                        double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                        double norm = sqrt((g[0] * g[0] + g[1] * g[1]) + g[2] * g[2]);
                         if (norm > 1e-12)
-                            shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                            shade(a, sr, sg, sb, -g[0] / norm, -g[1] / norm, -g[2] / norm, -r.dx, -r.dy, -r.dz);
                     }
                     double w = (1.0 - acc_a) * ahat;
                     acc_r += w * sr;
@@ -346,21 +401,21 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                     acc_a += w;
                     if (acc_a >= a.term_alpha) break;
                 }
-            } else if (a.classify == 0) {
+            } else if (KIND == kPost) {
                 // post-classified (_kernels.py:508-537)
-                double s = sample_block(a, bi, bj, bk, x, y, z);
+                double s = sample_in<CUBIC>(a.vol, a, bi, bj, bk, x, y, z);
                 int sbin = lut_bin(s, a.lut_lo, a.lut_inv_w, a.nlut);
                 double sa = __ldg(a.lut + 4 * sbin + 3);
                 if (sa > 0.0) {
                     double sr = __ldg(a.lut + 4 * sbin), sg = __ldg(a.lut + 4 * sbin + 1), sb = __ldg(a.lut + 4 * sbin + 2);
                     double ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
-                    if (a.lighting) {
-                        double gx, gy, gz;
-                        attr_grad(a, x, y, z, bi, bj, bk, gx, gy, gz);
+                    if (LIGHT) {
+                        double g[3];
+                        attr_grad<CUBIC>(a, x, y, z, bi, bj, bk, g);
                         n_shaded += 1;
-                        double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                        double norm = sqrt((g[0] * g[0] + g[1] * g[1]) + g[2] * g[2]);
                         if (norm > 1e-12)
-                            shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                            shade(a, sr, sg, sb, -g[0] / norm, -g[1] / norm, -g[2] / norm, -r.dx, -r.dy, -r.dz);
                     }
                     double w = (1.0 - acc_a) * ahat;
                     acc_r += w * sr;
@@ -371,11 +426,11 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 }
             } else {
                 // pre-integrated (_kernels.py:538-581)
-                double s = sample_block(a, bi, bj, bk, x, y, z);
+                double s = sample_in<CUBIC>(a.vol, a, bi, bj, bk, x, y, z);
                 if (!prev_valid && n > 0) {
                     double tp = t - step;
-                    prev_s = attr_sample(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
-                                         divide(r.oz + tp * r.dz, a.dsz));
+                    prev_s = attr_sample<CUBIC>(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
+                                                divide(r.oz + tp * r.dz, a.dsz));
                     prev_valid = true;
                 }
                 double sf = prev_valid ? prev_s : s;
@@ -385,13 +440,13 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 double seg_a = __ldg(cell + 3);
                 if (seg_a > 0.0) {
                     double seg_r = __ldg(cell), seg_g = __ldg(cell + 1), seg_b = __ldg(cell + 2);
-                    if (a.lighting) {
-                        double gx, gy, gz;
-                        attr_grad(a, x, y, z, bi, bj, bk, gx, gy, gz);
+                    if (LIGHT) {
+                        double g[3];
+                        attr_grad<CUBIC>(a, x, y, z, bi, bj, bk, g);
                         n_shaded += 1;
-                        double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                        double norm = sqrt((g[0] * g[0] + g[1] * g[1]) + g[2] * g[2]);
                         if (norm > 1e-12) {
-                            double ndl = fabs(((gx * -r.dx + gy * -r.dy) + gz * -r.dz) / norm);
+                            double ndl = fabs(((g[0] * -r.dx + g[1] * -r.dy) + g[2] * -r.dz) / norm);
                             double scale = a.ka + a.kd * ndl;
                             double spec = a.ks * vr_pow(ndl, a.shin) * seg_a;
                             seg_r = clampf(scale * seg_r + spec, 0.0, 1.0);
@@ -439,10 +494,11 @@ VR_D unsigned long long warp_sum(unsigned long long v) {
     return v;
 }
 
+template <int KIND, bool CUBIC, bool LIGHT, bool SKIP>
 __global__ void __launch_bounds__(kThreads) raycast_kernel(const __grid_constant__ RenderArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int lx = (warp & 1) * 8 + (lane & 7);   // 0..15 inside the cell
-    const int ly = (warp >> 1) * 4 + (lane >> 3);  // 0..7
+    const int lx = (warp & 1) * 8 + (lane & 7);   // 0..15 inside the 16x8 cell
+    const int ly = (warp >> 1) * 4 + (lane >> 3);  // 0..7; each warp an 8x4 tile
     const int slot = blockIdx.x;
     const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
     const int cx = (cell % a.cells_x) * kTileW + lx;
@@ -453,15 +509,12 @@ __global__ void __launch_bounds__(kThreads) raycast_kernel(const __grid_constant
         Ray r = make_ray(a, a.tx + cx, a.ty + cy);
         double t0, t1;
         clip_to_bounds(r, a.ext_mm, t0, t1);
-        RayResult res = march(a, r, t0, t1);
+        RayResult res = march<KIND, CUBIC, LIGHT, SKIP>(a, r, t0, t1);
         const long long p = a.il_n > 1 ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx
                                         : (long long)cy * a.tw + cx;
         if (a.premult) {
             double4 *o = reinterpret_cast<double4 *>(a.premult) + p;
-            o->x = res.r;
-            o->y = res.g;
-            o->z = res.b;
-            o->w = res.a;
+            *o = make_double4(res.r, res.g, res.b, res.a);
         }
         if (a.pixels) {
             double alpha = res.a;
@@ -472,8 +525,7 @@ __global__ void __launch_bounds__(kThreads) raycast_kernel(const __grid_constant
                 g0 = res.g / den;
                 b0 = res.b / den;
             }
-            uchar4 px = make_uchar4(to_u8(r0), to_u8(g0), to_u8(b0), to_u8(alpha));
-            reinterpret_cast<uchar4 *>(a.pixels)[p] = px;
+            reinterpret_cast<uchar4 *>(a.pixels)[p] = make_uchar4(to_u8(r0), to_u8(g0), to_u8(b0), to_u8(alpha));
         }
         if (a.depth) a.depth[p] = res.depth;
         if (a.taken) a.taken[p] = res.taken;
@@ -494,12 +546,39 @@ __global__ void __launch_bounds__(kThreads) raycast_kernel(const __grid_constant
     }
 }
 
+using KernelFn = void (*)(RenderArgs);
+
+template <int KIND, bool CUBIC, bool LIGHT>
+KernelFn pick_skip(bool skip) {
+    return skip ? raycast_kernel<KIND, CUBIC, LIGHT, true> : raycast_kernel<KIND, CUBIC, LIGHT, false>;
+}
+
+template <int KIND, bool CUBIC>
+KernelFn pick_light(bool light, bool skip) {
+    return light ? pick_skip<KIND, CUBIC, true>(skip) : pick_skip<KIND, CUBIC, false>(skip);
+}
+
+template <int KIND>
+KernelFn pick_cubic(bool cubic, bool light, bool skip) {
+    return cubic ? pick_light<KIND, true>(light, skip) : pick_light<KIND, false>(light, skip);
+}
+
+KernelFn pick(const RenderArgs &a) {
+    const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
+    if (a.mode == 1) return pick_cubic<kIso>(c, l, s);
+    switch (a.classify) {
+        case 1: return pick_cubic<kPre>(c, l, s);
+        case 2: return pick_cubic<kPreint>(c, l, s);
+        default: return pick_cubic<kPost>(c, l, s);
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
     if (a.tw <= 0 || a.th <= 0) return cudaSuccess;
     if (a.slots <= 0) return cudaSuccess;
-    raycast_kernel<<<a.slots, kThreads, 0, stream>>>(a);
+    pick(a)<<<a.slots, kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -38,6 +38,9 @@ struct RenderArgs {
     const uint8_t *empty;    // nblocks
     const double *box;       // nblocks x 6: lo xyz (aabb_lo - margin), hi xyz (aabb_hi + margin)
     const int *vmin, *vmax;  // nblocks (iso skip predicate)
+    const int *uni;          // 6: union of the fitted global AABBs (lo xyz, hi xyz); lo > hi = none
+    double margin;           // SKIP_MARGIN applied to every box
+    double inv_step;         // 1 / step (leap estimates only; sample positions use step)
 
     // outputs (all optional)
     uint8_t *pixels;
