@@ -20,6 +20,8 @@ struct vr_volume {
     double sx, sy, sz;
     int16_t *data;
     int32_t vmin, vmax;
+    short2 *cells;  // dilated 4^3 cell min/max for transparency culling
+    int ncx, ncy, ncz;
 };
 
 struct vr_grid {
@@ -166,7 +168,12 @@ int vr_interleave_size(const vr_camera *cam, int64_t *cells_per_rank, int64_t *p
 static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     long long n = v->nx * v->ny * v->nz;
     int *d_range = nullptr;
-    cudaError_t e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
+    v->ncx = (int)((v->nx + vr::kCell - 1) / vr::kCell);
+    v->ncy = (int)((v->ny + vr::kCell - 1) / vr::kCell);
+    v->ncz = (int)((v->nz + vr::kCell - 1) / vr::kCell);
+    cudaError_t e = cudaMalloc((void **)&v->cells, sizeof(short2) * (size_t)v->ncx * v->ncy * v->ncz);
+    if (e == cudaSuccess) e = vr::launch_cell_minmax(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->cells, s);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
     if (e == cudaSuccess) e = vr::launch_value_range(v->data, n, d_range, s);
     int h[2] = {0, 0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(h, d_range, sizeof(h), cudaMemcpyDeviceToHost, s);
@@ -174,6 +181,7 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
         cudaFree(v->data);
+        cudaFree(v->cells);
         delete v;
         return cuda_fail(e, "volume value range");
     }
@@ -212,6 +220,7 @@ int vr_volume_create(int device, int64_t nx, int64_t ny, int64_t nz, double sx, 
     e = cudaMemcpyAsync(v->data, src, bytes, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) {
         cudaFree(v->data);
+        cudaFree(v->cells);
         delete v;
         return cuda_fail(e, "volume upload");
     }
@@ -238,6 +247,7 @@ int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, 
     e = vr::launch_phantom(kind, (int)nx, (int)ny, (int)nz, v->data, s);
     if (e != cudaSuccess) {
         cudaFree(v->data);
+        cudaFree(v->cells);
         delete v;
         return cuda_fail(e, "phantom kernel");
     }
@@ -248,6 +258,7 @@ int vr_volume_destroy(vr_volume *v) {
     if (!v) return VR_OK;
     DeviceGuard g(v->device);
     cudaFree(v->data);
+    cudaFree(v->cells);
     delete v;
     return VR_OK;
 }
@@ -535,6 +546,16 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     a.shaded = (unsigned long long *)out->shaded;
     int nblocks = grid ? grid->nblocks : 1;
     if (a.blocks_hit) VR_CUDA(cudaMemsetAsync(a.blocks_hit, 0, nblocks, s));
+    Scratch lut_range(s);
+    if (a.mode == VR_MODE_DVR && a.classify == VR_CLS_POST && vol->cells) {
+        VR_CUDA(lut_range.alloc(2 * sizeof(int)));
+        VR_CUDA(vr::launch_lut_range(lut, prm->nlut, (int *)lut_range.p, s));
+        a.lut_range = (const int *)lut_range.p;
+        a.cells = vol->cells;
+        a.ncx = vol->ncx;
+        a.ncy = vol->ncy;
+        a.cull = 1;
+    }
     VisScratch vs(s);
     if (grid) {
         VR_CUDA(vs.init(grid, lut, prm->nlut, prm->lut_lo, prm->lut_hi, prm->margin, false));

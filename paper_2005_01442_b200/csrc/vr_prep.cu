@@ -313,6 +313,53 @@ __global__ void box_kernel(const Layout L, const VisArgs v) {
     }
 }
 
+// ------------------------------------------------------- transparency culling
+
+__global__ void __launch_bounds__(kBlock) cell_minmax_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
+                                                             int ncx, int ncy, int ncz, short2 *cells) {
+    long long n = (long long)ncx * ncy * ncz;
+    long long py = nx, pz = (long long)nx * ny;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+        int cx = (int)(c % ncx);
+        long long r = c / ncx;
+        int cy = (int)(r % ncy), cz = (int)(r / ncy);
+        int x0 = max(cx * kCell - 1, 0), x1 = min(cx * kCell + kCell + 1, nx - 1);
+        int y0 = max(cy * kCell - 1, 0), y1 = min(cy * kCell + kCell + 1, ny - 1);
+        int z0 = max(cz * kCell - 1, 0), z1 = min(cz * kCell + kCell + 1, nz - 1);
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int z = z0; z <= z1; ++z)
+            for (int y = y0; y <= y1; ++y) {
+                const int16_t *row = vol + z * pz + y * py;
+                for (int x = x0; x <= x1; ++x) {
+                    int v = __ldg(row + x);
+                    lo = min(lo, v);
+                    hi = max(hi, v);
+                }
+            }
+        cells[c] = make_short2((short)lo, (short)hi);
+    }
+}
+
+__global__ void lut_range_kernel(const double *lut, int nbins, int *range) {
+    __shared__ int first, last;
+    if (threadIdx.x == 0) {
+        first = nbins;
+        last = -1;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nbins; i += blockDim.x) {
+        if (__ldg(lut + 4 * i + 3) > 0.0) {
+            atomicMin(&first, i);
+            atomicMax(&last, i);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        range[0] = first;
+        range[1] = last;
+    }
+}
+
 __global__ void count_hits_kernel(const uint8_t *hits, int n, unsigned long long *out) {
     unsigned long long c = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) c += hits[i] ? 1 : 0;
@@ -531,6 +578,18 @@ cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs
     dim3 grid(v.nblocks, zsplit_for(L));
     aabb_kernel<<<grid, kBlock, 0, s>>>(vol, L, v);
     box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cell_minmax(const int16_t *vol, int nx, int ny, int nz, short2 *cells, cudaStream_t s) {
+    int ncx = (nx + kCell - 1) / kCell, ncy = (ny + kCell - 1) / kCell, ncz = (nz + kCell - 1) / kCell;
+    long long n = (long long)ncx * ncy * ncz;
+    cell_minmax_kernel<<<grid_for(n, kBlock, 148 * 32), kBlock, 0, s>>>(vol, nx, ny, nz, ncx, ncy, ncz, cells);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_lut_range(const double *lut, int nbins, int *range, cudaStream_t s) {
+    lut_range_kernel<<<1, 1024, 0, s>>>(lut, nbins, range);
     return cudaGetLastError();
 }
 

@@ -37,6 +37,17 @@ struct VisArgs {
 cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,
                               cudaStream_t s);
 
+// Transparency culling support.  cells[c] = (min, max) of the voxels whose
+// index lies in [4c-1, 4c+5) per axis (clamped to the volume): every tap of a
+// trilinear or Catmull-Rom sample whose clamped base index floor(x) falls in
+// cell c is one of them.  TF-independent, built once per volume.
+constexpr int kCell = 4;
+cudaError_t launch_cell_minmax(const int16_t *vol, int nx, int ny, int nz, short2 *cells, cudaStream_t s);
+
+// range[0] = first LUT bin with nonzero opacity (nbins if none),
+// range[1] = last such bin (-1 if none)
+cudaError_t launch_lut_range(const double *lut, int nbins, int *range, cudaStream_t s);
+
 // blocks_visited = sum(blocks_hit) -> *out (render.py:467)
 cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out, cudaStream_t s);
 

@@ -172,6 +172,28 @@ VR_D void shade(const RenderArgs &a, double &r, double &g, double &b, double nx,
 VR_D double dmin(double a, double b) { return a < b ? a : b; }
 VR_D double dmax(double a, double b) { return a > b ? a : b; }
 
+// True when the interpolated value at (x, y, z) provably classifies to a
+// zero-opacity LUT bin, so the reference's sample would contribute nothing
+// (_kernels.py:513-515: alpha == 0 -> no compositing).  Every tap of the
+// sample lies in [g-1, g+2] per axis, g = floor(clamp(coordinate)), all of
+// which the dilated cell of g covers; a Catmull-Rom value lies within
+// [min - K(max-min), max + K(max-min)] with K = (1.25^3 - 1)/2 < 0.5 (per
+// axis sum |w| = 1 + t(1-t) <= 1.25), trilinear within [min, max].  The
+// 1e-3 slack dwarfs the float64 rounding of the 64-term sum (~1e-12).
+template <bool CUBIC>
+VR_D bool provably_transparent(const RenderArgs &a, double x, double y, double z, int first_vis, int last_vis) {
+    const int gx = (int)clampf(x, 0.0, (double)(a.L.n[0] - 1));
+    const int gy = (int)clampf(y, 0.0, (double)(a.L.n[1] - 1));
+    const int gz = (int)clampf(z, 0.0, (double)(a.L.n[2] - 1));
+    const short2 mm = __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2));
+    const double lo = (double)mm.x, hi = (double)mm.y;
+    const double k = CUBIC ? 0.5 : 0.0;
+    const double up = hi + k * (hi - lo) + 1e-3;
+    const double dn = lo - k * (hi - lo) - 1e-3;
+    return lut_bin(up, a.lut_lo, a.lut_inv_w, a.nlut) < first_vis ||
+           lut_bin(dn, a.lut_lo, a.lut_inv_w, a.nlut) > last_vis;
+}
+
 // Parameter interval in which the (exact) ray lies inside the box [lo, hi]
 // expanded by delta on every side; returns false when it never does.  For an
 // axis the ray does not move along, the computed coordinate is exactly
@@ -286,6 +308,12 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
         double prev_s = 0.0;
         bool prev_valid = false, prev_skippable = false;
         int last_hit = -1;
+        int first_vis = 0, last_vis = 0;
+        const bool cull = KIND == kPost && a.cull;
+        if (cull) {
+            first_vis = __ldg(a.lut_range);
+            last_vis = __ldg(a.lut_range + 1);
+        }
         long long n = 0;
         while (n < N) {
             const double t = t0 + ((double)n + 0.5) * step;
@@ -403,6 +431,10 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 }
             } else if (KIND == kPost) {
                 // post-classified (_kernels.py:508-537)
+                if (cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis)) {
+                    ++n;
+                    continue;
+                }
                 double s = sample_in<CUBIC>(a.vol, a, bi, bj, bk, x, y, z);
                 int sbin = lut_bin(s, a.lut_lo, a.lut_inv_w, a.nlut);
                 double sa = __ldg(a.lut + 4 * sbin + 3);

@@ -42,6 +42,13 @@ struct RenderArgs {
     double margin;           // SKIP_MARGIN applied to every box
     double inv_step;         // 1 / step (leap estimates only; sample positions use step)
 
+    // transparency culling (post-classification): dilated 4^3 cell min/max and
+    // the LUT's first/last bins with nonzero opacity
+    const short2 *cells;
+    int ncx, ncy;
+    const int *lut_range;
+    int cull;
+
     // outputs (all optional)
     uint8_t *pixels;
     double *premult;
