@@ -357,7 +357,8 @@ def run_ours(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (torso phantom generated on the device, bit-identical to the reference's)",
         "samples_per_sec": taken * fps, "samples_taken": taken, "samples_skipped": st["samples_skipped"],
-        "shaded_samples": shaded,
+        "shaded_samples": shaded, "interpolated_samples": st.get("interpolated"),
+        "march_iterations": st.get("march_iterations"),
         "config": {"workload": args.config, "desc": cfg["desc"], "volume": list(cfg["dims"]),
                    "image": [W, H], "tf": cfg["tf"], "parallelism": f"sort-first x{world}",
                    "l2": "flushed between steps (512 MiB write)"},

@@ -108,7 +108,8 @@ typedef struct {
                             reference raises EmptyBlock for those,
                             blocks.py:186-187) -- the last three written, and
                             blocks_visited only when blocks_hit is given */
-    uint64_t *shaded;    /* [1] optional: samples that ran the gradient (for the roofline) */
+    uint64_t *work;      /* [3] optional, accumulated: gradient evaluations (shaded samples),
+                            interpolated samples (taken minus culled), march-loop iterations */
     void *ev_start;      /* optional cudaEvent_t recorded just before the ray-cast kernel */
     void *ev_stop;       /* optional cudaEvent_t recorded just after it */
 } vr_render_outputs;

@@ -51,22 +51,30 @@ def up_to_date() -> bool:
     return all(p.stat().st_mtime <= t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    """Compile the library (to ``out`` with extra -D ``defines`` for experiments)."""
+    target = Path(out) if out else LIB_PATH
+    if not force and out is None and not defines and up_to_date():
         return LIB_PATH
-    tmp = LIB_PATH.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, "-I", str(ROOT / "include"),
+    tmp = target.with_suffix(".so.tmp")
+    cmd = [nvcc(), *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"),
            *map(str, sources()), "-o", str(tmp)]
     proc = subprocess.run(cmd, capture_output=True, text=True)
-    log = PKG / "build.log"
+    log = target.with_suffix(".build.log") if out else PKG / "build.log"
     log.write_text(" ".join(cmd) + "\n" + proc.stdout + proc.stderr)
     if proc.returncode != 0:
         raise RuntimeError(f"nvcc failed ({proc.returncode}); see {log}\n{proc.stderr[-4000:]}")
-    os.replace(tmp, LIB_PATH)
+    os.replace(tmp, target)
     if verbose:
         print(proc.stderr)
-    return LIB_PATH
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+
+    if len(sys.argv) > 2:  # _build.py OUT.so DEFINE [DEFINE ...]
+        print(build(force=True, out=Path(sys.argv[1]), defines=tuple(sys.argv[2:])))
+    else:
+        print(build(force=True, verbose=True))

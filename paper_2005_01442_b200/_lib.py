@@ -8,11 +8,14 @@ every entry point that needs the GPU raises.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 from . import errors
 
 LIB_PATH = Path(__file__).resolve().parent / "libvoxelray_b200.so"
+if os.environ.get("VR_LIB"):  # development: load an alternative build of the same ABI
+    LIB_PATH = Path(os.environ["VR_LIB"]).resolve()
 
 VR_OK, VR_EINVALID, VR_EBLOCKSPEC, VR_EISO, VR_ECUDA, VR_ENOMEM = range(6)
 MODE_DVR, MODE_ISO = 0, 1
@@ -60,7 +63,7 @@ class RenderOutputs(ctypes.Structure):
     _fields_ = [
         ("pixels", ctypes.c_void_p), ("premult", ctypes.c_void_p), ("depth", ctypes.c_void_p),
         ("taken", ctypes.c_void_p), ("skipped", ctypes.c_void_p), ("blocks_hit", ctypes.c_void_p),
-        ("totals", ctypes.c_void_p), ("shaded", ctypes.c_void_p),
+        ("totals", ctypes.c_void_p), ("work", ctypes.c_void_p),
         ("ev_start", ctypes.c_void_p), ("ev_stop", ctypes.c_void_p),
     ]
 

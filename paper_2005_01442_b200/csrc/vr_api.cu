@@ -22,6 +22,8 @@ struct vr_volume {
     int32_t vmin, vmax;
     short2 *cells;  // dilated 4^3 cell min/max for transparency culling
     int ncx, ncy, ncz;
+    int16_t *bricks;  // K1: the voxels in 4^3 bricks (what the ray caster reads)
+    int bnx, bny, bnz;
 };
 
 struct vr_grid {
@@ -171,7 +173,12 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     v->ncx = (int)((v->nx + vr::kCell - 1) / vr::kCell);
     v->ncy = (int)((v->ny + vr::kCell - 1) / vr::kCell);
     v->ncz = (int)((v->nz + vr::kCell - 1) / vr::kCell);
+    v->bnx = (int)((v->nx + 3) / 4);
+    v->bny = (int)((v->ny + 3) / 4);
+    v->bnz = (int)((v->nz + 3) / 4);
     cudaError_t e = cudaMalloc((void **)&v->cells, sizeof(short2) * (size_t)v->ncx * v->ncy * v->ncz);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&v->bricks, sizeof(int16_t) * 64 * (size_t)v->bnx * v->bny * v->bnz);
+    if (e == cudaSuccess) e = vr::launch_brick_volume(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bricks, s);
     if (e == cudaSuccess) e = vr::launch_cell_minmax(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->cells, s);
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
     if (e == cudaSuccess) e = vr::launch_value_range(v->data, n, d_range, s);
@@ -182,6 +189,7 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     if (e != cudaSuccess) {
         cudaFree(v->data);
         cudaFree(v->cells);
+        cudaFree(v->bricks);
         delete v;
         return cuda_fail(e, "volume value range");
     }
@@ -221,6 +229,7 @@ int vr_volume_create(int device, int64_t nx, int64_t ny, int64_t nz, double sx, 
     if (e != cudaSuccess) {
         cudaFree(v->data);
         cudaFree(v->cells);
+        cudaFree(v->bricks);
         delete v;
         return cuda_fail(e, "volume upload");
     }
@@ -248,6 +257,7 @@ int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, 
     if (e != cudaSuccess) {
         cudaFree(v->data);
         cudaFree(v->cells);
+        cudaFree(v->bricks);
         delete v;
         return cuda_fail(e, "phantom kernel");
     }
@@ -259,6 +269,7 @@ int vr_volume_destroy(vr_volume *v) {
     DeviceGuard g(v->device);
     cudaFree(v->data);
     cudaFree(v->cells);
+    cudaFree(v->bricks);
     delete v;
     return VR_OK;
 }
@@ -472,6 +483,9 @@ static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
 
     a = vr::RenderArgs();
     a.vol = vol->data;
+    a.bv.p = vol->bricks;
+    a.bv.bpy = (long long)vol->bnx * 64;
+    a.bv.bpz = (long long)vol->bnx * vol->bny * 64;
     a.L = grid ? grid->L : monolithic_layout(vol);
     a.dsx = vr::make_divisor(vol->sx);
     a.dsy = vr::make_divisor(vol->sy);
@@ -543,14 +557,15 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     a.skipped = (long long *)out->skipped;
     a.blocks_hit = out->blocks_hit;
     a.totals = (unsigned long long *)out->totals;
-    a.shaded = (unsigned long long *)out->shaded;
+    a.work = (unsigned long long *)out->work;
     int nblocks = grid ? grid->nblocks : 1;
     if (a.blocks_hit) VR_CUDA(cudaMemsetAsync(a.blocks_hit, 0, nblocks, s));
     Scratch lut_range(s);
     if (a.mode == VR_MODE_DVR && a.classify == VR_CLS_POST && vol->cells) {
-        VR_CUDA(lut_range.alloc(2 * sizeof(int)));
+        VR_CUDA(lut_range.alloc(16));
         VR_CUDA(vr::launch_lut_range(lut, prm->nlut, (int *)lut_range.p, s));
         a.lut_range = (const int *)lut_range.p;
+        a.work_counter = (unsigned long long *)((char *)lut_range.p + 8);
         a.cells = vol->cells;
         a.ncx = vol->ncx;
         a.ncy = vol->ncy;

@@ -86,19 +86,101 @@ VR_D void cr_weights(double t, double &w0, double &w1, double &w2, double &w3) {
     w3 = 0.5 * (t3 - t2);
 }
 
-// A block of the volume seen through the reference's atlas addressing: local
-// coordinates in [0, e), voxels at base[(k*py) + (j*px) + i] with the global
-// pitches (the atlas copy of a block holds the same voxels, blocks.py:269-294).
-template <class T>
-struct Brick {
-    const T *base;
-    long long pz, py;  // plane and row pitch in elements
-    int ex, ey, ez;    // block extents
+// ------------------------------------------------------------ volume views
+// Voxel access by global index (x, y, z).  Three layouts: the x-fastest
+// linear volume (ScalarVolume.values order), the same for uint8 planes
+// (pre-classified RGBA), and the 4x4x4-brick layout K1 builds for the ray
+// caster -- one brick is one 128-byte line, so the 4x4x4 Catmull-Rom
+// neighbourhood of a sample touches at most 8 lines, and neighbouring rays of
+// a warp share them, whatever the view direction.
+struct LinearVol {
+    const int16_t *p;
+    long long py, pz;
+    VR_D const int16_t *at_ptr(int x, int y, int z) const { return p + (long long)z * pz + (long long)y * py + x; }
+    VR_D double at(int x, int y, int z) const { return tap(at_ptr(x, y, z)); }
+    VR_D void row4(int x, int y, int z, double v[4]) const {
+        const int16_t *q = at_ptr(x, y, z);
+        v[0] = tap(q);
+        v[1] = tap(q + 1);
+        v[2] = tap(q + 2);
+        v[3] = tap(q + 3);
+    }
+    VR_D void row2(int x, int y, int z, double v[2]) const {
+        const int16_t *q = at_ptr(x, y, z);
+        v[0] = tap(q);
+        v[1] = tap(q + 1);
+    }
+};
+
+struct LinearU8 {
+    const uint8_t *p;
+    long long py, pz;
+    VR_D const uint8_t *at_ptr(int x, int y, int z) const { return p + (long long)z * pz + (long long)y * py + x; }
+    VR_D double at(int x, int y, int z) const { return tap(at_ptr(x, y, z)); }
+    VR_D void row4(int x, int y, int z, double v[4]) const {
+        const uint8_t *q = at_ptr(x, y, z);
+        v[0] = tap(q);
+        v[1] = tap(q + 1);
+        v[2] = tap(q + 2);
+        v[3] = tap(q + 3);
+    }
+    VR_D void row2(int x, int y, int z, double v[2]) const {
+        const uint8_t *q = at_ptr(x, y, z);
+        v[0] = tap(q);
+        v[1] = tap(q + 1);
+    }
+};
+
+struct BrickVol {
+    const int16_t *p;
+    long long bpy, bpz;  // int16 elements per row of bricks / per plane of bricks
+    VR_D const int16_t *row_ptr(int x, int y, int z) const {
+        return p + (long long)(z >> 2) * bpz + (long long)(y >> 2) * bpy + ((long long)(x >> 2) << 6) +
+               ((z & 3) << 4) + ((y & 3) << 2);
+    }
+    VR_D double at(int x, int y, int z) const { return tap(row_ptr(x, y, z) + (x & 3)); }
+    // four (two) consecutive voxels from x: the 8-byte brick row holding x,
+    // plus the next brick's row when the run crosses into it
+    VR_D unsigned long long run(int x, int y, int z, int len) const {
+        const int16_t *q = row_ptr(x, y, z);
+        unsigned long long lo = __ldg(reinterpret_cast<const unsigned long long *>(q));
+        const int o = x & 3;
+        if (o + len > 4) {
+            unsigned long long hi = __ldg(reinterpret_cast<const unsigned long long *>(q + 64));
+            lo = (lo >> (16 * o)) | (hi << (64 - 16 * o));
+        } else {
+            lo >>= 16 * o;
+        }
+        return lo;
+    }
+    VR_D void row4(int x, int y, int z, double v[4]) const {
+        unsigned long long w = run(x, y, z, 4);
+        v[0] = (double)(short)(w & 0xffff);
+        v[1] = (double)(short)((w >> 16) & 0xffff);
+        v[2] = (double)(short)((w >> 32) & 0xffff);
+        v[3] = (double)(short)(w >> 48);
+    }
+    VR_D void row2(int x, int y, int z, double v[2]) const {
+        unsigned long long w = run(x, y, z, 2);
+        v[0] = (double)(short)(w & 0xffff);
+        v[1] = (double)(short)((w >> 16) & 0xffff);
+    }
+};
+
+// A block of the decomposition seen through the reference's atlas
+// addressing: local coordinates in [0, e) per axis, local voxel i at global
+// index origin + i (the atlas copy of a block holds exactly those voxels,
+// blocks.py:269-294).
+template <class V>
+struct Block {
+    V vol;
+    int ox, oy, oz;
+    int ex, ey, ez;
 };
 
 // _kernels.py:52-80
-template <class T>
-VR_D double tri_sample(const Brick<T> &b, double x, double y, double z) {
+template <class V>
+VR_D double tri_sample(const Block<V> &b, double x, double y, double z) {
     x = clampf(x, 0.0, b.ex - 1.0);
     y = clampf(y, 0.0, b.ey - 1.0);
     z = clampf(z, 0.0, b.ez - 1.0);
@@ -108,22 +190,24 @@ VR_D double tri_sample(const Brick<T> &b, double x, double y, double z) {
     double fx = x - (double)i0;
     double fy = y - (double)j0;
     double fz = z - (double)k0;
-    const T *p = b.base + (long long)k0 * b.pz + (long long)j0 * b.py + i0;
-    const T *q = p + b.pz;
-    double v000 = tap(p), v100 = tap(p + 1), v010 = tap(p + b.py), v110 = tap(p + b.py + 1);
-    double v001 = tap(q), v101 = tap(q + 1), v011 = tap(q + b.py), v111 = tap(q + b.py + 1);
-    double c00 = v000 + (v100 - v000) * fx;
-    double c10 = v010 + (v110 - v010) * fx;
-    double c01 = v001 + (v101 - v001) * fx;
-    double c11 = v011 + (v111 - v011) * fx;
+    const int gx = b.ox + i0, gy = b.oy + j0, gz = b.oz + k0;
+    double r00[2], r10[2], r01[2], r11[2];
+    b.vol.row2(gx, gy, gz, r00);
+    b.vol.row2(gx, gy + 1, gz, r10);
+    b.vol.row2(gx, gy, gz + 1, r01);
+    b.vol.row2(gx, gy + 1, gz + 1, r11);
+    double c00 = r00[0] + (r00[1] - r00[0]) * fx;
+    double c10 = r10[0] + (r10[1] - r10[0]) * fx;
+    double c01 = r01[0] + (r01[1] - r01[0]) * fx;
+    double c11 = r11[0] + (r11[1] - r11[0]) * fx;
     double c0 = c00 + (c10 - c00) * fy;
     double c1 = c01 + (c11 - c01) * fy;
     return c0 + (c1 - c0) * fz;
 }
 
 // _kernels.py:94-143: taps clamped to the block, rows summed x -> y -> z.
-template <class T>
-VR_D double cub_sample(const Brick<T> &b, double x, double y, double z) {
+template <class V>
+VR_D double cub_sample(const Block<V> &b, double x, double y, double z) {
     x = clampf(x, 0.0, b.ex - 1.0);
     y = clampf(y, 0.0, b.ey - 1.0);
     z = clampf(z, 0.0, b.ez - 1.0);
@@ -134,28 +218,143 @@ VR_D double cub_sample(const Brick<T> &b, double x, double y, double z) {
     cr_weights(x - (double)i0, wx0, wx1, wx2, wx3);
     cr_weights(y - (double)j0, wy0, wy1, wy2, wy3);
     cr_weights(z - (double)k0, wz0, wz1, wz2, wz3);
-    int ia = max(i0 - 1, 0), ic = min(i0 + 1, b.ex - 1), id = min(i0 + 2, b.ex - 1);
-    long long ja = (long long)max(j0 - 1, 0) * b.py, jb = (long long)j0 * b.py;
-    long long jc = (long long)min(j0 + 1, b.ey - 1) * b.py, jd = (long long)min(j0 + 2, b.ey - 1) * b.py;
-    long long kz[4] = {(long long)max(k0 - 1, 0) * b.pz, (long long)k0 * b.pz,
-                       (long long)min(k0 + 1, b.ez - 1) * b.pz,
-                       (long long)min(k0 + 2, b.ez - 1) * b.pz};
+    const int gx[4] = {b.ox + max(i0 - 1, 0), b.ox + i0, b.ox + min(i0 + 1, b.ex - 1), b.ox + min(i0 + 2, b.ex - 1)};
+    const int gy[4] = {b.oy + max(j0 - 1, 0), b.oy + j0, b.oy + min(j0 + 1, b.ey - 1), b.oy + min(j0 + 2, b.ey - 1)};
+    const int gz[4] = {b.oz + max(k0 - 1, 0), b.oz + k0, b.oz + min(k0 + 1, b.ez - 1), b.oz + min(k0 + 2, b.ez - 1)};
+    // unclamped rows are four consecutive voxels
+    const bool run = i0 >= 1 && i0 + 2 <= b.ex - 1;
     double pl[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-        const T *pb = b.base + kz[c];
-        const T *r0 = pb + ja, *r1 = pb + jb, *r2 = pb + jc, *r3 = pb + jd;
-        double s0 = ((wx0 * tap(r0 + ia) + wx1 * tap(r0 + i0)) + wx2 * tap(r0 + ic)) + wx3 * tap(r0 + id);
-        double s1 = ((wx0 * tap(r1 + ia) + wx1 * tap(r1 + i0)) + wx2 * tap(r1 + ic)) + wx3 * tap(r1 + id);
-        double s2 = ((wx0 * tap(r2 + ia) + wx1 * tap(r2 + i0)) + wx2 * tap(r2 + ic)) + wx3 * tap(r2 + id);
-        double s3 = ((wx0 * tap(r3 + ia) + wx1 * tap(r3 + i0)) + wx2 * tap(r3 + ic)) + wx3 * tap(r3 + id);
-        pl[c] = ((wy0 * s0 + wy1 * s1) + wy2 * s2) + wy3 * s3;
+        double s[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double v[4];
+            if (run) {
+                b.vol.row4(gx[0], gy[r], gz[c], v);
+            } else {
+                v[0] = b.vol.at(gx[0], gy[r], gz[c]);
+                v[1] = b.vol.at(gx[1], gy[r], gz[c]);
+                v[2] = b.vol.at(gx[2], gy[r], gz[c]);
+                v[3] = b.vol.at(gx[3], gy[r], gz[c]);
+            }
+            s[r] = ((wx0 * v[0] + wx1 * v[1]) + wx2 * v[2]) + wx3 * v[3];
+        }
+        pl[c] = ((wy0 * s[0] + wy1 * s[1]) + wy2 * s[2]) + wy3 * s[3];
     }
     return ((wz0 * pl[0] + wz1 * pl[1]) + wz2 * pl[2]) + wz3 * pl[3];
 }
 
-template <class T>
-VR_D double sample(const Brick<T> &b, double x, double y, double z, bool cubic) {
+// ---------------------------------------------------- brick-layout sampling
+// The brick volume is read in 8-voxel windows: the 8-byte row of the brick
+// holding `base` (= first tap index rounded down to a multiple of 4) and the
+// same row of the next brick in x.  Every tap of a row lies in that window
+// (taps span at most 4 consecutive indices, clamping only pulls them
+// inwards), so all rows of a sample are fetched with independent loads
+// issued before any arithmetic -- one L2 round trip per interpolation instead
+// of one per row -- and each tap is a shift of the window.
+VR_D double window_tap(unsigned long long lo, unsigned long long hi, unsigned s) {
+    const unsigned long long w = s < 64 ? (lo >> s) : (hi >> (s - 64));
+    return (double)(short)(w & 0xffffull);
+}
+
+VR_D long long brick_row_y(const BrickVol &v, int gy) { return (long long)(gy >> 2) * v.bpy + ((gy & 3) << 2); }
+VR_D long long brick_row_z(const BrickVol &v, int gz) { return (long long)(gz >> 2) * v.bpz + ((gz & 3) << 4); }
+
+// _kernels.py:52-80 on the brick layout
+VR_D double tri_sample(const Block<BrickVol> &b, double x, double y, double z) {
+    x = clampf(x, 0.0, b.ex - 1.0);
+    y = clampf(y, 0.0, b.ey - 1.0);
+    z = clampf(z, 0.0, b.ez - 1.0);
+    int i0 = clampi((int)x, 0, b.ex - 2);
+    int j0 = clampi((int)y, 0, b.ey - 2);
+    int k0 = clampi((int)z, 0, b.ez - 2);
+    double fx = x - (double)i0;
+    double fy = y - (double)j0;
+    double fz = z - (double)k0;
+    const int gx = b.ox + i0, base = gx & ~3;
+    const unsigned s0 = 16u * (unsigned)(gx - base), s1 = s0 + 16u;
+    const bool need_hi = (gx - base) == 3;
+    const int16_t *px = b.vol.p + ((long long)(base >> 2) << 6);
+    const long long y0 = brick_row_y(b.vol, b.oy + j0), y1 = brick_row_y(b.vol, b.oy + j0 + 1);
+    const long long z0 = brick_row_z(b.vol, b.oz + k0), z1 = brick_row_z(b.vol, b.oz + k0 + 1);
+    const unsigned long long *q00 = reinterpret_cast<const unsigned long long *>(px + y0 + z0);
+    const unsigned long long *q10 = reinterpret_cast<const unsigned long long *>(px + y1 + z0);
+    const unsigned long long *q01 = reinterpret_cast<const unsigned long long *>(px + y0 + z1);
+    const unsigned long long *q11 = reinterpret_cast<const unsigned long long *>(px + y1 + z1);
+    const unsigned long long l00 = __ldg(q00), l10 = __ldg(q10), l01 = __ldg(q01), l11 = __ldg(q11);
+    unsigned long long h00 = 0, h10 = 0, h01 = 0, h11 = 0;
+    if (need_hi) {
+        h00 = __ldg(q00 + 16);
+        h10 = __ldg(q10 + 16);
+        h01 = __ldg(q01 + 16);
+        h11 = __ldg(q11 + 16);
+    }
+    double v000 = window_tap(l00, h00, s0), v100 = window_tap(l00, h00, s1);
+    double v010 = window_tap(l10, h10, s0), v110 = window_tap(l10, h10, s1);
+    double v001 = window_tap(l01, h01, s0), v101 = window_tap(l01, h01, s1);
+    double v011 = window_tap(l11, h11, s0), v111 = window_tap(l11, h11, s1);
+    double c00 = v000 + (v100 - v000) * fx;
+    double c10 = v010 + (v110 - v010) * fx;
+    double c01 = v001 + (v101 - v001) * fx;
+    double c11 = v011 + (v111 - v011) * fx;
+    double c0 = c00 + (c10 - c00) * fy;
+    double c1 = c01 + (c11 - c01) * fy;
+    return c0 + (c1 - c0) * fz;
+}
+
+// _kernels.py:94-143 on the brick layout: same taps, same x -> y -> z sums.
+VR_D double cub_sample(const Block<BrickVol> &b, double x, double y, double z) {
+    x = clampf(x, 0.0, b.ex - 1.0);
+    y = clampf(y, 0.0, b.ey - 1.0);
+    z = clampf(z, 0.0, b.ez - 1.0);
+    int i0 = clampi((int)x, 0, b.ex - 1);
+    int j0 = clampi((int)y, 0, b.ey - 1);
+    int k0 = clampi((int)z, 0, b.ez - 1);
+    double wx0, wx1, wx2, wx3, wy0, wy1, wy2, wy3, wz0, wz1, wz2, wz3;
+    cr_weights(x - (double)i0, wx0, wx1, wx2, wx3);
+    cr_weights(y - (double)j0, wy0, wy1, wy2, wy3);
+    cr_weights(z - (double)k0, wz0, wz1, wz2, wz3);
+    const int gx0 = b.ox + max(i0 - 1, 0), gx3 = b.ox + min(i0 + 2, b.ex - 1);
+    const int base = gx0 & ~3;
+    const unsigned s0 = 16u * (unsigned)(gx0 - base);
+    const unsigned s1 = 16u * (unsigned)(b.ox + i0 - base);
+    const unsigned s2 = 16u * (unsigned)(b.ox + min(i0 + 1, b.ex - 1) - base);
+    const unsigned s3 = 16u * (unsigned)(gx3 - base);
+    const bool need_hi = (gx3 - base) >= 4;
+    const int16_t *px = b.vol.p + ((long long)(base >> 2) << 6);
+    const long long yo[4] = {brick_row_y(b.vol, b.oy + max(j0 - 1, 0)), brick_row_y(b.vol, b.oy + j0),
+                             brick_row_y(b.vol, b.oy + min(j0 + 1, b.ey - 1)),
+                             brick_row_y(b.vol, b.oy + min(j0 + 2, b.ey - 1))};
+    const long long zo[4] = {brick_row_z(b.vol, b.oz + max(k0 - 1, 0)), brick_row_z(b.vol, b.oz + k0),
+                             brick_row_z(b.vol, b.oz + min(k0 + 1, b.ez - 1)),
+                             brick_row_z(b.vol, b.oz + min(k0 + 2, b.ez - 1))};
+    unsigned long long lo[16], hi[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const unsigned long long *q = reinterpret_cast<const unsigned long long *>(px + zo[c] + yo[r]);
+            lo[4 * c + r] = __ldg(q);
+            hi[4 * c + r] = need_hi ? __ldg(q + 16) : 0ull;
+        }
+    double pl[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        double s[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const unsigned long long l = lo[4 * c + r], h = hi[4 * c + r];
+            s[r] = ((wx0 * window_tap(l, h, s0) + wx1 * window_tap(l, h, s1)) + wx2 * window_tap(l, h, s2)) +
+                   wx3 * window_tap(l, h, s3);
+        }
+        pl[c] = ((wy0 * s[0] + wy1 * s[1]) + wy2 * s[2]) + wy3 * s[3];
+    }
+    return ((wz0 * pl[0] + wz1 * pl[1]) + wz2 * pl[2]) + wz3 * pl[3];
+}
+
+template <class V>
+VR_D double sample(const Block<V> &b, double x, double y, double z, bool cubic) {
     return cubic ? cub_sample(b, x, y, z) : tri_sample(b, x, y, z);
 }
 

@@ -313,6 +313,22 @@ __global__ void box_kernel(const Layout L, const VisArgs v) {
     }
 }
 
+// ----------------------------------------------------------- K1 bricks
+
+__global__ void __launch_bounds__(kBlock) brick_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
+                                                       int bnx, int bny, long long total, int16_t *bricks) {
+    long long py = nx, pz = (long long)nx * ny;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        long long b = e >> 6;
+        int w = (int)(e & 63);
+        int bx = (int)(b % bnx);
+        long long r = b / bnx;
+        int by = (int)(r % bny), bz = (int)(r / bny);
+        int x = bx * 4 + (w & 3), y = by * 4 + ((w >> 2) & 3), z = bz * 4 + (w >> 4);
+        bricks[e] = (x < nx && y < ny && z < nz) ? __ldg(vol + z * pz + y * py + x) : (int16_t)0;
+    }
+}
+
 // ------------------------------------------------------- transparency culling
 
 __global__ void __launch_bounds__(kBlock) cell_minmax_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
@@ -394,10 +410,11 @@ __global__ void __launch_bounds__(kBlock) sample_points_kernel(const int16_t *vo
                                                                double *out) {
     long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    Brick<int16_t> b;
-    b.base = vol;
-    b.py = nx;
-    b.pz = (long long)nx * ny;
+    Block<LinearVol> b;
+    b.vol.p = vol;
+    b.vol.py = nx;
+    b.vol.pz = (long long)nx * ny;
+    b.ox = b.oy = b.oz = 0;
     b.ex = nx;
     b.ey = ny;
     b.ez = nz;
@@ -578,6 +595,13 @@ cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs
     dim3 grid(v.nblocks, zsplit_for(L));
     aabb_kernel<<<grid, kBlock, 0, s>>>(vol, L, v);
     box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_brick_volume(const int16_t *vol, int nx, int ny, int nz, int16_t *bricks, cudaStream_t s) {
+    int bnx = (nx + 3) / 4, bny = (ny + 3) / 4, bnz = (nz + 3) / 4;
+    long long total = (long long)bnx * bny * bnz * 64;
+    brick_kernel<<<grid_for(total, kBlock, 148 * 64), kBlock, 0, s>>>(vol, nx, ny, nz, bnx, bny, total, bricks);
     return cudaGetLastError();
 }
 

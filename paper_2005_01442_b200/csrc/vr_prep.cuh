@@ -37,6 +37,11 @@ struct VisArgs {
 cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,
                               cudaStream_t s);
 
+// K1 brick upload: re-lay the x-fastest volume into 4x4x4 bricks of 64 voxels
+// (128 bytes, x fastest inside a brick, bricks x-fastest), padded with zeros
+// to whole bricks; bn* = ceil(n*/4).
+cudaError_t launch_brick_volume(const int16_t *vol, int nx, int ny, int nz, int16_t *bricks, cudaStream_t s);
+
 // Transparency culling support.  cells[c] = (min, max) of the voxels whose
 // index lies in [4c-1, 4c+5) per axis (clamped to the volume): every tap of a
 // trilinear or Catmull-Rom sample whose clamped base index floor(x) falls in

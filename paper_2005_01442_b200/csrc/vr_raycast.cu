@@ -89,23 +89,23 @@ VR_D int owner(const RenderArgs &a, int axis, double v) {
 // _attr_sample (_kernels.py:211-233) with the owning block already known:
 // local coordinates x - origin, taps clamped to the block, voxels read in
 // place from the volume (the atlas copy holds the same voxels).
-template <bool CUBIC, class T>
-VR_D double sample_in(const T *vol, const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z) {
-    const int ox = block_origin(a.L, bi), oy = block_origin(a.L, bj), oz = block_origin(a.L, bk);
-    Brick<T> b;
-    b.base = vol + (long long)oz * a.L.pz + (long long)oy * a.L.py + ox;
-    b.pz = a.L.pz;
-    b.py = a.L.py;
+template <bool CUBIC, class V>
+VR_D double sample_in(const V &vol, const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z) {
+    Block<V> b;
+    b.vol = vol;
+    b.ox = block_origin(a.L, bi);
+    b.oy = block_origin(a.L, bj);
+    b.oz = block_origin(a.L, bk);
     b.ex = block_extent(a.L, 0, bi);
     b.ey = block_extent(a.L, 1, bj);
     b.ez = block_extent(a.L, 2, bk);
-    const double lx = x - (double)ox, ly = y - (double)oy, lz = z - (double)oz;
+    const double lx = x - (double)b.ox, ly = y - (double)b.oy, lz = z - (double)b.oz;
     return CUBIC ? cub_sample(b, lx, ly, lz) : tri_sample(b, lx, ly, lz);
 }
 
 template <bool CUBIC>
 VR_D double attr_sample(const RenderArgs &a, double x, double y, double z) {
-    return sample_in<CUBIC>(a.vol, a, owner(a, 0, x), owner(a, 1, y), owner(a, 2, z), x, y, z);
+    return sample_in<CUBIC>(a.bv, a, owner(a, 0, x), owner(a, 1, y), owner(a, 2, z), x, y, z);
 }
 
 // _attr_grad (_kernels.py:236-253): six taps at +-0.5 voxel, each attributed
@@ -130,7 +130,7 @@ VR_D void attr_grad(const RenderArgs &a, double x, double y, double z, int bi, i
             pz = z + h;
             qk = owner(a, 2, pz);
         }
-        double s = sample_in<CUBIC>(a.vol, a, qi, qj, qk, px, py, pz);
+        double s = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
         if (q & 1)
             g[axis] = plus - s;
         else
@@ -144,7 +144,11 @@ VR_D void attr_grad(const RenderArgs &a, double x, double y, double z, int bi, i
 // _attr_rgba (_kernels.py:256-276)
 template <bool CUBIC>
 VR_D double attr_rgba(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z, int ch) {
-    double v = sample_in<CUBIC>(a.rgba + (long long)ch * a.rgba_plane, a, bi, bj, bk, x, y, z);
+    LinearU8 plane;
+    plane.p = a.rgba + (long long)ch * a.rgba_plane;
+    plane.py = a.L.py;
+    plane.pz = a.L.pz;
+    double v = sample_in<CUBIC>(plane, a, bi, bj, bk, x, y, z);
     return clampf(v / 255.0, 0.0, 1.0);
 }
 
@@ -276,10 +280,53 @@ VR_D long long leap_count(const RenderArgs &a, const Ray &r, const double inv[3]
     return k < 1 ? 1 : k;
 }
 
+// Number k >= 1 of samples, starting at the taken, provably transparent sample
+// n, that are all taken and provably transparent: they stay in the same
+// dilated culling cell (so the same min/max bound applies) and, on the block
+// path, in the same ownership cell and inside the same visibility box (so
+// the skip predicate stays false).  Computed positions are monotone in n, so
+// only the exit side of each interval needs the delta guard; the one-sample
+// slack absorbs the rounding of t.
+template <bool SKIP>
+VR_D long long culled_run(const RenderArgs &a, const Ray &r, const double inv[3], double t0, long long n, double t,
+                          const double p[3], const int bidx[3], int b) {
+    const double delta = 1e-6;
+    const double d[3] = {r.dx, r.dy, r.dz};
+    const double o[3] = {r.ox, r.oy, r.oz};
+    const double s[3] = {a.dsx.s, a.dsy.s, a.dsz.s};
+    double t_safe = DBL_MAX;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (d[k] == 0.0) continue;
+        const int g = (int)clampf(p[k], 0.0, (double)(a.L.n[k] - 1));
+        const int c = g >> 2, clast = (a.L.n[k] - 1) >> 2;
+        if (d[k] > 0.0 && c < clast) t_safe = dmin(t_safe, ((4.0 * (c + 1) - delta) * s[k] - o[k]) * inv[k]);
+        if (d[k] < 0.0 && c > 0) t_safe = dmin(t_safe, ((4.0 * c + delta) * s[k] - o[k]) * inv[k]);
+        if (SKIP) {
+            if (d[k] > 0.0 && bidx[k] < a.L.nb[k] - 1) {
+                double X = (1.0 + (double)((bidx[k] + 1) * a.L.stride)) - delta;
+                t_safe = dmin(t_safe, (X * s[k] - o[k]) * inv[k]);
+            } else if (d[k] < 0.0 && bidx[k] > 0) {
+                double X = (1.0 + (double)(bidx[k] * a.L.stride)) + delta;
+                t_safe = dmin(t_safe, (X * s[k] - o[k]) * inv[k]);
+            }
+            const double *bx = a.box + 6 * (long long)b;
+            const double edge = d[k] > 0.0 ? __ldg(bx + 3 + k) - delta : __ldg(bx + k) + delta;
+            t_safe = dmin(t_safe, (edge * s[k] - o[k]) * inv[k]);
+        }
+    }
+    if (!(t_safe > t)) return 1;
+    double q = (t_safe - t0) * a.inv_step - 0.5;
+    if (q > 4.0e15) return LLONG_MAX / 4;
+    long long m = (long long)floor(q) - 1;
+    long long k = m - n + 1;
+    return k < 1 ? 1 : k;
+}
+
 struct RayResult {
     double r, g, b, a;
     double depth;
-    long long taken, skipped, shaded;
+    long long taken, skipped, shaded, eval, iter;
 };
 
 // One pixel of _kernels.march (:343-594).
@@ -288,7 +335,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
     constexpr bool chained = (KIND == kIso) || (KIND == kPreint);  // _kernels.py:341
     RayResult res;
     double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
-    long long n_taken = 0, n_skip = 0, n_shaded = 0;
+    long long n_taken = 0, n_skip = 0, n_shaded = 0, n_eval = 0, n_iter = 0;
     double depth = __longlong_as_double(0x7ff8000000000000LL);  // NaN
     if (t1 >= t0) {
         const double step = a.step;
@@ -300,7 +347,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
         while (N > 0 && (t0 + ((double)(N - 1) + 0.5) * step) > t1) --N;
         const int nbx = a.L.nb[0], nby = a.L.nb[1];
         double inv[3] = {0.0, 0.0, 0.0};
-        if (SKIP) {
+        if (SKIP || (KIND == kPost && a.cull)) {
             inv[0] = r.dx != 0.0 ? 1.0 / r.dx : 0.0;
             inv[1] = r.dy != 0.0 ? 1.0 / r.dy : 0.0;
             inv[2] = r.dz != 0.0 ? 1.0 / r.dz : 0.0;
@@ -316,6 +363,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
         }
         long long n = 0;
         while (n < N) {
+            ++n_iter;
             const double t = t0 + ((double)n + 0.5) * step;
             const double x = divide(r.ox + t * r.dx, a.dsx);
             const double y = divide(r.oy + t * r.dy, a.dsy);
@@ -356,7 +404,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
 
             if (KIND == kIso) {
                 // _kernels.py:405-468
-                double s = sample_in<CUBIC>(a.vol, a, bi, bj, bk, x, y, z);
+                double s = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
                 if (!prev_valid && n > 0) {
                     double tp = t - step;
                     prev_s = attr_sample<CUBIC>(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
@@ -432,10 +480,16 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
             } else if (KIND == kPost) {
                 // post-classified (_kernels.py:508-537)
                 if (cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis)) {
-                    ++n;
+                    const double p[3] = {x, y, z};
+                    const int bidx[3] = {bi, bj, bk};
+                    long long k = culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, b);
+                    if (k > N - n) k = N - n;
+                    n_taken += k - 1;
+                    n += k;
                     continue;
                 }
-                double s = sample_in<CUBIC>(a.vol, a, bi, bj, bk, x, y, z);
+                ++n_eval;
+                double s = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
                 int sbin = lut_bin(s, a.lut_lo, a.lut_inv_w, a.nlut);
                 double sa = __ldg(a.lut + 4 * sbin + 3);
                 if (sa > 0.0) {
@@ -458,7 +512,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 }
             } else {
                 // pre-integrated (_kernels.py:538-581)
-                double s = sample_in<CUBIC>(a.vol, a, bi, bj, bk, x, y, z);
+                double s = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
                 if (!prev_valid && n > 0) {
                     double tp = t - step;
                     prev_s = attr_sample<CUBIC>(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
@@ -513,6 +567,8 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
     res.taken = n_taken;
     res.skipped = n_skip;
     res.shaded = n_shaded;
+    res.eval = KIND == kPost ? n_eval : n_taken;
+    res.iter = n_iter;
     return res;
 }
 
@@ -527,7 +583,10 @@ VR_D unsigned long long warp_sum(unsigned long long v) {
 }
 
 template <int KIND, bool CUBIC, bool LIGHT, bool SKIP>
-__global__ void __launch_bounds__(kThreads) raycast_kernel(const __grid_constant__ RenderArgs a) {
+#ifndef VR_RAYCAST_MIN_BLOCKS
+#define VR_RAYCAST_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kThreads, VR_RAYCAST_MIN_BLOCKS) raycast_kernel(const __grid_constant__ RenderArgs a) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lx = (warp & 1) * 8 + (lane & 7);   // 0..15 inside the 16x8 cell
     const int ly = (warp >> 1) * 4 + (lane >> 3);  // 0..7; each warp an 8x4 tile
@@ -536,7 +595,7 @@ __global__ void __launch_bounds__(kThreads) raycast_kernel(const __grid_constant
     const int cx = (cell % a.cells_x) * kTileW + lx;
     const int cy = (cell / a.cells_x) * kTileH + ly;
     const bool active = cell < a.ncells && cx < a.tw && cy < a.th;
-    unsigned long long taken = 0, skipped = 0, shaded = 0;
+    unsigned long long taken = 0, skipped = 0, shaded = 0, evals = 0, iters = 0;
     if (active) {
         Ray r = make_ray(a, a.tx + cx, a.ty + cy);
         double t0, t1;
@@ -565,20 +624,308 @@ __global__ void __launch_bounds__(kThreads) raycast_kernel(const __grid_constant
         taken = (unsigned long long)res.taken;
         skipped = (unsigned long long)res.skipped;
         shaded = (unsigned long long)res.shaded;
+        evals = (unsigned long long)res.eval;
+        iters = (unsigned long long)res.iter;
     }
     taken = warp_sum(taken);
     skipped = warp_sum(skipped);
-    shaded = warp_sum(shaded);
-    if (lane == 0) {
-        if (a.totals && (taken | skipped)) {
-            atomicAdd(a.totals, taken);
-            atomicAdd(a.totals + 1, skipped);
+    if (lane == 0 && a.totals && (taken | skipped)) {
+        atomicAdd(a.totals, taken);
+        atomicAdd(a.totals + 1, skipped);
+    }
+    if (a.work) {
+        shaded = warp_sum(shaded);
+        evals = warp_sum(evals);
+        iters = warp_sum(iters);
+        if (lane == 0) {
+            if (shaded) atomicAdd(a.work, shaded);
+            if (evals) atomicAdd(a.work + 1, evals);
+            if (iters) atomicAdd(a.work + 2, iters);
         }
-        if (a.shaded && shaded) atomicAdd(a.shaded, shaded);
+    }
+}
+
+// ------------------------------------------------- persistent post-classified
+// The headline path (post-classified DVR, _kernels.py:343-404, 508-537,
+// 583-594) as a persistent kernel.  Ray cost is extremely uneven (a grazing
+// ray near bone takes ~700 samples, most rays none), so one ray per thread
+// leaves a warp's lanes idle behind its slowest ray.  Here every lane pulls
+// rays from a global counter (work items in 8x4-tile order, so a warp's rays
+// stay coherent) and takes the next one as soon as its ray ends.  Each trip a
+// lane advances its ray by a bounded number of cheap steps -- skip-predicate
+// leaps, culled runs -- until it needs an interpolation, then all lanes with
+// pending work evaluate one interpolation together: the sample (stage 0) or
+// one of the six gradient taps (stages 1..6, in the reference's
+// +x,-x,+y,-y,+z,-z order).  Every sample's arithmetic is unchanged.
+
+struct PostRay {
+    Ray r;
+    double inv[3];
+    double t0;
+    long long n, N;
+    double acc_r, acc_g, acc_b, acc_a;
+    double x, y, z;
+    double sr, sg, sb, ahat, gplus, gx, gy, gz;
+    long long taken, skipped;
+    int bi, bj, bk;
+    int stage;     // -1 none pending, 0 sample, 1..6 gradient taps
+    int last_hit;
+    long long out;  // output index of the pixel
+    bool live;
+};
+
+constexpr int kPhaseACap = 8;  // cheap steps a lane may take per trip
+
+// Work item -> pixel.  Items are numbered cell slot by cell slot, 128 per
+// slot, each 32-item group one 8x4 warp tile (the layout of raycast_kernel).
+VR_D bool start_ray(const RenderArgs &a, long long item, PostRay &R) {
+    const int slot = (int)(item >> 7), local = (int)(item & 127);
+    const int w = local >> 5, l = local & 31;
+    const int lx = (w & 1) * 8 + (l & 7), ly = (w >> 1) * 4 + (l >> 3);
+    const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
+    const int cx = (cell % a.cells_x) * kTileW + lx;
+    const int cy = (cell / a.cells_x) * kTileH + ly;
+    if (cell >= a.ncells || cx >= a.tw || cy >= a.th) return false;
+    R.out = a.il_n > 1 ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx : (long long)cy * a.tw + cx;
+    R.r = make_ray(a, a.tx + cx, a.ty + cy);
+    double t0, t1;
+    clip_to_bounds(R.r, a.ext_mm, t0, t1);
+    R.t0 = t0;
+    R.N = 0;
+    if (t1 >= t0) {
+        long long nsteps = (long long)ceil((t1 - t0) / a.step);
+        if (nsteps < 1) nsteps = 1;
+        long long N = nsteps;
+        while (N > 0 && (t0 + ((double)(N - 1) + 0.5) * a.step) > t1) --N;
+        R.N = N;
+    }
+    R.inv[0] = R.r.dx != 0.0 ? 1.0 / R.r.dx : 0.0;
+    R.inv[1] = R.r.dy != 0.0 ? 1.0 / R.r.dy : 0.0;
+    R.inv[2] = R.r.dz != 0.0 ? 1.0 / R.r.dz : 0.0;
+    R.n = 0;
+    R.acc_r = R.acc_g = R.acc_b = R.acc_a = 0.0;
+    R.taken = R.skipped = 0;
+    R.stage = -1;
+    R.last_hit = -1;
+    R.live = true;
+    return true;
+}
+
+template <bool CUBIC, bool LIGHT, bool SKIP>
+__global__ void __launch_bounds__(kThreads) raycast_post_kernel(const __grid_constant__ RenderArgs a) {
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const long long total = (long long)a.slots * (kTileW * kTileH);
+    const int nbx = a.L.nb[0], nby = a.L.nb[1];
+    const bool cull = a.cull != 0;
+    const int first_vis = cull ? __ldg(a.lut_range) : 0;
+    const int last_vis = cull ? __ldg(a.lut_range + 1) : 0;
+    unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
+    PostRay R;
+    R.live = false;
+    bool exhausted = false;
+    for (;;) {
+        // ---- fetch rays for idle lanes (one atomic per warp)
+        const bool want = !R.live && !exhausted;
+        const unsigned m = __ballot_sync(full, want);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(a.work_counter, (unsigned long long)__popc(m));
+            base = __shfl_sync(full, base, leader);
+            if (want) {
+                const long long item = (long long)base + __popc(m & ((1u << lane) - 1u));
+                if (item >= total)
+                    exhausted = true;
+                else
+                    start_ray(a, item, R);
+            }
+        }
+        if (__all_sync(full, !R.live && exhausted)) break;
+        if (!R.live) continue;
+
+        // ---- phase A: cheap steps until an interpolation is needed
+        int steps = 0;
+        while (R.stage < 0 && R.n < R.N && steps < kPhaseACap) {
+            ++steps;
+            ++c_iter;
+            const long long n = R.n;
+            const double t = R.t0 + ((double)n + 0.5) * a.step;
+            const double x = divide(R.r.ox + t * R.r.dx, a.dsx);
+            const double y = divide(R.r.oy + t * R.r.dy, a.dsy);
+            const double z = divide(R.r.oz + t * R.r.dz, a.dsz);
+            const int bi = owner(a, 0, x), bj = owner(a, 1, y), bk = owner(a, 2, z);
+            const int b = (bk * nby + bj) * nbx + bi;
+            const double p[3] = {x, y, z};
+            const int bidx[3] = {bi, bj, bk};
+            if (SKIP) {
+                bool skippable, cell_only = true;
+                if (__ldg(a.empty + b) == 1) {
+                    skippable = true;
+                } else {
+                    const double *bx = a.box + 6 * (long long)b;
+                    skippable = x < __ldg(bx) || x > __ldg(bx + 3) || y < __ldg(bx + 1) ||
+                                y > __ldg(bx + 4) || z < __ldg(bx + 2) || z > __ldg(bx + 5);
+                    cell_only = false;
+                }
+                if (skippable) {
+                    long long k = leap_count<kPost>(a, R.r, R.inv, R.t0, n, t, p, bidx, b, cell_only);
+                    if (k > R.N - n) k = R.N - n;
+                    R.skipped += k;
+                    R.n = n + k;
+                    continue;
+                }
+            }
+            if (b != R.last_hit) {
+                if (a.blocks_hit) a.blocks_hit[b] = 1;
+                R.last_hit = b;
+            }
+            if (cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis)) {
+                long long k = culled_run<SKIP>(a, R.r, R.inv, R.t0, n, t, p, bidx, b);
+                if (k > R.N - n) k = R.N - n;
+                R.taken += k;
+                R.n = n + k;
+                continue;
+            }
+            R.taken += 1;
+            R.x = x;
+            R.y = y;
+            R.z = z;
+            R.bi = bi;
+            R.bj = bj;
+            R.bk = bk;
+            R.stage = 0;
+        }
+
+        // ---- phase B: one interpolation per lane with pending work
+        bool finished = false;
+        if (R.stage >= 0) {
+            double px = R.x, py = R.y, pz = R.z;
+            int qi = R.bi, qj = R.bj, qk = R.bk;
+            if (LIGHT && R.stage > 0) {
+                const int q = R.stage - 1;
+                const double h = (q & 1) ? -0.5 : 0.5;
+                if (q < 2) {
+                    px = R.x + h;
+                    qi = owner(a, 0, px);
+                } else if (q < 4) {
+                    py = R.y + h;
+                    qj = owner(a, 1, py);
+                } else {
+                    pz = R.z + h;
+                    qk = owner(a, 2, pz);
+                }
+            }
+            const double v = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
+            ++c_eval;
+            bool composite = false;
+            if (R.stage == 0) {
+                const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
+                const double sa = __ldg(a.lut + 4 * sbin + 3);
+                if (sa > 0.0) {
+                    R.sr = __ldg(a.lut + 4 * sbin);
+                    R.sg = __ldg(a.lut + 4 * sbin + 1);
+                    R.sb = __ldg(a.lut + 4 * sbin + 2);
+                    R.ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
+                    if (LIGHT)
+                        R.stage = 1;
+                    else
+                        composite = true;
+                } else {
+                    R.stage = -1;
+                    R.n += 1;
+                }
+            } else {
+                const int q = R.stage - 1;
+                if (q & 1) {
+                    const double dg = R.gplus - v;
+                    if (q == 1) R.gx = dg;
+                    else if (q == 3) R.gy = dg;
+                    else R.gz = dg;
+                } else {
+                    R.gplus = v;
+                }
+                if (R.stage < 6) {
+                    R.stage += 1;
+                } else {
+                    const double gx = divide(R.gx, a.dsx), gy = divide(R.gy, a.dsy), gz = divide(R.gz, a.dsz);
+                    ++c_shaded;
+                    const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                    if (norm > 1e-12)
+                        shade(a, R.sr, R.sg, R.sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
+                    composite = true;
+                }
+            }
+            if (composite) {
+                const double w = (1.0 - R.acc_a) * R.ahat;
+                R.acc_r += w * R.sr;
+                R.acc_g += w * R.sg;
+                R.acc_b += w * R.sb;
+                R.acc_a += w;
+                R.stage = -1;
+                R.n += 1;
+                if (R.acc_a >= a.term_alpha) finished = true;  // early ray termination
+            }
+        }
+        if (R.stage < 0 && R.n >= R.N) finished = true;
+
+        // ---- finish: background, epilogue, per-pixel outputs
+        if (finished) {
+            const double w = 1.0 - R.acc_a;
+            const double rr = R.acc_r + w * a.bg[0] * a.bg[3];
+            const double gg = R.acc_g + w * a.bg[1] * a.bg[3];
+            const double bb = R.acc_b + w * a.bg[2] * a.bg[3];
+            const double aa = R.acc_a + w * a.bg[3];
+            const long long p = R.out;
+            if (a.premult) reinterpret_cast<double4 *>(a.premult)[p] = make_double4(rr, gg, bb, aa);
+            if (a.pixels) {
+                double r0 = 0.0, g0 = 0.0, b0 = 0.0;
+                if (aa > 0.0) {
+                    const double den = aa > 1e-12 ? aa : 1e-12;
+                    r0 = rr / den;
+                    g0 = gg / den;
+                    b0 = bb / den;
+                }
+                reinterpret_cast<uchar4 *>(a.pixels)[p] = make_uchar4(to_u8(r0), to_u8(g0), to_u8(b0), to_u8(aa));
+            }
+            if (a.depth) a.depth[p] = __longlong_as_double(0x7ff8000000000000LL);
+            if (a.taken) a.taken[p] = R.taken;
+            if (a.skipped) a.skipped[p] = R.skipped;
+            c_taken += (unsigned long long)R.taken;
+            c_skip += (unsigned long long)R.skipped;
+            R.live = false;
+        }
+    }
+    c_taken = warp_sum(c_taken);
+    c_skip = warp_sum(c_skip);
+    if (lane == 0 && a.totals && (c_taken | c_skip)) {
+        atomicAdd(a.totals, c_taken);
+        atomicAdd(a.totals + 1, c_skip);
+    }
+    if (a.work) {
+        c_shaded = warp_sum(c_shaded);
+        c_eval = warp_sum(c_eval);
+        c_iter = warp_sum(c_iter);
+        if (lane == 0) {
+            if (c_shaded) atomicAdd(a.work, c_shaded);
+            if (c_eval) atomicAdd(a.work + 1, c_eval);
+            if (c_iter) atomicAdd(a.work + 2, c_iter);
+        }
     }
 }
 
 using KernelFn = void (*)(RenderArgs);
+
+template <bool CUBIC, bool LIGHT>
+KernelFn pick_post(bool skip) {
+    return skip ? raycast_post_kernel<CUBIC, LIGHT, true> : raycast_post_kernel<CUBIC, LIGHT, false>;
+}
+
+KernelFn pick_persistent(const RenderArgs &a) {
+    const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
+    if (c) return l ? pick_post<true, true>(s) : pick_post<true, false>(s);
+    return l ? pick_post<false, true>(s) : pick_post<false, false>(s);
+}
 
 template <int KIND, bool CUBIC, bool LIGHT>
 KernelFn pick_skip(bool skip) {
@@ -610,6 +957,20 @@ KernelFn pick(const RenderArgs &a) {
 cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
     if (a.tw <= 0 || a.th <= 0) return cudaSuccess;
     if (a.slots <= 0) return cudaSuccess;
+    if (a.mode == 0 && a.classify == 0 && a.work_counter) {
+        // persistent: enough CTAs to fill every SM at the kernel's occupancy
+        KernelFn k = pick_persistent(a);
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
+        long long ctas = (long long)sms * (per_sm > 0 ? per_sm : 1);
+        if (ctas > a.slots) ctas = a.slots;
+        cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), stream);
+        if (e != cudaSuccess) return e;
+        k<<<(unsigned)ctas, kThreads, 0, stream>>>(a);
+        return cudaGetLastError();
+    }
     pick(a)<<<a.slots, kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }

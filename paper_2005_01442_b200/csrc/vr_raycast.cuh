@@ -7,6 +7,7 @@ namespace vr {
 struct RenderArgs {
     // volume and its block layout (monolithic = one block spanning the volume)
     const int16_t *vol;
+    BrickVol bv;  // the same voxels in 4^3 bricks (K1), read by every interpolation
     Layout L;
     Divisor dsx, dsy, dsz;  // spacing divisors (x = (o + t*d) / s)
     double ext_mm[3];       // (n-1)*s, volume.py:62-67
@@ -49,6 +50,8 @@ struct RenderArgs {
     const int *lut_range;
     int cull;
 
+    unsigned long long *work_counter;  // persistent kernel's ray queue head (zeroed per launch)
+
     // outputs (all optional)
     uint8_t *pixels;
     double *premult;
@@ -56,7 +59,7 @@ struct RenderArgs {
     long long *taken, *skipped;
     uint8_t *blocks_hit;
     unsigned long long *totals;  // [0] taken, [1] skipped
-    unsigned long long *shaded;  // [0] gradient evaluations
+    unsigned long long *work;    // [0] gradient evaluations, [1] interpolations, [2] loop iterations
 };
 
 // CTA = 16 x 8 pixels, four warps, each warp an 8 x 4 screen tile so that the

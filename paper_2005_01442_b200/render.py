@@ -456,7 +456,7 @@ class Renderer:
         o.skipped = _lib.ptr(self.skipped).value
         o.blocks_hit = _lib.ptr(self.blocks_hit).value
         o.totals = self.totals.data_ptr()
-        o.shaded = self.totals.data_ptr() + 5 * 8
+        o.work = self.totals.data_ptr() + 5 * 8
         if self._events:
             o.ev_start, o.ev_stop = self._events[0].value, self._events[1].value
         return o
@@ -466,7 +466,7 @@ class Renderer:
         torch = self.torch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.totals[0:2].zero_()
-        self.totals[5].zero_()
+        self.totals[5:8].zero_()
         out = self.outputs()
         _lib.check(_lib.load().vr_render(
             self.dvol.handle, self.dgrid.handle if self.dgrid else None, ctypes.byref(self.cam),
@@ -477,6 +477,7 @@ class Renderer:
         t = self.totals.cpu().tolist()
         return {"samples_taken": t[0], "samples_skipped": t[1], "blocks_visited": t[2],
                 "blocks_empty": t[3], "empty_block_errors": t[4], "shaded": t[5],
+                "interpolated": t[6], "march_iterations": t[7],
                 "blocks_total": self.dgrid.count if self.dgrid else 1,
                 "rays": self.cam.tile_w * self.cam.tile_h if not self.interleave else self.npix}
 
