@@ -212,12 +212,15 @@ int vr_gradient_points(const vr_volume *vol, const double *pts, int64_t n, int c
 /* Number of voxels with value >= thr (builder-defined, no
  * reference function).  count: device uint64 (accumulated; zero it first). */
 int vr_threshold_count(const vr_volume *vol, int32_t thr, uint64_t *count, void *stream);
-/* Method-of-spheres voxel form: for each ball q (centre mm, radius mm) the
- * number of member voxels -- value >= thr and centre (i*sx,j*sy,k*sz) with
- * ((dx^2 + dy^2) + dz^2) <= r^2 -- and the number of their exposed faces (a
- * 6-neighbour below thr or outside the volume), giving V = count * voxel
- * volume and a face-count surface S for SVR = S / V.  centres (nballs,3), radii (nballs) device
- * float64; counts/faces device uint64 (overwritten).  faces may be NULL. */
+/* Method-of-spheres voxel form: for each ball q (centre
+ * mm, radius mm), the member voxels -- value >= thr and centre
+ * (i*sx, j*sy, k*sz) with ((dx^2 + dy^2) + dz^2) <= r^2 -- are counted, and
+ * their exposed faces (6-neighbour below thr or outside the volume) per
+ * axis: faces[3q+0] x-faces (area sy*sz each), [3q+1] y-faces (sx*sz),
+ * [3q+2] z-faces (sx*sy).  V = count * sx*sy*sz, S = sum of face areas,
+ * SVR = S / V.  centres (nballs,3), radii (nballs) device float64;
+ * counts (nballs) and faces (nballs*3) device uint64, overwritten; faces may
+ * be NULL. */
 int vr_ball_counts(const vr_volume *vol, int32_t thr, const double *centres,
                    const double *radii, int64_t nballs, uint64_t *counts, uint64_t *faces,
                    void *stream);

@@ -749,11 +749,12 @@ uint64_t vro_threshold_count(const int16_t *vals, int64_t n, int32_t thr) {
  * ((dx^2 + dy^2) + dz^2) in float64. */
 void vro_ball_counts(const int16_t *vals, int64_t nx, int64_t ny, int64_t nz, double sx,
                      double sy, double sz, int32_t thr, const double *centres,
-                     const double *radii, int64_t nballs, uint64_t *counts) {
+                     const double *radii, int64_t nballs, uint64_t *counts, uint64_t *faces) {
+    const int64_t py = nx, pz = nx * ny;
     for (int64_t q = 0; q < nballs; ++q) {
         double cx = centres[3 * q], cy = centres[3 * q + 1], cz = centres[3 * q + 2];
         double r2 = radii[q] * radii[q];
-        uint64_t c = 0;
+        uint64_t c = 0, f[3] = {0, 0, 0};
         for (int64_t k = 0; k < nz; ++k) {
             double dz = (double)k * sz - cz;
             for (int64_t j = 0; j < ny; ++j) {
@@ -761,10 +762,21 @@ void vro_ball_counts(const int16_t *vals, int64_t nx, int64_t ny, int64_t nz, do
                 const int16_t *row = vals + (k * ny + j) * nx;
                 for (int64_t i = 0; i < nx; ++i) {
                     double dx = (double)i * sx - cx;
-                    if (row[i] >= thr && (dx * dx + dy * dy) + dz * dz <= r2) c++;
+                    if (!(row[i] >= thr && (dx * dx + dy * dy) + dz * dz <= r2)) continue;
+                    c++;
+                    const int16_t *p = row + i;
+                    /* exposed faces: neighbour below thr or outside the volume */
+                    f[0] += (i == 0 || p[-1] < thr) + (i == nx - 1 || p[1] < thr);
+                    f[1] += (j == 0 || p[-py] < thr) + (j == ny - 1 || p[py] < thr);
+                    f[2] += (k == 0 || p[-pz] < thr) + (k == nz - 1 || p[pz] < thr);
                 }
             }
         }
         counts[q] = c;
+        if (faces) {
+            faces[3 * q] = f[0];
+            faces[3 * q + 1] = f[1];
+            faces[3 * q + 2] = f[2];
+        }
     }
 }

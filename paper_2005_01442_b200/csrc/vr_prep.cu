@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kBlock) ball_kernel(const int16_t *__restrict_
     int i0 = max(0, (int)floor((cx - rad) / sx) - 1), i1 = min(nx - 1, (int)ceil((cx + rad) / sx) + 1);
     int j0 = max(0, (int)floor((cy - rad) / sy) - 1), j1 = min(ny - 1, (int)ceil((cy + rad) / sy) + 1);
     int k0 = max(0, (int)floor((cz - rad) / sz) - 1), k1 = min(nz - 1, (int)ceil((cz + rad) / sz) + 1);
-    unsigned long long c = 0, f = 0;
+    unsigned long long c = 0, fx = 0, fy = 0, fz = 0;
     if (i0 <= i1 && j0 <= j1 && k0 <= k1) {
         int wx = i1 - i0 + 1, wy = j1 - j0 + 1;
         long long cnt = (long long)wx * wy * (k1 - k0 + 1);
@@ -488,31 +488,32 @@ __global__ void __launch_bounds__(kBlock) ball_kernel(const int16_t *__restrict_
             if (__ldg(p) < thr) continue;
             c += 1;
             if (faces) {
-                f += (i == 0 || __ldg(p - 1) < thr) ? 1 : 0;
-                f += (i == nx - 1 || __ldg(p + 1) < thr) ? 1 : 0;
-                f += (j == 0 || __ldg(p - py) < thr) ? 1 : 0;
-                f += (j == ny - 1 || __ldg(p + py) < thr) ? 1 : 0;
-                f += (k == 0 || __ldg(p - pz) < thr) ? 1 : 0;
-                f += (k == nz - 1 || __ldg(p + pz) < thr) ? 1 : 0;
+                // exposed faces: 6-neighbour below thr or outside the volume
+                fx += ((i == 0 || __ldg(p - 1) < thr) ? 1 : 0) + ((i == nx - 1 || __ldg(p + 1) < thr) ? 1 : 0);
+                fy += ((j == 0 || __ldg(p - py) < thr) ? 1 : 0) + ((j == ny - 1 || __ldg(p + py) < thr) ? 1 : 0);
+                fz += ((k == 0 || __ldg(p - pz) < thr) ? 1 : 0) + ((k == nz - 1 || __ldg(p + pz) < thr) ? 1 : 0);
             }
         }
     }
     c = warp_sum(c);
-    f = warp_sum(f);
-    __shared__ unsigned long long pc[kBlock / 32], pf[kBlock / 32];
+    fx = warp_sum(fx);
+    fy = warp_sum(fy);
+    fz = warp_sum(fz);
+    __shared__ unsigned long long part[4][kBlock / 32];
     if ((threadIdx.x & 31) == 0) {
-        pc[threadIdx.x >> 5] = c;
-        pf[threadIdx.x >> 5] = f;
+        part[0][threadIdx.x >> 5] = c;
+        part[1][threadIdx.x >> 5] = fx;
+        part[2][threadIdx.x >> 5] = fy;
+        part[3][threadIdx.x >> 5] = fz;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long sc = 0, sf = 0;
-        for (int w = 0; w < kBlock / 32; ++w) {
-            sc += pc[w];
-            sf += pf[w];
-        }
-        counts[q] = sc;
-        if (faces) faces[q] = sf;
+    if (threadIdx.x < 4) {
+        unsigned long long s = 0;
+        for (int w = 0; w < kBlock / 32; ++w) s += part[threadIdx.x][w];
+        if (threadIdx.x == 0)
+            counts[q] = s;
+        else if (faces)
+            faces[3 * q + threadIdx.x - 1] = s;
     }
 }
 

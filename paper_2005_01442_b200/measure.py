@@ -44,15 +44,15 @@ def threshold_volume_mm3(volume, thr: int, device: int = 0) -> float:
 
 
 def ball_counts(volume, thr: int, centres, radii, device: int = 0):
-    """(counts, faces) uint64 arrays, one entry per ball."""
+    """(counts (nballs,), faces (nballs, 3) exposed faces per axis) as uint64."""
     torch, dvol, dev = _dev(volume, device)
     c = np.ascontiguousarray(centres, dtype=np.float64).reshape(-1, 3)
-    r = np.ascontiguousarray(np.broadcast_to(np.asarray(radii, dtype=np.float64), (c.shape[0],)))
+    r = np.array(np.broadcast_to(np.asarray(radii, dtype=np.float64), (c.shape[0],)))
     n = c.shape[0]
     ct = torch.from_numpy(c).to(dev)
     rt = torch.from_numpy(r).to(dev)
     counts = torch.empty(n, dtype=torch.int64, device=dev)
-    faces = torch.empty(n, dtype=torch.int64, device=dev)
+    faces = torch.empty((n, 3), dtype=torch.int64, device=dev)
     _lib.check(_lib.load().vr_ball_counts(dvol.handle, int(thr), _lib.ptr(ct), _lib.ptr(rt), n,
                                           _lib.ptr(counts), _lib.ptr(faces),
                                           _lib.ptr_stream(torch.cuda.current_stream(dev))))
@@ -63,11 +63,9 @@ def ball_measure(volume, thr: int, centres, radii, device: int = 0) -> dict:
     """V (mm^3), S (mm^2) and SVR = S/V per ball (NaN where V == 0)."""
     counts, faces = ball_counts(volume, thr, centres, radii, device)
     sx, sy, sz = volume.spacing
-    # faces are counted per axis-agnostic unit; weight by the mean face area
-    # only when spacing is isotropic, else report the per-axis-exact count
-    voxel = sx * sy * sz
-    V = counts.astype(np.float64) * voxel
-    S = faces.astype(np.float64) * ((sx * sy + sy * sz + sx * sz) / 3.0)
+    V = counts.astype(np.float64) * (sx * sy * sz)
+    f = faces.astype(np.float64)
+    S = (f[:, 0] * (sy * sz) + f[:, 1] * (sx * sz)) + f[:, 2] * (sx * sy)
     with np.errstate(divide="ignore", invalid="ignore"):
         svr = np.where(V > 0, S / V, np.nan)
     return {"count": counts, "faces": faces, "V_mm3": V, "S_mm2": S, "svr": svr}
