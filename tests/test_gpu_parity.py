@@ -196,3 +196,74 @@ def test_threshold_count_vs_oracle(vr):
     m = vr.ball_measure(vol, 550, centres, radii)
     sx, sy, sz = vol.spacing
     assert np.allclose(m["V_mm3"], want * (sx * sy * sz))
+
+
+# ----------------------------------------------------------- full sizes
+
+SURVEY_STATS = {
+    # SURVEY.md section 6, measured from the unmodified reference: (dims, size,
+    # settings, samples_taken, samples_skipped, blocks total/empty/visited)
+    "c1_pinhole_mono": ((64, 64, 64), 128, dict(interpolation="tricubic"), 1497332, 0, (1, 0, 1)),
+    "c1_blocks": ((64, 64, 64), 128, dict(interpolation="tricubic", use_blocks=True), 187643, 1309689, (1, 0, 1)),
+    "c2_blocks": ((256, 256, 256), 512, dict(interpolation="tricubic", use_blocks=True), 2350246, 94500169,
+                  (125, 110, 15)),
+    "c3_blocks": ((512, 512, 512), 1024, dict(interpolation="tricubic", use_blocks=True), 8879559, 767407605,
+                  (729, 675, 46)),
+}
+
+
+def _centered(vr, dims, size):
+    ext = tuple(float(d - 1) for d in dims)
+    c = tuple(0.5 * e for e in ext)
+    return vr.Camera(position=(c[0] + 2.2 * max(ext), c[1], c[2]), look_at=c, width=size, height=size)
+
+
+@pytest.mark.parametrize("key", sorted(SURVEY_STATS))
+def test_reference_stats_at_benchmark_sizes(vr, key):
+    """RenderStats equal the numbers the unmodified reference produced."""
+    dims, size, kw, taken, skipped, blocks = SURVEY_STATS[key]
+    vol = vr.generate_phantom("torso", dims)
+    img = vr.render(vol, _centered(vr, dims, size), vr.get_preset("bone"), vr.RenderSettings(**kw))
+    st = img.stats
+    assert (st.samples_taken, st.samples_skipped) == (taken, skipped)
+    assert (st.blocks_total, st.blocks_empty, st.blocks_visited) == blocks
+
+
+def test_full_c3_frame_bit_exact_vs_oracle(vr):
+    """The headline frame (512^3 -> 1024^2, tricubic, bricks 64/3, bone,
+    lighting) against the CPU restatement of the reference, every pixel."""
+    from oracle import oracle as O
+
+    dims = (512, 512, 512)
+    vol = vr.generate_phantom("torso", dims)
+    cam = _centered(vr, dims, 1024)
+    tf = vr.get_preset("bone")
+    s = vr.RenderSettings(interpolation="tricubic", use_blocks=True)
+    img = vr.render(vol, cam, tf, s, return_premultiplied=True)
+    ref = O.render(vol.values, vol.spacing, cam, tf.values, tf.rgba, tf.domain, s)
+    assert np.array_equal(img.premultiplied, ref.out)
+    assert np.array_equal(img.pixels, ref.pixels)
+    assert img.stats.samples_taken == ref.samples_taken
+    assert img.stats.samples_skipped == ref.samples_skipped
+    assert img.stats.blocks_visited == ref.blocks_visited
+
+
+@pytest.mark.parametrize("tfname,interp", [("soft-tissue", "tricubic"), ("bone", "trilinear"),
+                                            ("grayscale", "tricubic")])
+def test_128_cube_vs_oracle(vr, tfname, interp):
+    from oracle import oracle as O
+
+    dims = (128, 112, 96)
+    vol = vr.generate_phantom("torso", dims, (0.9, 1.0, 1.3))
+    ext = vol.extent_mm
+    c = tuple(0.5 * e for e in ext)
+    cam = vr.Camera(position=(c[0] + 150.0, c[1] - 90.0, c[2] + 60.0), look_at=c, up=(0.0, 0.2, 1.0),
+                    vertical_fov_deg=35.0, width=160, height=120)
+    tf = vr.get_preset(tfname)
+    for use_blocks in (False, True):
+        s = vr.RenderSettings(interpolation=interp, use_blocks=use_blocks, block_size=32, overlap=3)
+        img = vr.render(vol, cam, tf, s, return_premultiplied=True)
+        ref = O.render(vol.values, vol.spacing, cam, tf.values, tf.rgba, tf.domain, s)
+        assert np.array_equal(img.premultiplied, ref.out), (tfname, interp, use_blocks)
+        assert img.stats.samples_taken == ref.samples_taken
+        assert img.stats.samples_skipped == ref.samples_skipped
