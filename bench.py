@@ -67,7 +67,17 @@ def parse():
     p.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    return p.parse_args()
+    p.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
+                   help="override a RenderSettings field of the config (ablations)")
+    args = p.parse_args()
+    for kv in args.set:
+        key, val = kv.split("=", 1)
+        try:
+            CONFIGS[args.config]["settings"][key] = json.loads(val)
+        except json.JSONDecodeError:
+            CONFIGS[args.config]["settings"][key] = val
+        CONFIGS[args.config]["desc"] += f" [{kv}]"
+    return args
 
 
 def centered_camera(cls, extent, size, **kw):

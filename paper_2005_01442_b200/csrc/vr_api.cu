@@ -134,6 +134,12 @@ void cell_counts(const vr_camera *c, int &cells_x, int &ncells, int &slots, long
 
 extern "C" {
 
+#ifdef VR_DEBUG_TIMES
+// development builds only: device buffer receiving per-warp timestamps
+static unsigned long long *g_debug_times = nullptr;
+void vr_debug_set_times(void *p) { g_debug_times = (unsigned long long *)p; }
+#endif
+
 const char *vr_last_error(void) { return g_err.c_str(); }
 int vr_abi_version(void) { return VR_ABI_VERSION; }
 
@@ -560,12 +566,21 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     a.work = (unsigned long long *)out->work;
     int nblocks = grid ? grid->nblocks : 1;
     if (a.blocks_hit) VR_CUDA(cudaMemsetAsync(a.blocks_hit, 0, nblocks, s));
-    Scratch lut_range(s);
+    Scratch lut_range(s), heavy(s);
     if (a.mode == VR_MODE_DVR && a.classify == VR_CLS_POST && vol->cells) {
-        VR_CUDA(lut_range.alloc(16));
+        // [lut first/last visible bin][ray queue head][heavy pushed][heavy claimed]
+        VR_CUDA(lut_range.alloc(32));
         VR_CUDA(vr::launch_lut_range(lut, prm->nlut, (int *)lut_range.p, s));
         a.lut_range = (const int *)lut_range.p;
         a.work_counter = (unsigned long long *)((char *)lut_range.p + 8);
+        a.heavy_count = a.work_counter + 1;
+        a.heavy_head = a.work_counter + 2;
+        const long long items = (long long)a.slots * vr::kTileW * vr::kTileH;
+        a.heavy_cap = items < (1LL << 20) ? items : (1LL << 20);
+        if (!getenv("VR_NO_HEAVY")) {
+            VR_CUDA(heavy.alloc((size_t)a.heavy_cap * vr::kHeavyRayBytes));
+            a.heavy = heavy.p;
+        }
         a.cells = vol->cells;
         a.ncx = vol->ncx;
         a.ncy = vol->ncy;
@@ -581,6 +596,9 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.vmax = grid->vmax;
         a.uni = vs.v.uni;
     }
+#ifdef VR_DEBUG_TIMES
+    a.debug_times = g_debug_times;
+#endif
     if (out->ev_start) VR_CUDA(cudaEventRecord((cudaEvent_t)out->ev_start, s));
     VR_CUDA(vr::launch_raycast(a, s));
     if (out->ev_stop) VR_CUDA(cudaEventRecord((cudaEvent_t)out->ev_stop, s));

@@ -670,11 +670,24 @@ struct PostRay {
     int bi, bj, bk;
     int stage;     // -1 none pending, 0 sample, 1..6 gradient taps
     int last_hit;
+    int work;      // steps spent on this ray by this lane
     long long out;  // output index of the pixel
+    long long item; // work item (pixel) the ray came from
     bool live;
 };
 
-constexpr int kPhaseACap = 8;  // cheap steps a lane may take per trip
+constexpr int kPhaseACap = 8;      // cheap steps a lane may take per trip
+constexpr int kDonateMinLeft = 64; // tail rays with at least this many samples left move to the heavy queue
+
+// A long ray handed from the per-lane kernel to the warp-cooperative one:
+// everything needed to continue it exactly where it stopped.
+struct HeavyRay {
+    long long item;
+    long long n;
+    double acc[4];
+    long long taken, skipped;
+};
+static_assert(sizeof(HeavyRay) == kHeavyRayBytes, "HeavyRay layout");
 
 // Work item -> pixel.  Items are numbered cell slot by cell slot, 128 per
 // slot, each 32-item group one 8x4 warp tile (the layout of raycast_kernel).
@@ -707,8 +720,35 @@ VR_D bool start_ray(const RenderArgs &a, long long item, PostRay &R) {
     R.taken = R.skipped = 0;
     R.stage = -1;
     R.last_hit = -1;
+    R.work = 0;
+    R.item = item;
     R.live = true;
     return true;
+}
+
+// Background composite, straight-alpha uint8 epilogue and per-pixel outputs
+// of a finished ray (_kernels.py:583-594, render.py:454-459).
+VR_D void finish_ray(const RenderArgs &a, long long p, double acc_r, double acc_g, double acc_b, double acc_a,
+                     long long taken, long long skipped) {
+    const double w = 1.0 - acc_a;
+    const double rr = acc_r + w * a.bg[0] * a.bg[3];
+    const double gg = acc_g + w * a.bg[1] * a.bg[3];
+    const double bb = acc_b + w * a.bg[2] * a.bg[3];
+    const double aa = acc_a + w * a.bg[3];
+    if (a.premult) reinterpret_cast<double4 *>(a.premult)[p] = make_double4(rr, gg, bb, aa);
+    if (a.pixels) {
+        double r0 = 0.0, g0 = 0.0, b0 = 0.0;
+        if (aa > 0.0) {
+            const double den = aa > 1e-12 ? aa : 1e-12;
+            r0 = rr / den;
+            g0 = gg / den;
+            b0 = bb / den;
+        }
+        reinterpret_cast<uchar4 *>(a.pixels)[p] = make_uchar4(to_u8(r0), to_u8(g0), to_u8(b0), to_u8(aa));
+    }
+    if (a.depth) a.depth[p] = __longlong_as_double(0x7ff8000000000000LL);
+    if (a.taken) a.taken[p] = taken;
+    if (a.skipped) a.skipped[p] = skipped;
 }
 
 template <bool CUBIC, bool LIGHT, bool SKIP>
@@ -724,6 +764,11 @@ __global__ void __launch_bounds__(kThreads) raycast_post_kernel(const __grid_con
     PostRay R;
     R.live = false;
     bool exhausted = false;
+#ifdef VR_DEBUG_TIMES
+    unsigned long long t_begin;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    unsigned long long n_rays = 0;
+#endif
     for (;;) {
         // ---- fetch rays for idle lanes (one atomic per warp)
         const bool want = !R.live && !exhausted;
@@ -742,7 +787,36 @@ __global__ void __launch_bounds__(kThreads) raycast_post_kernel(const __grid_con
             }
         }
         if (__all_sync(full, !R.live && exhausted)) break;
+        // the queue head is global: a warp whose lanes are all busy with long
+        // rays must still learn that the queue has drained
+        int head_done = 0;
+        if (lane == 0 && a.heavy)
+            head_done = *reinterpret_cast<volatile unsigned long long *>(a.work_counter) >= (unsigned long long)total;
+        const bool drained = __shfl_sync(full, head_done, 0) != 0 || __any_sync(full, exhausted);
         if (!R.live) continue;
+
+        // ---- once the ray queue has drained, hand long rays to the
+        // warp-cooperative kernel (at a clean point, nothing pending): the
+        // frame would otherwise end with a few warps finishing grazing rays
+        // of ~700 samples while every other SM idles
+        if (a.heavy && drained && R.work >= 0 && R.stage < 0 && R.N - R.n >= kDonateMinLeft) {
+            const unsigned long long slot = atomicAdd(a.heavy_count, 1ull);
+            if (slot < (unsigned long long)a.heavy_cap) {
+                HeavyRay h;
+                h.item = R.item;
+                h.n = R.n;
+                h.acc[0] = R.acc_r;
+                h.acc[1] = R.acc_g;
+                h.acc[2] = R.acc_b;
+                h.acc[3] = R.acc_a;
+                h.taken = R.taken;
+                h.skipped = R.skipped;
+                static_cast<HeavyRay *>(a.heavy)[slot] = h;
+                R.live = false;
+                continue;
+            }
+            R.work = INT_MIN;  // queue full: keep it here
+        }
 
         // ---- phase A: cheap steps until an interpolation is needed
         int steps = 0;
@@ -868,32 +942,217 @@ __global__ void __launch_bounds__(kThreads) raycast_post_kernel(const __grid_con
             }
         }
         if (R.stage < 0 && R.n >= R.N) finished = true;
+        R.work += steps + 1;
 
         // ---- finish: background, epilogue, per-pixel outputs
         if (finished) {
-            const double w = 1.0 - R.acc_a;
-            const double rr = R.acc_r + w * a.bg[0] * a.bg[3];
-            const double gg = R.acc_g + w * a.bg[1] * a.bg[3];
-            const double bb = R.acc_b + w * a.bg[2] * a.bg[3];
-            const double aa = R.acc_a + w * a.bg[3];
-            const long long p = R.out;
-            if (a.premult) reinterpret_cast<double4 *>(a.premult)[p] = make_double4(rr, gg, bb, aa);
-            if (a.pixels) {
-                double r0 = 0.0, g0 = 0.0, b0 = 0.0;
-                if (aa > 0.0) {
-                    const double den = aa > 1e-12 ? aa : 1e-12;
-                    r0 = rr / den;
-                    g0 = gg / den;
-                    b0 = bb / den;
-                }
-                reinterpret_cast<uchar4 *>(a.pixels)[p] = make_uchar4(to_u8(r0), to_u8(g0), to_u8(b0), to_u8(aa));
-            }
-            if (a.depth) a.depth[p] = __longlong_as_double(0x7ff8000000000000LL);
-            if (a.taken) a.taken[p] = R.taken;
-            if (a.skipped) a.skipped[p] = R.skipped;
+            finish_ray(a, R.out, R.acc_r, R.acc_g, R.acc_b, R.acc_a, R.taken, R.skipped);
             c_taken += (unsigned long long)R.taken;
             c_skip += (unsigned long long)R.skipped;
             R.live = false;
+        }
+    }
+#ifdef VR_DEBUG_TIMES
+    if (a.debug_times) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        const unsigned long long rays = warp_sum(c_iter ? 1ull : 0ull);
+        if (lane == 0) {
+            const long long w = (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            a.debug_times[4 * w] = t_begin;
+            a.debug_times[4 * w + 1] = t_end;
+            a.debug_times[4 * w + 2] = sm;
+            a.debug_times[4 * w + 3] = rays;
+        }
+    }
+#endif
+    c_taken = warp_sum(c_taken);
+    c_skip = warp_sum(c_skip);
+    if (lane == 0 && a.totals && (c_taken | c_skip)) {
+        atomicAdd(a.totals, c_taken);
+        atomicAdd(a.totals + 1, c_skip);
+    }
+    if (a.work) {
+        c_shaded = warp_sum(c_shaded);
+        c_eval = warp_sum(c_eval);
+        c_iter = warp_sum(c_iter);
+        if (lane == 0) {
+            if (c_shaded) atomicAdd(a.work, c_shaded);
+            if (c_eval) atomicAdd(a.work + 1, c_eval);
+            if (c_iter) atomicAdd(a.work + 2, c_iter);
+        }
+    }
+}
+
+// --------------------------------------------- warp-cooperative long rays
+// Continues the rays raycast_post_kernel handed over.  One warp owns one ray
+// and walks it 32 consecutive samples at a time, one per lane: each lane
+// evaluates its sample's exact skip predicate, transparency bound and, when
+// needed, interpolation, classification and gradient (in parallel); the
+// contributions are then composited strictly in sample order -- every lane
+// replays the same sequence of float64 updates from shuffled values -- and
+// stopped at the early-termination sample, so colour and counts are those of
+// the sequential march.  Chunks with nothing to evaluate extend by the same
+// provable leaps as the per-lane kernel, taken from the chunk's last sample.
+template <bool CUBIC, bool LIGHT, bool SKIP>
+__global__ void __launch_bounds__(kThreads) raycast_heavy_kernel(const __grid_constant__ RenderArgs a) {
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const int nbx = a.L.nb[0], nby = a.L.nb[1];
+    const bool cull = a.cull != 0;
+    const int first_vis = cull ? __ldg(a.lut_range) : 0;
+    const int last_vis = cull ? __ldg(a.lut_range + 1) : 0;
+    unsigned long long pushed = *a.heavy_count;
+    const long long count = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
+    unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(a.heavy_head, 1ull);
+        idx = __shfl_sync(full, idx, 0);
+        if ((long long)idx >= count) break;
+        const HeavyRay h = static_cast<const HeavyRay *>(a.heavy)[idx];
+        PostRay R;
+        start_ray(a, h.item, R);
+        long long n = h.n;
+        double acc_r = h.acc[0], acc_g = h.acc[1], acc_b = h.acc[2], acc_a = h.acc[3];
+        long long taken = h.taken, skipped = h.skipped;
+        while (n < R.N) {
+            ++c_iter;
+            const long long m = n + lane;
+            const bool valid = m < R.N;
+            bool skippable = false, cell_only = true, cand = false;
+            double x = 0.0, y = 0.0, z = 0.0, t = 0.0;
+            int bi = 0, bj = 0, bk = 0, b = 0;
+            if (valid) {
+                t = R.t0 + ((double)m + 0.5) * a.step;
+                x = divide(R.r.ox + t * R.r.dx, a.dsx);
+                y = divide(R.r.oy + t * R.r.dy, a.dsy);
+                z = divide(R.r.oz + t * R.r.dz, a.dsz);
+                bi = owner(a, 0, x);
+                bj = owner(a, 1, y);
+                bk = owner(a, 2, z);
+                b = (bk * nby + bj) * nbx + bi;
+                if (SKIP) {
+                    if (__ldg(a.empty + b) == 1) {
+                        skippable = true;
+                    } else {
+                        const double *bx = a.box + 6 * (long long)b;
+                        skippable = x < __ldg(bx) || x > __ldg(bx + 3) || y < __ldg(bx + 1) ||
+                                    y > __ldg(bx + 4) || z < __ldg(bx + 2) || z > __ldg(bx + 5);
+                        cell_only = false;
+                    }
+                }
+                cand = !skippable && !(cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis));
+            }
+            // evaluate this lane's sample
+            double sr = 0.0, sg = 0.0, sb = 0.0, ahat = 0.0;
+            bool contrib = false;
+            if (cand) {
+                ++c_eval;
+                const double v = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
+                const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
+                const double sa = __ldg(a.lut + 4 * sbin + 3);
+                if (sa > 0.0) {
+                    contrib = true;
+                    sr = __ldg(a.lut + 4 * sbin);
+                    sg = __ldg(a.lut + 4 * sbin + 1);
+                    sb = __ldg(a.lut + 4 * sbin + 2);
+                    ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
+                    if (LIGHT) {
+                        double gx = 0.0, gy = 0.0, gz = 0.0, plus = 0.0;
+#pragma unroll 1
+                        for (int q = 0; q < 6; ++q) {
+                            double px = x, py = y, pz = z;
+                            int qi = bi, qj = bj, qk = bk;
+                            const double hh = (q & 1) ? -0.5 : 0.5;
+                            if (q < 2) {
+                                px = x + hh;
+                                qi = owner(a, 0, px);
+                            } else if (q < 4) {
+                                py = y + hh;
+                                qj = owner(a, 1, py);
+                            } else {
+                                pz = z + hh;
+                                qk = owner(a, 2, pz);
+                            }
+                            const double s = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
+                            if (q & 1) {
+                                const double dg = plus - s;
+                                if (q == 1) gx = dg;
+                                else if (q == 3) gy = dg;
+                                else gz = dg;
+                            } else {
+                                plus = s;
+                            }
+                        }
+                        gx = divide(gx, a.dsx);
+                        gy = divide(gy, a.dsy);
+                        gz = divide(gz, a.dsz);
+                        ++c_shaded;
+                        const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                        if (norm > 1e-12)
+                            shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
+                    }
+                }
+            }
+            // composite in sample order, identically on every lane (_kernels.py:531-537)
+            unsigned cm = __ballot_sync(full, contrib);
+            int et_lane = 32;
+            while (cm) {
+                const int src = __ffs(cm) - 1;
+                cm &= cm - 1;
+                const double r_ = __shfl_sync(full, sr, src), g_ = __shfl_sync(full, sg, src);
+                const double b_ = __shfl_sync(full, sb, src), ah = __shfl_sync(full, ahat, src);
+                const double w = (1.0 - acc_a) * ah;
+                acc_r += w * r_;
+                acc_g += w * g_;
+                acc_b += w * b_;
+                acc_a += w;
+                if (acc_a >= a.term_alpha) {
+                    et_lane = src;
+                    break;
+                }
+            }
+            // counts up to and including the terminating sample
+            const unsigned upto = et_lane >= 31 ? full : ((2u << et_lane) - 1u);
+            const bool is_taken = valid && !skippable;
+            const unsigned tmask = __ballot_sync(full, is_taken) & upto;
+            const unsigned smask = __ballot_sync(full, valid && skippable) & upto;
+            taken += __popc(tmask);
+            skipped += __popc(smask);
+            if (is_taken && lane <= et_lane && a.blocks_hit) a.blocks_hit[b] = 1;
+            if (et_lane < 32) break;
+            // advance; a chunk with nothing to evaluate extends by a provable run
+            long long next = n + 32;
+            const bool any_cand = __ballot_sync(full, cand) != 0;
+            if (!any_cand && n + 31 < R.N) {
+                long long k = 1;
+                if (lane == 31) {
+                    const double p[3] = {x, y, z};
+                    const int bidx[3] = {bi, bj, bk};
+                    k = skippable ? leap_count<kPost>(a, R.r, R.inv, R.t0, m, t, p, bidx, b, cell_only)
+                                  : culled_run<SKIP>(a, R.r, R.inv, R.t0, m, t, p, bidx, b);
+                }
+                k = __shfl_sync(full, k, 31);
+                const bool last_skip = __shfl_sync(full, skippable, 31);
+                const long long last = n + 31;
+                if (k > R.N - last) k = R.N - last;
+                if (k > 1) {
+                    if (last_skip)
+                        skipped += k - 1;
+                    else
+                        taken += k - 1;
+                    next = last + k;
+                }
+            }
+            n = next;
+        }
+        if (lane == 0) {
+            finish_ray(a, R.out, acc_r, acc_g, acc_b, acc_a, taken, skipped);
+            c_taken += (unsigned long long)taken;
+            c_skip += (unsigned long long)skipped;
         }
     }
     c_taken = warp_sum(c_taken);
@@ -915,6 +1174,17 @@ __global__ void __launch_bounds__(kThreads) raycast_post_kernel(const __grid_con
 }
 
 using KernelFn = void (*)(RenderArgs);
+
+template <bool CUBIC, bool LIGHT>
+KernelFn pick_heavy(bool skip) {
+    return skip ? raycast_heavy_kernel<CUBIC, LIGHT, true> : raycast_heavy_kernel<CUBIC, LIGHT, false>;
+}
+
+KernelFn pick_cooperative(const RenderArgs &a) {
+    const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
+    if (c) return l ? pick_heavy<true, true>(s) : pick_heavy<true, false>(s);
+    return l ? pick_heavy<false, true>(s) : pick_heavy<false, false>(s);
+}
 
 template <bool CUBIC, bool LIGHT>
 KernelFn pick_post(bool skip) {
@@ -966,9 +1236,15 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
         long long ctas = (long long)sms * (per_sm > 0 ? per_sm : 1);
         if (ctas > a.slots) ctas = a.slots;
-        cudaError_t e = cudaMemsetAsync(a.work_counter, 0, sizeof(unsigned long long), stream);
+        cudaError_t e = cudaMemsetAsync(a.work_counter, 0, 3 * sizeof(unsigned long long), stream);
         if (e != cudaSuccess) return e;
         k<<<(unsigned)ctas, kThreads, 0, stream>>>(a);
+        if (a.heavy) {
+            KernelFn h = pick_cooperative(a);
+            int per_sm_h = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, h, kThreads, 0);
+            h<<<(unsigned)(sms * (per_sm_h > 0 ? per_sm_h : 1)), kThreads, 0, stream>>>(a);
+        }
         return cudaGetLastError();
     }
     pick(a)<<<a.slots, kThreads, 0, stream>>>(a);

@@ -51,6 +51,13 @@ struct RenderArgs {
     int cull;
 
     unsigned long long *work_counter;  // persistent kernel's ray queue head (zeroed per launch)
+    unsigned long long *debug_times;   // VR_DEBUG_TIMES builds: per warp (start, end, smid, lanes used)
+
+    // long rays handed over to the warp-cooperative kernel (HeavyRay records)
+    void *heavy;
+    unsigned long long *heavy_count;  // records pushed (zeroed per launch)
+    unsigned long long *heavy_head;   // records claimed by the cooperative kernel
+    long long heavy_cap;
 
     // outputs (all optional)
     uint8_t *pixels;
@@ -68,6 +75,7 @@ struct RenderArgs {
 constexpr int kTileW = 16;
 constexpr int kTileH = 8;
 constexpr int kThreads = 128;
+constexpr size_t kHeavyRayBytes = 64;  // sizeof(HeavyRay) in vr_raycast.cu
 
 cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream);
 

@@ -1,0 +1,53 @@
+"""Per-warp timeline of the persistent ray-cast kernel (needs a library built
+with -DVR_DEBUG_TIMES):
+
+    python paper_2005_01442_b200/_build.py build_variants/dbg.so VR_DEBUG_TIMES
+    VR_LIB=build_variants/dbg.so python tools/diag_warps.py c3
+"""
+
+import ctypes
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2005_01442_b200 as vr  # noqa: E402
+from paper_2005_01442_b200 import _lib  # noqa: E402
+
+
+def main(config="c3"):
+    cfg = bench.CONFIGS[config]
+    dvol = vr.device_phantom("torso", cfg["dims"])
+    nx, ny, nz = dvol.dims
+    cam = bench.make_camera(vr, cfg, (nx - 1.0, ny - 1.0, nz - 1.0))
+    r = vr.Renderer(dvol, cam, vr.get_preset(cfg["tf"]), vr.RenderSettings(**cfg["settings"]), time_kernel=True)
+    buf = torch.zeros(4 * 148 * 64, dtype=torch.int64, device="cuda")
+    L = _lib.load()
+    L.vr_debug_set_times.argtypes = [ctypes.c_void_p]
+    L.vr_debug_set_times(ctypes.c_void_p(buf.data_ptr()))
+    for _ in range(3):
+        r.render_async()
+    torch.cuda.synchronize()
+    print("kernel ms", r.kernel_ms())
+    t = buf.cpu().numpy().reshape(-1, 4)
+    t = t[t[:, 1] > 0]
+    t0 = t[:, 0].min()
+    start = (t[:, 0] - t0) / 1e3
+    end = (t[:, 1] - t0) / 1e3
+    print(f"warps {len(t)}  start max {start.max():.1f} us  end: min {end.min():.1f} "
+          f"p10 {np.percentile(end, 10):.1f} p50 {np.percentile(end, 50):.1f} p90 {np.percentile(end, 90):.1f} "
+          f"p99 {np.percentile(end, 99):.1f} max {end.max():.1f} us")
+    busy = np.zeros(400)
+    for e in end:
+        busy[: int(e / (end.max() / 400)) + 0] += 1
+    print("warps alive over time (10 buckets):", [int(busy[i * 40]) for i in range(10)])
+    order = np.argsort(-end)[:10]
+    print("latest warps (end us, sm):", [(round(end[i], 1), int(t[i, 2])) for i in order])
+
+
+if __name__ == "__main__":
+    main(*sys.argv[1:])
