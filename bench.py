@@ -53,6 +53,10 @@ CONFIGS = {
     "c4": dict(dims=(512, 512, 2048), size=2048, tf="bone", projection="pinhole",
                settings=dict(interpolation="tricubic", use_blocks=True),
                desc="512x512x2048 -> 2048^2, tricubic, bricks 64/3"),
+    "c5": dict(dims=(512, 512, 512), size=1024, tf="bone", projection="pinhole", views=36,
+               settings=dict(interpolation="tricubic", use_blocks=True),
+               measure=dict(threshold=550, balls=64, radius=16.0),
+               desc="turntable: 36 views/step (10 deg apart) of C3 + threshold count and 64 ball measures"),
 }
 
 L2_FLUSH_BYTES = 512 << 20
@@ -67,6 +71,7 @@ def parse():
     p.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
     p.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
                    help="override a RenderSettings field of the config (ablations)")
     args = p.parse_args()
@@ -172,7 +177,10 @@ def committed_traffic(config):
     return None
 
 
-def dist_setup(n):
+def dist_setup(n, backend):
+    """One process per GPU (torchrun env); NCCL over NVLink by default.  gloo
+    (CPU transport, several ranks may share one GPU) exists only to exercise
+    the multi-rank code path where fewer GPUs than ranks are available."""
     if n <= 1:
         return 0, 1, 0
     import torch
@@ -182,9 +190,28 @@ def dist_setup(n):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group("gloo")
     return rank, world, local
+
+
+def orbit_cameras(vr, extent, size, views):
+    """Turntable (C5): azimuth k*360/views degrees in the z = centre plane at
+    2.2x the largest extent (viewer orbit, frontend/src/camera.ts:35-44)."""
+    import math
+
+    cx, cy, cz = (0.5 * e for e in extent)
+    d = 2.2 * max(extent)
+    cams = []
+    for k in range(views):
+        ang = 2.0 * math.pi * k / views
+        cams.append(vr.Camera(position=(cx + d * math.cos(ang), cy + d * math.sin(ang), cz),
+                              look_at=(cx, cy, cz), width=size, height=size))
+    return cams
 
 
 def cpu_oracle_frame(values, spacing, camera, tf, settings, nthreads=0):
@@ -249,15 +276,27 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def launches_per_frame(settings):
+    """Kernels of ours in one frame (vr_render): TF visibility (3, block path),
+    LUT opacity range + per-lane ray caster + cooperative ray caster
+    (post-classified), or the one-thread-per-ray kernel, and the
+    blocks_visited count."""
+    post = settings.mode == "dvr" and settings.classification == "post"
+    n = 3 if settings.use_blocks else 0
+    n += 3 if post else 1
+    return n + 1
+
+
 def run_ours(args):
-    import numpy as np
+    import ctypes
+
     import torch
 
     import paper_2005_01442_b200 as vr
     from paper_2005_01442_b200 import _lib
-    from paper_2005_01442_b200.distributed import gather_frame
+    from paper_2005_01442_b200.distributed import gather_frame, render_sharded
 
-    rank, world, local = dist_setup(args.gpus)
+    rank, world, local = dist_setup(args.gpus, args.dist_backend)
     if world == 1:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -266,28 +305,52 @@ def run_ours(args):
     dvol = vr.device_phantom("torso", cfg["dims"], spacing, device=dev.index)
     nx, ny, nz = dvol.dims
     extent = ((nx - 1) * spacing[0], (ny - 1) * spacing[1], (nz - 1) * spacing[2])
-    camera = make_camera(vr, cfg, extent)
+    views = cfg.get("views", 1)
+    cameras = orbit_cameras(vr, extent, cfg["size"], views) if views > 1 else [make_camera(vr, cfg, extent)]
     tf = vr.get_preset(cfg["tf"])
     settings = vr.RenderSettings(**cfg["settings"])
-    rend = vr.Renderer(dvol, camera, tf, settings, device=dev.index,
+    rend = vr.Renderer(dvol, cameras[0], tf, settings, device=dev.index,
                        interleave=(world, rank) if world > 1 else None, time_kernel=True)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
-    W, H = camera.width, camera.height
+    W, H = cameras[0].width, cameras[0].height
+    measure = cfg.get("measure")
+    L = _lib.load()
+    if measure:
+        # K4 batched with the sweep: whole-volume threshold count + ball counts
+        import numpy as np
+
+        rng = np.random.default_rng(0)
+        centres = torch.from_numpy(rng.uniform(0.2, 0.8, size=(measure["balls"], 3)) * np.array(extent)).to(dev)
+        radii = torch.full((measure["balls"],), float(measure["radius"]), dtype=torch.float64, device=dev)
+        k4 = torch.zeros(1 + 4 * measure["balls"], dtype=torch.int64, device=dev)
 
     def frame():
-        rend.render_async(stream)
-        if world > 1:
-            gather_frame(rend.pixels.reshape(-1, 4), W, H)
+        for cam in cameras:
+            if views > 1:
+                rend.set_camera(cam)
+            rend.render_async(stream)
+            if world > 1:
+                packed = rend.pixels.reshape(-1, 4)
+                gather_frame(packed if args.dist_backend == "nccl" else packed.cpu(), W, H)
+        if measure:
+            k4[:1].zero_()
+            s = _lib.ptr_stream(stream)
+            _lib.check(L.vr_threshold_count(dvol.handle, int(measure["threshold"]), _lib.ptr(k4), s))
+            nb = measure["balls"]
+            _lib.check(L.vr_ball_counts(dvol.handle, int(measure["threshold"]), _lib.ptr(centres), _lib.ptr(radii),
+                                        nb, ctypes.c_void_p(k4.data_ptr() + 8),
+                                        ctypes.c_void_p(k4.data_ptr() + 8 + 8 * nb), s))
 
     for _ in range(max(args.warmup, 3)):
         frame()
     torch.cuda.synchronize()
-    st = rend.stats()
+    st = rend.stats()  # the last view of the sweep
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([st["samples_taken"], st["samples_skipped"], st["shaded"]], device=dev)
+        t = torch.tensor([st["samples_taken"], st["samples_skipped"], st["shaded"]], dtype=torch.int64)
+        t = t if args.dist_backend == "gloo" else t.to(dev)
         dist.all_reduce(t)
         st["samples_taken"], st["samples_skipped"], st["shaded"] = (int(x) for x in t.tolist())
         dist.barrier()
@@ -295,7 +358,7 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     step_ms, kern_ms = [], []
     torch.cuda.synchronize()
-    with ClockSampler(dev.index if world == 1 else local) as clocks:
+    with ClockSampler(dev.index) as clocks:
         for _ in range(args.steps):
             flush.fill_(1)  # evict the previous frame's working set from L2 (outside the timed pair)
             ev0.record(stream)
@@ -303,54 +366,72 @@ def run_ours(args):
             ev1.record(stream)
             ev1.synchronize()
             step_ms.append(ev0.elapsed_time(ev1))
-            kern_ms.append(rend.kernel_ms())
+            kern_ms.append(rend.kernel_ms())  # last view's ray-cast launches
         torch.cuda.synchronize()
     total_ms = sum(step_ms)
+    kern_total = sum(kern_ms)
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([total_ms, sum(kern_ms)], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms, kern_total], dtype=torch.float64)
+        t = t if args.dist_backend == "gloo" else t.to(dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, kern_total = t.tolist()
-    else:
-        kern_total = sum(kern_ms)
-    fps = args.steps / (total_ms / 1e3)
+    fps = args.steps * views / (total_ms / 1e3)
     taken, shaded = st["samples_taken"], st["shaded"]
     kern_s = kern_total / args.steps / 1e3
     cubic = settings.interpolation == "tricubic"
     b_sample = 128 if cubic else 16
     b_grad = 768 if cubic else 96
-    # rank-local bytes for the local kernel: per-rank share of the frame
+    # bytes the ray-cast launches of one rank process: its share of the frame
     algo_bytes = (taken * b_sample + shaded * b_grad + W * H * 4) / world
     achieved = algo_bytes / kern_s / 1e9
     peak, peak_kind = measured_peak()
-    launches_per_step = (5 if settings.use_blocks else 2)
 
     e2e = None
-    if not args.no_e2e and rank == 0 and world == 1:
+    if not args.no_e2e and views == 1:
         host_vol = vr.ScalarVolume(dvol.download(), spacing, dvol.value_range)
         host_vol._attach_device(dvol)
+        cam = cameras[0]
+        api = ("paper_2005_01442_b200.render(ScalarVolume, Camera, TF, RenderSettings) -> ImageRGBA "
+               "(C-ABI vr_render_to_host; volume cached on device)")
+        if world == 1:
+            def call():
+                return vr.render(host_vol, cam, tf, settings).pixels
+        else:
+            import torch.distributed as dist
+
+            api = ("paper_2005_01442_b200.distributed.render_sharded(volume, camera, TF, settings) -> "
+                   "host frame on rank 0 (sort-first cells, NCCL gather)")
+
+            def call():
+                return render_sharded(host_vol, cam, tf, settings)[0]
         for _ in range(3):
-            vr.render(host_vol, camera, tf, settings)
+            call()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            img = vr.render(host_vol, camera, tf, settings)
+            px = call()
+        torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64)
+            t = t if args.dist_backend == "gloo" else t.to(dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
         e2e = {"value": args.steps / e2e_s, "unit": "frames/s",
                "h2d_bytes_per_step": 4096 * 4 * 8,
-               "d2h_bytes_per_step": int(img.pixels.nbytes) + 5 * 8,
-               "api": "paper_2005_01442_b200.render(ScalarVolume, Camera, TF, RenderSettings) -> ImageRGBA "
-                      "(C-ABI vr_render_to_host; volume cached on device)"}
-    elif rank == 0 and world > 1:
-        e2e = None
+               "d2h_bytes_per_step": W * H * 4 + (5 * 8 if world == 1 else 0),
+               "api": api}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and views == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
 
         values = dvol.download()
-        t, r = cpu_oracle_frame(values, spacing, camera, tf, settings)
+        t, r = cpu_oracle_frame(values, spacing, cameras[0], tf, settings)
         cpu = {"value": 1.0 / t, "unit": "frames/s", "cores": O.num_threads(), "kind": "port",
                "sample": f"one full {args.config} frame via oracle.render (C restatement of "
                          "_kernels.march + block prep, OpenMP over pixels)",
@@ -370,15 +451,17 @@ def run_ours(args):
         "shaded_samples": shaded, "interpolated_samples": st.get("interpolated"),
         "march_iterations": st.get("march_iterations"),
         "config": {"workload": args.config, "desc": cfg["desc"], "volume": list(cfg["dims"]),
-                   "image": [W, H], "tf": cfg["tf"], "parallelism": f"sort-first x{world}",
+                   "image": [W, H], "views_per_step": views, "tf": cfg["tf"],
+                   "parallelism": f"sort-first x{world} ({args.dist_backend if world > 1 else 'single GPU'})",
                    "l2": "flushed between steps (512 MiB write)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,
-                     "traffic": committed_traffic(args.config), "kernel": "raycast_kernel",
+                     "traffic": committed_traffic(args.config),
+                     "kernel": "raycast_post_kernel + raycast_heavy_kernel (one vr_render launch pair)",
                      "kernel_ms": kern_s * 1e3,
                      "bytes_model": f"taken*{b_sample} + shaded*{b_grad} + W*H*4 per launch"},
         "clocks": clocks.summary(),
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": (launches_per_frame(settings) * views + (2 if measure else 0)) * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -577,7 +578,11 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.heavy_head = a.work_counter + 2;
         const long long items = (long long)a.slots * vr::kTileW * vr::kTileH;
         a.heavy_cap = items < (1LL << 20) ? items : (1LL << 20);
-        if (!getenv("VR_NO_HEAVY")) {
+        // development knob: VR_HEAVY_MIN_LEFT (default 64, the best of a
+        // 0..512 sweep at C2/C3; 0 disables the hand-off)
+        const char *hm = getenv("VR_HEAVY_MIN_LEFT");
+        a.heavy_min_left = hm ? atoll(hm) : 64;
+        if (a.heavy_min_left > 0) {
             VR_CUDA(heavy.alloc((size_t)a.heavy_cap * vr::kHeavyRayBytes));
             a.heavy = heavy.p;
         }

@@ -677,7 +677,6 @@ struct PostRay {
 };
 
 constexpr int kPhaseACap = 8;      // cheap steps a lane may take per trip
-constexpr int kDonateMinLeft = 64; // tail rays with at least this many samples left move to the heavy queue
 
 // A long ray handed from the per-lane kernel to the warp-cooperative one:
 // everything needed to continue it exactly where it stopped.
@@ -752,7 +751,10 @@ VR_D void finish_ray(const RenderArgs &a, long long p, double acc_r, double acc_
 }
 
 template <bool CUBIC, bool LIGHT, bool SKIP>
-__global__ void __launch_bounds__(kThreads) raycast_post_kernel(const __grid_constant__ RenderArgs a) {
+#ifndef VR_POST_MIN_BLOCKS
+#define VR_POST_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (latency-bound; swept 1..5)
+#endif
+__global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_kernel(const __grid_constant__ RenderArgs a) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const long long total = (long long)a.slots * (kTileW * kTileH);
@@ -799,7 +801,7 @@ __global__ void __launch_bounds__(kThreads) raycast_post_kernel(const __grid_con
         // warp-cooperative kernel (at a clean point, nothing pending): the
         // frame would otherwise end with a few warps finishing grazing rays
         // of ~700 samples while every other SM idles
-        if (a.heavy && drained && R.work >= 0 && R.stage < 0 && R.N - R.n >= kDonateMinLeft) {
+        if (a.heavy && drained && R.work >= 0 && R.stage < 0 && R.N - R.n >= a.heavy_min_left) {
             const unsigned long long slot = atomicAdd(a.heavy_count, 1ull);
             if (slot < (unsigned long long)a.heavy_cap) {
                 HeavyRay h;
@@ -997,7 +999,10 @@ __global__ void __launch_bounds__(kThreads) raycast_post_kernel(const __grid_con
 // the sequential march.  Chunks with nothing to evaluate extend by the same
 // provable leaps as the per-lane kernel, taken from the chunk's last sample.
 template <bool CUBIC, bool LIGHT, bool SKIP>
-__global__ void __launch_bounds__(kThreads) raycast_heavy_kernel(const __grid_constant__ RenderArgs a) {
+#ifndef VR_HEAVY_MIN_BLOCKS
+#define VR_HEAVY_MIN_BLOCKS 6  // <= 80 registers: 24 warps/SM (swept 1..8)
+#endif
+__global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_kernel(const __grid_constant__ RenderArgs a) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
@@ -1007,6 +1012,10 @@ __global__ void __launch_bounds__(kThreads) raycast_heavy_kernel(const __grid_co
     unsigned long long pushed = *a.heavy_count;
     const long long count = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
     unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
+#ifdef VR_DEBUG_TIMES
+    unsigned long long t_begin, n_rays = 0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+#endif
     for (;;) {
         unsigned long long idx = 0;
         if (lane == 0) idx = atomicAdd(a.heavy_head, 1ull);
@@ -1050,7 +1059,6 @@ __global__ void __launch_bounds__(kThreads) raycast_heavy_kernel(const __grid_co
             double sr = 0.0, sg = 0.0, sb = 0.0, ahat = 0.0;
             bool contrib = false;
             if (cand) {
-                ++c_eval;
                 const double v = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
                 const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
                 const double sa = __ldg(a.lut + 4 * sbin + 3);
@@ -1090,7 +1098,6 @@ __global__ void __launch_bounds__(kThreads) raycast_heavy_kernel(const __grid_co
                         gx = divide(gx, a.dsx);
                         gy = divide(gy, a.dsy);
                         gz = divide(gz, a.dsz);
-                        ++c_shaded;
                         const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
                         if (norm > 1e-12)
                             shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
@@ -1122,6 +1129,14 @@ __global__ void __launch_bounds__(kThreads) raycast_heavy_kernel(const __grid_co
             const unsigned smask = __ballot_sync(full, valid && skippable) & upto;
             taken += __popc(tmask);
             skipped += __popc(smask);
+            // work the sequential march would do (lanes past the terminating
+            // sample were evaluated speculatively and are not counted)
+            const unsigned emask = __ballot_sync(full, cand) & upto;
+            const unsigned cmask = __ballot_sync(full, contrib) & upto;
+            if (lane == 0) {
+                c_eval += __popc(emask);
+                if (LIGHT) c_shaded += __popc(cmask);
+            }
             if (is_taken && lane <= et_lane && a.blocks_hit) a.blocks_hit[b] = 1;
             if (et_lane < 32) break;
             // advance; a chunk with nothing to evaluate extends by a provable run
@@ -1154,7 +1169,21 @@ __global__ void __launch_bounds__(kThreads) raycast_heavy_kernel(const __grid_co
             c_taken += (unsigned long long)taken;
             c_skip += (unsigned long long)skipped;
         }
+#ifdef VR_DEBUG_TIMES
+        ++n_rays;
+#endif
     }
+#ifdef VR_DEBUG_TIMES
+    if (a.debug_times && lane == 0) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        const long long w = 148 * 32 + (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+        a.debug_times[4 * w] = t_begin;
+        a.debug_times[4 * w + 1] = t_end;
+        a.debug_times[4 * w + 2] = count;
+        a.debug_times[4 * w + 3] = n_rays;
+    }
+#endif
     c_taken = warp_sum(c_taken);
     c_skip = warp_sum(c_skip);
     if (lane == 0 && a.totals && (c_taken | c_skip)) {

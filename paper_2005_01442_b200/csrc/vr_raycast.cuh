@@ -58,6 +58,7 @@ struct RenderArgs {
     unsigned long long *heavy_count;  // records pushed (zeroed per launch)
     unsigned long long *heavy_head;   // records claimed by the cooperative kernel
     long long heavy_cap;
+    long long heavy_min_left;  // tail rays with at least this many samples left are handed over
 
     // outputs (all optional)
     uint8_t *pixels;

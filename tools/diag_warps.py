@@ -25,7 +25,7 @@ def main(config="c3"):
     nx, ny, nz = dvol.dims
     cam = bench.make_camera(vr, cfg, (nx - 1.0, ny - 1.0, nz - 1.0))
     r = vr.Renderer(dvol, cam, vr.get_preset(cfg["tf"]), vr.RenderSettings(**cfg["settings"]), time_kernel=True)
-    buf = torch.zeros(4 * 148 * 64, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(4 * 148 * 64, dtype=torch.int64, device="cuda")  # [0, 148*32) kernel 1 warps, rest kernel 2
     L = _lib.load()
     L.vr_debug_set_times.argtypes = [ctypes.c_void_p]
     L.vr_debug_set_times(ctypes.c_void_p(buf.data_ptr()))
@@ -33,9 +33,17 @@ def main(config="c3"):
         r.render_async()
     torch.cuda.synchronize()
     print("kernel ms", r.kernel_ms())
-    t = buf.cpu().numpy().reshape(-1, 4)
+    allt = buf.cpu().numpy().reshape(-1, 4)
+    t = allt[: 148 * 32]
     t = t[t[:, 1] > 0]
     t0 = t[:, 0].min()
+    h = allt[148 * 32:]
+    h = h[h[:, 1] > 0]
+    if len(h):
+        hs, he = (h[:, 0] - t0) / 1e3, (h[:, 1] - t0) / 1e3
+        print(f"cooperative kernel: {len(h)} warps, heavy rays {h[0, 2]}, rays/warp max {h[:, 3].max()} "
+              f"mean {h[:, 3].mean():.1f}; start {hs.min():.1f}..{hs.max():.1f} us, end p50 "
+              f"{np.percentile(he, 50):.1f} p90 {np.percentile(he, 90):.1f} max {he.max():.1f} us")
     start = (t[:, 0] - t0) / 1e3
     end = (t[:, 1] - t0) / 1e3
     print(f"warps {len(t)}  start max {start.max():.1f} us  end: min {end.min():.1f} "
