@@ -420,7 +420,7 @@ struct VisScratch {
         v.visbits = (unsigned int *)(base + off_bits);
         v.empty = (uint8_t *)(base + off_empty);
         v.aabb = (int *)(base + off_aabb);
-        v.box = (double *)(base + off_box);
+        v.box = (float *)(base + off_box);  // 32 B per block (sized 48 B above)
         v.aabb_global = want_global ? (long long *)(base + off_glob) : nullptr;
         v.counters = (unsigned long long *)(base + off_cnt);
         v.uni = (int *)(base + off_uni);

@@ -290,6 +290,8 @@ __global__ void box_kernel(const Layout L, const VisArgs v) {
     const int ext[3] = {block_extent(L, 0, bi), block_extent(L, 1, bj), block_extent(L, 2, bk)};
     const int *ab = v.aabb + 6 * b;
     bool fitted = !v.empty[b] && ab[3] >= 0;
+    v.box[8 * b + 3] = v.empty[b] ? 1.0f : 0.0f;
+    v.box[8 * b + 7] = 0.0f;
     if (!v.empty[b] && !fitted) atomicAdd(v.counters + 1, 1ull);  // reference raises EmptyBlock
     for (int k = 0; k < 3; ++k) {
         long long lo, hi;
@@ -300,8 +302,9 @@ __global__ void box_kernel(const Layout L, const VisArgs v) {
             lo = LLONG_MAX / 2;
             hi = -1;
         }
-        v.box[6 * b + k] = (double)lo - v.margin;
-        v.box[6 * b + 3 + k] = (double)hi + v.margin;
+        // integers +- margin (2 or 3): exact in float32 for |value| < 2^24
+        v.box[8 * b + k] = (float)((double)lo - v.margin);
+        v.box[8 * b + 4 + k] = (float)((double)hi + v.margin);
         if (v.aabb_global) {
             v.aabb_global[6 * b + k] = lo;
             v.aabb_global[6 * b + 3 + k] = hi;

@@ -28,7 +28,7 @@ struct VisArgs {
     unsigned int *visbits;   // 65536 bits: int16 value v visible <=> bit (v + 32768)
     uint8_t *empty;          // nblocks
     int *aabb;               // nblocks x 6 local min/max (x,y,z) of visible voxels
-    double *box;             // nblocks x 6 render box (global, +- margin)
+    float *box;              // nblocks x 8: box lo xyz - margin, empty flag, hi xyz + margin, 0 (BlockRec)
     long long *aabb_global;  // optional nblocks x 6 int64 inclusive global aabb (lo xyz, hi xyz)
     unsigned long long *counters;  // [0] empty blocks, [1] non-empty blocks without a visible voxel
     int *uni;                // 6: union of the fitted global AABBs (lo xyz, hi xyz)

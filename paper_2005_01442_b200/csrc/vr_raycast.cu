@@ -176,6 +176,28 @@ VR_D void shade(const RenderArgs &a, double &r, double &g, double &b, double nx,
 VR_D double dmin(double a, double b) { return a < b ? a : b; }
 VR_D double dmax(double a, double b) { return a > b ? a : b; }
 
+// Per-frame skip state of one block, 32 bytes (box_kernel, vr_prep.cu): the
+// visibility box +- margin (integers +- 2 or 3, exact in float32) and the
+// empty flag, fetched with two 16-byte loads.
+struct BlockRec {
+    float4 lo;  // x, y, z, empty (1.0f / 0.0f)
+    float4 hi;  // x, y, z, unused
+};
+
+VR_D BlockRec block_rec(const RenderArgs &a, int b) {
+    const float4 *p = reinterpret_cast<const float4 *>(a.box) + 2 * (long long)b;
+    BlockRec r;
+    r.lo = __ldg(p);
+    r.hi = __ldg(p + 1);
+    return r;
+}
+
+// The reference's DVR skip predicate (_kernels.py:381-391) for block b.
+VR_D bool dvr_skippable(const BlockRec &r, double x, double y, double z) {
+    return r.lo.w != 0.0f || x < (double)r.lo.x || x > (double)r.hi.x || y < (double)r.lo.y ||
+           y > (double)r.hi.y || z < (double)r.lo.z || z > (double)r.hi.z;
+}
+
 // True when the interpolated value at (x, y, z) provably classifies to a
 // zero-opacity LUT bin, so the reference's sample would contribute nothing
 // (_kernels.py:513-515: alpha == 0 -> no compositing).  Every tap of the
@@ -230,7 +252,7 @@ VR_D bool slab(const double o[3], const double d[3], const double inv[3], const 
 // reciprocal multiplies stand in for divisions for the same reason.
 template <int KIND>
 VR_D long long leap_count(const RenderArgs &a, const Ray &r, const double inv[3], double t0, long long n,
-                          double t, const double p[3], const int bidx[3], int b, bool cell_only) {
+                          double t, const double p[3], const int bidx[3], const BlockRec &rec, bool cell_only) {
     const double delta = 1e-6;
     const double d[3] = {r.dx, r.dy, r.dz};
     const double o[3] = {r.ox, r.oy, r.oz};
@@ -248,9 +270,8 @@ VR_D long long leap_count(const RenderArgs &a, const Ray &r, const double inv[3]
     }
     if (KIND != kIso) {
         if (!cell_only) {
-            const double *bx = a.box + 6 * (long long)b;
-            const double lo[3] = {__ldg(bx), __ldg(bx + 1), __ldg(bx + 2)};
-            const double hi[3] = {__ldg(bx + 3), __ldg(bx + 4), __ldg(bx + 5)};
+            const double lo[3] = {(double)rec.lo.x, (double)rec.lo.y, (double)rec.lo.z};
+            const double hi[3] = {(double)rec.hi.x, (double)rec.hi.y, (double)rec.hi.z};
             double tin, tout;
             if (slab(o, d, inv, s, p, lo, hi, delta, tin, tout) && tout >= t)
                 t_safe = (tin > t) ? dmin(t_safe, tin) : t;
@@ -289,7 +310,7 @@ VR_D long long leap_count(const RenderArgs &a, const Ray &r, const double inv[3]
 // slack absorbs the rounding of t.
 template <bool SKIP>
 VR_D long long culled_run(const RenderArgs &a, const Ray &r, const double inv[3], double t0, long long n, double t,
-                          const double p[3], const int bidx[3], int b) {
+                          const double p[3], const int bidx[3], const BlockRec &rec) {
     const double delta = 1e-6;
     const double d[3] = {r.dx, r.dy, r.dz};
     const double o[3] = {r.ox, r.oy, r.oz};
@@ -310,8 +331,9 @@ VR_D long long culled_run(const RenderArgs &a, const Ray &r, const double inv[3]
                 double X = (1.0 + (double)(bidx[k] * a.L.stride)) + delta;
                 t_safe = dmin(t_safe, (X * s[k] - o[k]) * inv[k]);
             }
-            const double *bx = a.box + 6 * (long long)b;
-            const double edge = d[k] > 0.0 ? __ldg(bx + 3 + k) - delta : __ldg(bx + k) + delta;
+            const float lo_k = k == 0 ? rec.lo.x : (k == 1 ? rec.lo.y : rec.lo.z);
+            const float hi_k = k == 0 ? rec.hi.x : (k == 1 ? rec.hi.y : rec.hi.z);
+            const double edge = d[k] > 0.0 ? (double)hi_k - delta : (double)lo_k + delta;
             t_safe = dmin(t_safe, (edge * s[k] - o[k]) * inv[k]);
         }
     }
@@ -371,22 +393,20 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
             const int bi = owner(a, 0, x), bj = owner(a, 1, y), bk = owner(a, 2, z);
             const int b = (bk * nby + bj) * nbx + bi;
 
+            BlockRec rec = {};
             if (SKIP) {
                 bool skippable, cell_only = true;
                 if (KIND == kIso) {
                     skippable = (double)__ldg(a.vmax + b) < a.isovalue || (double)__ldg(a.vmin + b) > a.isovalue;
-                } else if (__ldg(a.empty + b) == 1) {
-                    skippable = true;
                 } else {
-                    const double *bx = a.box + 6 * (long long)b;
-                    skippable = x < __ldg(bx) || x > __ldg(bx + 3) || y < __ldg(bx + 1) ||
-                                y > __ldg(bx + 4) || z < __ldg(bx + 2) || z > __ldg(bx + 5);
-                    cell_only = false;
+                    rec = block_rec(a, b);
+                    skippable = dvr_skippable(rec, x, y, z);
+                    cell_only = rec.lo.w != 0.0f;
                 }
                 if (skippable && (prev_skippable || !chained)) {
                     const double p[3] = {x, y, z};
                     const int bidx[3] = {bi, bj, bk};
-                    long long k = leap_count<KIND>(a, r, inv, t0, n, t, p, bidx, b, cell_only);
+                    long long k = leap_count<KIND>(a, r, inv, t0, n, t, p, bidx, rec, cell_only);
                     long long m = (N - n < k) ? N : n + k;
                     n_skip += m - n;
                     n = m;
@@ -482,7 +502,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 if (cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis)) {
                     const double p[3] = {x, y, z};
                     const int bidx[3] = {bi, bj, bk};
-                    long long k = culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, b);
+                    long long k = culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, rec);
                     if (k > N - n) k = N - n;
                     n_taken += k - 1;
                     n += k;
@@ -834,18 +854,13 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
             const int b = (bk * nby + bj) * nbx + bi;
             const double p[3] = {x, y, z};
             const int bidx[3] = {bi, bj, bk};
+            BlockRec rec = {};
             if (SKIP) {
-                bool skippable, cell_only = true;
-                if (__ldg(a.empty + b) == 1) {
-                    skippable = true;
-                } else {
-                    const double *bx = a.box + 6 * (long long)b;
-                    skippable = x < __ldg(bx) || x > __ldg(bx + 3) || y < __ldg(bx + 1) ||
-                                y > __ldg(bx + 4) || z < __ldg(bx + 2) || z > __ldg(bx + 5);
-                    cell_only = false;
-                }
+                rec = block_rec(a, b);
+                const bool skippable = dvr_skippable(rec, x, y, z);
+                const bool cell_only = rec.lo.w != 0.0f;
                 if (skippable) {
-                    long long k = leap_count<kPost>(a, R.r, R.inv, R.t0, n, t, p, bidx, b, cell_only);
+                    long long k = leap_count<kPost>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec, cell_only);
                     if (k > R.N - n) k = R.N - n;
                     R.skipped += k;
                     R.n = n + k;
@@ -857,7 +872,7 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
                 R.last_hit = b;
             }
             if (cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis)) {
-                long long k = culled_run<SKIP>(a, R.r, R.inv, R.t0, n, t, p, bidx, b);
+                long long k = culled_run<SKIP>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec);
                 if (k > R.N - n) k = R.N - n;
                 R.taken += k;
                 R.n = n + k;
@@ -1034,6 +1049,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
             bool skippable = false, cell_only = true, cand = false;
             double x = 0.0, y = 0.0, z = 0.0, t = 0.0;
             int bi = 0, bj = 0, bk = 0, b = 0;
+            BlockRec rec = {};
             if (valid) {
                 t = R.t0 + ((double)m + 0.5) * a.step;
                 x = divide(R.r.ox + t * R.r.dx, a.dsx);
@@ -1044,14 +1060,9 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 bk = owner(a, 2, z);
                 b = (bk * nby + bj) * nbx + bi;
                 if (SKIP) {
-                    if (__ldg(a.empty + b) == 1) {
-                        skippable = true;
-                    } else {
-                        const double *bx = a.box + 6 * (long long)b;
-                        skippable = x < __ldg(bx) || x > __ldg(bx + 3) || y < __ldg(bx + 1) ||
-                                    y > __ldg(bx + 4) || z < __ldg(bx + 2) || z > __ldg(bx + 5);
-                        cell_only = false;
-                    }
+                    rec = block_rec(a, b);
+                    skippable = dvr_skippable(rec, x, y, z);
+                    cell_only = rec.lo.w != 0.0f;
                 }
                 cand = !skippable && !(cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis));
             }
@@ -1147,8 +1158,8 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 if (lane == 31) {
                     const double p[3] = {x, y, z};
                     const int bidx[3] = {bi, bj, bk};
-                    k = skippable ? leap_count<kPost>(a, R.r, R.inv, R.t0, m, t, p, bidx, b, cell_only)
-                                  : culled_run<SKIP>(a, R.r, R.inv, R.t0, m, t, p, bidx, b);
+                    k = skippable ? leap_count<kPost>(a, R.r, R.inv, R.t0, m, t, p, bidx, rec, cell_only)
+                                  : culled_run<SKIP>(a, R.r, R.inv, R.t0, m, t, p, bidx, rec);
                 }
                 k = __shfl_sync(full, k, 31);
                 const bool last_skip = __shfl_sync(full, skippable, 31);

@@ -37,7 +37,7 @@ struct RenderArgs {
 
     // block classification (K2 outputs; unused when skip_empty == 0)
     const uint8_t *empty;    // nblocks
-    const double *box;       // nblocks x 6: lo xyz (aabb_lo - margin), hi xyz (aabb_hi + margin)
+    const float *box;        // nblocks x 8 (BlockRec): lo xyz - margin, empty, hi xyz + margin, 0
     const int *vmin, *vmax;  // nblocks (iso skip predicate)
     const int *uni;          // 6: union of the fitted global AABBs (lo xyz, hi xyz); lo > hi = none
     double margin;           // SKIP_MARGIN applied to every box
