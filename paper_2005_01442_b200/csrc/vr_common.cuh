@@ -55,7 +55,14 @@ inline Divisor make_divisor(double s) {
     return d;
 }
 
-VR_D double divide(double x, const Divisor &d) { return d.pow2 ? x * d.inv : x / d.s; }
+// Rare paths live out of line so the hot loops stay within the instruction
+// cache (an inlined IEEE double division is ~20 instructions plus a slow
+// path, and the kernels call these from many sites).
+static __device__ __noinline__ double div_rn(double x, double s) { return x / s; }
+static __device__ __noinline__ double floor_div(double a, double s) { return floor(a / s); }
+static __device__ __noinline__ double pow_general(double x, double y) { return pow(x, y); }
+
+VR_D double divide(double x, const Divisor &d) { return d.pow2 ? x * d.inv : div_rn(x, d.s); }
 
 // floor((x - 1) / stride) clamped to [0, nb-1], as the reference's block
 // attribution does (_kernels.py:226-228, 372-374).  The quotient is first
@@ -68,7 +75,7 @@ VR_D int owner_block(double x, double stride, double inv_stride, int nb) {
     double q = a * inv_stride;
     double f = floor(q);
     double fr = q - f;
-    if (fr < 1e-9 || fr > 1.0 - 1e-9) f = floor(a / stride);
+    if (fr < 1e-9 || fr > 1.0 - 1e-9) f = floor_div(a, stride);
     // clamp in the float domain first so huge values cannot overflow the int
     if (f < 0.0) return 0;
     if (f > (double)(nb - 1)) return nb - 1;
@@ -448,7 +455,7 @@ VR_D double vr_pow(double x, const PowSpec &p) {
         case 0: return x;
         case 1: return (x == 0.0 && p.n == 0) ? 1.0 : pow_int_dd(x, p.n);
         case 2: return sqrt(x);
-        default: return pow(x, p.y);
+        default: return pow_general(x, p.y);
     }
 }
 

@@ -596,10 +596,11 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
 // rint(clip(.,0,1) * 255) with round-half-even.
 VR_D unsigned char to_u8(double v) { return (unsigned char)rint(clampf(v, 0.0, 1.0) * 255.0); }
 
+// Sum over the (converged) warp with one REDUX; a lane's per-launch counts
+// stay far below 2^32 (a lane handles at most a few hundred rays of at most a
+// few thousand samples), the 64-bit totals accumulate in global atomics.
 VR_D unsigned long long warp_sum(unsigned long long v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-    return v;
+    return (unsigned long long)__reduce_add_sync(0xffffffffu, (unsigned)v);
 }
 
 template <int KIND, bool CUBIC, bool LIGHT, bool SKIP>
@@ -1067,53 +1068,57 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 cand = !skippable && !(cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis));
             }
             // evaluate this lane's sample
+            // (one loop body for the sample and its six gradient taps keeps a
+            // single copy of the interpolant in the kernel: q = 0 the sample,
+            // q = 1..6 the taps +x,-x,+y,-y,+z,-z)
             double sr = 0.0, sg = 0.0, sb = 0.0, ahat = 0.0;
+            double gx = 0.0, gy = 0.0, gz = 0.0, plus = 0.0;
             bool contrib = false;
-            if (cand) {
-                const double v = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
-                const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
-                const double sa = __ldg(a.lut + 4 * sbin + 3);
-                if (sa > 0.0) {
+            const int nq = cand ? (LIGHT ? 7 : 1) : 0;
+#pragma unroll 1
+            for (int q = 0; q < nq; ++q) {
+                double px = x, py = y, pz = z;
+                int qi = bi, qj = bj, qk = bk;
+                if (q > 0) {
+                    const int g = q - 1;
+                    const double hh = (g & 1) ? -0.5 : 0.5;
+                    if (g < 2) {
+                        px = x + hh;
+                        qi = owner(a, 0, px);
+                    } else if (g < 4) {
+                        py = y + hh;
+                        qj = owner(a, 1, py);
+                    } else {
+                        pz = z + hh;
+                        qk = owner(a, 2, pz);
+                    }
+                }
+                const double v = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
+                if (q == 0) {
+                    const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
+                    const double sa = __ldg(a.lut + 4 * sbin + 3);
+                    if (!(sa > 0.0)) break;  // transparent: nothing to composite
                     contrib = true;
                     sr = __ldg(a.lut + 4 * sbin);
                     sg = __ldg(a.lut + 4 * sbin + 1);
                     sb = __ldg(a.lut + 4 * sbin + 2);
                     ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
-                    if (LIGHT) {
-                        double gx = 0.0, gy = 0.0, gz = 0.0, plus = 0.0;
-#pragma unroll 1
-                        for (int q = 0; q < 6; ++q) {
-                            double px = x, py = y, pz = z;
-                            int qi = bi, qj = bj, qk = bk;
-                            const double hh = (q & 1) ? -0.5 : 0.5;
-                            if (q < 2) {
-                                px = x + hh;
-                                qi = owner(a, 0, px);
-                            } else if (q < 4) {
-                                py = y + hh;
-                                qj = owner(a, 1, py);
-                            } else {
-                                pz = z + hh;
-                                qk = owner(a, 2, pz);
-                            }
-                            const double s = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
-                            if (q & 1) {
-                                const double dg = plus - s;
-                                if (q == 1) gx = dg;
-                                else if (q == 3) gy = dg;
-                                else gz = dg;
-                            } else {
-                                plus = s;
-                            }
-                        }
-                        gx = divide(gx, a.dsx);
-                        gy = divide(gy, a.dsy);
-                        gz = divide(gz, a.dsz);
-                        const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
-                        if (norm > 1e-12)
-                            shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
-                    }
+                } else if (q & 1) {
+                    plus = v;
+                } else {
+                    const double dg = plus - v;
+                    if (q == 2) gx = dg;
+                    else if (q == 4) gy = dg;
+                    else gz = dg;
                 }
+            }
+            if (LIGHT && contrib) {
+                gx = divide(gx, a.dsx);
+                gy = divide(gy, a.dsy);
+                gz = divide(gz, a.dsz);
+                const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                if (norm > 1e-12)
+                    shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
             }
             // composite in sample order, identically on every lane (_kernels.py:531-537)
             unsigned cm = __ballot_sync(full, contrib);
