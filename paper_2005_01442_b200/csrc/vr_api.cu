@@ -582,6 +582,8 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         // 0..512 sweep at C2/C3; 0 disables the hand-off)
         const char *hm = getenv("VR_HEAVY_MIN_LEFT");
         a.heavy_min_left = hm ? atoll(hm) : 64;
+        const char *ha = getenv("VR_HEAVY_AFTER");
+        a.heavy_after = ha ? atoi(ha) : 1 << 30;
         if (a.heavy_min_left > 0) {
             VR_CUDA(heavy.alloc((size_t)a.heavy_cap * vr::kHeavyRayBytes));
             a.heavy = heavy.p;

@@ -262,6 +262,8 @@ VR_D double cub_sample(const Block<V> &b, double x, double y, double z) {
 // of one per row -- and each tap is a shift of the window.
 VR_D double window_tap(unsigned long long lo, unsigned long long hi, unsigned s) {
     const unsigned long long w = s < 64 ? (lo >> s) : (hi >> (s - 64));
+    // (an exact magic-number conversion on the FP64 pipe measured slower
+    // than I2F: the sampler is latency-bound, not XU-bound)
     return (double)(short)(w & 0xffffull);
 }
 

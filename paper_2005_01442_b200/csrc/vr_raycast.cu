@@ -822,7 +822,8 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
         // warp-cooperative kernel (at a clean point, nothing pending): the
         // frame would otherwise end with a few warps finishing grazing rays
         // of ~700 samples while every other SM idles
-        if (a.heavy && drained && R.work >= 0 && R.stage < 0 && R.N - R.n >= a.heavy_min_left) {
+        if (a.heavy && (drained || R.work > a.heavy_after) && R.work >= 0 && R.stage < 0 &&
+            R.N - R.n >= a.heavy_min_left) {
             const unsigned long long slot = atomicAdd(a.heavy_count, 1ull);
             if (slot < (unsigned long long)a.heavy_cap) {
                 HeavyRay h;

@@ -59,6 +59,7 @@ struct RenderArgs {
     unsigned long long *heavy_head;   // records claimed by the cooperative kernel
     long long heavy_cap;
     long long heavy_min_left;  // tail rays with at least this many samples left are handed over
+    int heavy_after;           // ... and, before the queue drains, rays that took more steps than this
 
     // outputs (all optional)
     uint8_t *pixels;
