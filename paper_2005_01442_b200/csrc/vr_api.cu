@@ -183,6 +183,11 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     v->bnx = (int)((v->nx + 3) / 4);
     v->bny = (int)((v->ny + 3) / 4);
     v->bnz = (int)((v->nz + 3) / 4);
+    if ((long long)v->bnx * v->bny * 64 >= (1ll << 31)) {  // 32-bit row offsets inside a sample (vr_common.cuh)
+        cudaFree(v->data);
+        delete v;
+        return fail(VR_EINVALID, "volume slice too large (nx * ny must be < 2^31 / 4)");
+    }
     cudaError_t e = cudaMalloc((void **)&v->cells, sizeof(short2) * (size_t)v->ncx * v->ncy * v->ncz);
     if (e == cudaSuccess) e = cudaMalloc((void **)&v->bricks, sizeof(int16_t) * 64 * (size_t)v->bnx * v->bny * v->bnz);
     if (e == cudaSuccess) e = vr::launch_brick_volume(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bricks, s);

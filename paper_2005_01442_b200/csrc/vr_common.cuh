@@ -267,8 +267,18 @@ VR_D double window_tap(unsigned long long lo, unsigned long long hi, unsigned s)
     return (double)(short)(w & 0xffffull);
 }
 
-VR_D long long brick_row_y(const BrickVol &v, int gy) { return (long long)(gy >> 2) * v.bpy + ((gy & 3) << 2); }
-VR_D long long brick_row_z(const BrickVol &v, int gz) { return (long long)(gz >> 2) * v.bpz + ((gz & 3) << 4); }
+// Row offsets relative to the brick row/plane of the first tap g0 (taps span
+// at most two bricks per axis), in 32-bit arithmetic: the sample's base
+// pointer carries the 64-bit part once.
+VR_D unsigned brick_dy(const BrickVol &v, int gy, int gy0) {
+    return ((gy >> 2) != (gy0 >> 2) ? (unsigned)v.bpy : 0u) + ((unsigned)(gy & 3) << 2);
+}
+VR_D unsigned brick_dz(const BrickVol &v, int gz, int gz0) {
+    return ((gz >> 2) != (gz0 >> 2) ? (unsigned)v.bpz : 0u) + ((unsigned)(gz & 3) << 4);
+}
+VR_D const int16_t *brick_base(const BrickVol &v, int base, int gy0, int gz0) {
+    return v.p + (long long)(gz0 >> 2) * v.bpz + (long long)(gy0 >> 2) * v.bpy + ((long long)(base >> 2) << 6);
+}
 
 // _kernels.py:52-80 on the brick layout
 VR_D double tri_sample(const Block<BrickVol> &b, double x, double y, double z) {
@@ -284,13 +294,14 @@ VR_D double tri_sample(const Block<BrickVol> &b, double x, double y, double z) {
     const int gx = b.ox + i0, base = gx & ~3;
     const unsigned s0 = 16u * (unsigned)(gx - base), s1 = s0 + 16u;
     const bool need_hi = (gx - base) == 3;
-    const int16_t *px = b.vol.p + ((long long)(base >> 2) << 6);
-    const long long y0 = brick_row_y(b.vol, b.oy + j0), y1 = brick_row_y(b.vol, b.oy + j0 + 1);
-    const long long z0 = brick_row_z(b.vol, b.oz + k0), z1 = brick_row_z(b.vol, b.oz + k0 + 1);
-    const unsigned long long *q00 = reinterpret_cast<const unsigned long long *>(px + y0 + z0);
-    const unsigned long long *q10 = reinterpret_cast<const unsigned long long *>(px + y1 + z0);
-    const unsigned long long *q01 = reinterpret_cast<const unsigned long long *>(px + y0 + z1);
-    const unsigned long long *q11 = reinterpret_cast<const unsigned long long *>(px + y1 + z1);
+    const int gy = b.oy + j0, gz = b.oz + k0;
+    const int16_t *px = brick_base(b.vol, base, gy, gz);
+    const unsigned y0 = brick_dy(b.vol, gy, gy), y1 = brick_dy(b.vol, gy + 1, gy);
+    const unsigned z0 = brick_dz(b.vol, gz, gz), z1 = brick_dz(b.vol, gz + 1, gz);
+    const unsigned long long *q00 = reinterpret_cast<const unsigned long long *>(px + (y0 + z0));
+    const unsigned long long *q10 = reinterpret_cast<const unsigned long long *>(px + (y1 + z0));
+    const unsigned long long *q01 = reinterpret_cast<const unsigned long long *>(px + (y0 + z1));
+    const unsigned long long *q11 = reinterpret_cast<const unsigned long long *>(px + (y1 + z1));
     const unsigned long long l00 = __ldg(q00), l10 = __ldg(q10), l01 = __ldg(q01), l11 = __ldg(q11);
     unsigned long long h00 = 0, h10 = 0, h01 = 0, h11 = 0;
     if (need_hi) {
@@ -331,19 +342,20 @@ VR_D double cub_sample(const Block<BrickVol> &b, double x, double y, double z) {
     const unsigned s2 = 16u * (unsigned)(b.ox + min(i0 + 1, b.ex - 1) - base);
     const unsigned s3 = 16u * (unsigned)(gx3 - base);
     const bool need_hi = (gx3 - base) >= 4;
-    const int16_t *px = b.vol.p + ((long long)(base >> 2) << 6);
-    const long long yo[4] = {brick_row_y(b.vol, b.oy + max(j0 - 1, 0)), brick_row_y(b.vol, b.oy + j0),
-                             brick_row_y(b.vol, b.oy + min(j0 + 1, b.ey - 1)),
-                             brick_row_y(b.vol, b.oy + min(j0 + 2, b.ey - 1))};
-    const long long zo[4] = {brick_row_z(b.vol, b.oz + max(k0 - 1, 0)), brick_row_z(b.vol, b.oz + k0),
-                             brick_row_z(b.vol, b.oz + min(k0 + 1, b.ez - 1)),
-                             brick_row_z(b.vol, b.oz + min(k0 + 2, b.ez - 1))};
+    const int gy0 = b.oy + max(j0 - 1, 0), gz0 = b.oz + max(k0 - 1, 0);
+    const int16_t *px = brick_base(b.vol, base, gy0, gz0);
+    const unsigned yo[4] = {brick_dy(b.vol, gy0, gy0), brick_dy(b.vol, b.oy + j0, gy0),
+                            brick_dy(b.vol, b.oy + min(j0 + 1, b.ey - 1), gy0),
+                            brick_dy(b.vol, b.oy + min(j0 + 2, b.ey - 1), gy0)};
+    const unsigned zo[4] = {brick_dz(b.vol, gz0, gz0), brick_dz(b.vol, b.oz + k0, gz0),
+                            brick_dz(b.vol, b.oz + min(k0 + 1, b.ez - 1), gz0),
+                            brick_dz(b.vol, b.oz + min(k0 + 2, b.ez - 1), gz0)};
     unsigned long long lo[16], hi[16];
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-            const unsigned long long *q = reinterpret_cast<const unsigned long long *>(px + zo[c] + yo[r]);
+            const unsigned long long *q = reinterpret_cast<const unsigned long long *>(px + (zo[c] + yo[r]));
             lo[4 * c + r] = __ldg(q);
             hi[4 * c + r] = need_hi ? __ldg(q + 16) : 0ull;
         }

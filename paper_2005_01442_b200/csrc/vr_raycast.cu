@@ -1032,6 +1032,10 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
 #ifdef VR_DEBUG_TIMES
     unsigned long long t_begin, n_rays = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+    // warp statistics (lane 0): chunks, chunks with candidates, candidates,
+    // contributions, leaps, leapt samples, ET rays, rays, samples left at
+    // hand-off, then a histogram of candidates per chunk: 0, 1-4, 5-16, 17-32
+    unsigned long long st[14] = {};
 #endif
     for (;;) {
         unsigned long long idx = 0;
@@ -1154,6 +1158,17 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 c_eval += __popc(emask);
                 if (LIGHT) c_shaded += __popc(cmask);
             }
+#ifdef VR_DEBUG_TIMES
+            {
+                const int nc = __popc(__ballot_sync(full, cand));
+                st[0] += 1;
+                st[1] += nc > 0;
+                st[2] += nc;
+                st[3] += __popc(cmask);
+                st[nc == 0 ? 10 : nc <= 4 ? 11 : nc <= 16 ? 12 : 13] += 1;
+                if (et_lane < 32) st[6] += 1;
+            }
+#endif
             if (is_taken && lane <= et_lane && a.blocks_hit) a.blocks_hit[b] = 1;
             if (et_lane < 32) break;
             // advance; a chunk with nothing to evaluate extends by a provable run
@@ -1177,6 +1192,10 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                     else
                         taken += k - 1;
                     next = last + k;
+#ifdef VR_DEBUG_TIMES
+                    st[4] += 1;
+                    st[5] += k - 1;
+#endif
                 }
             }
             n = next;
@@ -1188,9 +1207,13 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
         }
 #ifdef VR_DEBUG_TIMES
         ++n_rays;
+        st[7] += 1;
+        st[8] += (unsigned long long)(R.N - h.n);
 #endif
     }
 #ifdef VR_DEBUG_TIMES
+    if (a.debug_times && lane == 0)
+        for (int i = 0; i < 14; ++i) atomicAdd(a.debug_times + 4 * 148 * 64 + i, st[i]);
     if (a.debug_times && lane == 0) {
         unsigned long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));

@@ -25,7 +25,7 @@ def main(config="c3"):
     nx, ny, nz = dvol.dims
     cam = bench.make_camera(vr, cfg, (nx - 1.0, ny - 1.0, nz - 1.0))
     r = vr.Renderer(dvol, cam, vr.get_preset(cfg["tf"]), vr.RenderSettings(**cfg["settings"]), time_kernel=True)
-    buf = torch.zeros(4 * 148 * 64, dtype=torch.int64, device="cuda")  # [0, 148*32) kernel 1 warps, rest kernel 2
+    buf = torch.zeros(4 * 148 * 64 + 64, dtype=torch.int64, device="cuda")  # [0, 148*32) kernel 1 warps, rest kernel 2
     L = _lib.load()
     L.vr_debug_set_times.argtypes = [ctypes.c_void_p]
     L.vr_debug_set_times(ctypes.c_void_p(buf.data_ptr()))
@@ -33,7 +33,13 @@ def main(config="c3"):
         r.render_async()
     torch.cuda.synchronize()
     print("kernel ms", r.kernel_ms())
-    allt = buf.cpu().numpy().reshape(-1, 4)
+    host = buf.cpu().numpy()
+    st = host[4 * 148 * 64:] // 3  # three frames rendered
+    names = ["chunks", "chunks_cand", "cands", "contribs", "leaps", "leapt", "et_rays", "rays", "left",
+             "h0", "h1-4", "h5-16", "h17-32"]
+    print("heavy stats:", {n: int(v) for n, v in zip(names[:9], st[:9])},
+          "cands/chunk hist:", {n: int(v) for n, v in zip(names[9:], st[10:14])})
+    allt = host[: 4 * 148 * 64].reshape(-1, 4)
     t = allt[: 148 * 32]
     t = t[t[:, 1] > 0]
     t0 = t[:, 0].min()

@@ -2,6 +2,7 @@
 
     python tools/ncu_summary.py launches gpurun_out/launches_c3.csv profiles/r01_launches_c3.md
     python tools/ncu_summary.py full gpurun_out/prof.ncu-rep profiles/r01_ncu_raycast_c3 [config]
+    python tools/ncu_summary.py traffic c3 profiles/a.json profiles/b.json   # kernels of one frame
 
 `full` writes <out>.md (metrics + top source lines) and <out>.json; with a
 config name it also writes profiles/ncu_raycast_<config>.json, which
@@ -22,6 +23,9 @@ METRICS = [
     "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
     "smsp__thread_inst_executed_per_inst_executed.ratio", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
     "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+    "sm__sass_thread_inst_executed_op_dadd_pred_on.sum", "sm__sass_thread_inst_executed_op_dmul_pred_on.sum",
+    "sm__sass_thread_inst_executed_op_dfma_pred_on.sum", "smsp__inst_executed_op_global_ld.sum",
+    "sm__cycles_elapsed.avg.per_second",
 ]
 
 
@@ -119,5 +123,12 @@ def full(rep, out, config=None):
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "traffic":
+        parts = [json.loads(Path(p).read_text()) for p in sys.argv[3:]]
+        Path(f"profiles/ncu_raycast_{sys.argv[2]}.json").write_text(json.dumps(
+            {"kernel": " + ".join(p["kernel"].split("(")[0] for p in parts),
+             "dram_bytes_per_launch": sum(p["dram_bytes_per_launch"] for p in parts),
+             "per_kernel": {p["kernel"].split("(")[0]: p["dram_bytes_per_launch"] for p in parts},
+             "source": [Path(p).name for p in sys.argv[3:]]}, indent=1))
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
