@@ -1009,15 +1009,34 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
 // Continues the rays raycast_post_kernel handed over.  One warp owns one ray
 // and walks it 32 consecutive samples at a time, one per lane: each lane
 // evaluates its sample's exact skip predicate, transparency bound and, when
-// needed, interpolation, classification and gradient (in parallel); the
-// contributions are then composited strictly in sample order -- every lane
-// replays the same sequence of float64 updates from shuffled values -- and
-// stopped at the early-termination sample, so colour and counts are those of
-// the sequential march.  Chunks with nothing to evaluate extend by the same
-// provable leaps as the per-lane kernel, taken from the chunk's last sample.
+// needed, interpolation and classification (in parallel).  The opacity
+// recurrence is then replayed in sample order -- every lane runs the same
+// float64 updates on shuffled values -- to find the early-termination sample
+// before any gradient is computed: at a bone surface a chunk is typically all
+// visible while the ray terminates within a few samples, so gradients past
+// that sample would be wasted.  The gradient taps of the samples up to it are
+// spread over the lanes, and colours composited in order, so colour and
+// counts are those of the sequential march.  Chunks with nothing to evaluate
+// extend by the same provable leaps as the per-lane kernel, taken from the
+// chunk's last sample.
+// position of the k-th (0-based) set bit of m (k < popc(m))
+VR_D int nth_bit(unsigned m, int k) {
+    int pos = 0;
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const int c = __popc(m & ((1u << w) - 1u));
+        if (k >= c) {
+            k -= c;
+            m >>= w;
+            pos += w;
+        }
+    }
+    return pos;
+}
+
 template <bool CUBIC, bool LIGHT, bool SKIP>
 #ifndef VR_HEAVY_MIN_BLOCKS
-#define VR_HEAVY_MIN_BLOCKS 6  // <= 80 registers: 24 warps/SM (swept 1..8)
+#define VR_HEAVY_MIN_BLOCKS 5  // <= 102 registers: 20 warps/SM (swept 1..8)
 #endif
 __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_kernel(const __grid_constant__ RenderArgs a) {
     const int lane = threadIdx.x & 31;
@@ -1035,7 +1054,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
     // warp statistics (lane 0): chunks, chunks with candidates, candidates,
     // contributions, leaps, leapt samples, ET rays, rays, samples left at
     // hand-off, then a histogram of candidates per chunk: 0, 1-4, 5-16, 17-32
-    unsigned long long st[14] = {};
+    unsigned long long st[18] = {};  // + histogram of visible samples per chunk: 1-2, 3-5, 6-10, 11-32
 #endif
     for (;;) {
         unsigned long long idx = 0;
@@ -1072,75 +1091,114 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 }
                 cand = !skippable && !(cull && provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis));
             }
-            // evaluate this lane's sample
-            // (one loop body for the sample and its six gradient taps keeps a
-            // single copy of the interpolant in the kernel: q = 0 the sample,
-            // q = 1..6 the taps +x,-x,+y,-y,+z,-z)
+            // Evaluate the chunk.  Round 0 interpolates every candidate sample
+            // on its own lane and classifies it.  Opacity alone decides early
+            // termination, so the alpha recurrence is replayed right away (in
+            // sample order, identically on every lane) to find the terminating
+            // sample; only the visible samples up to it need a gradient.  Their
+            // six taps each (+x,-x,+y,-y,+z,-z) are spread over the lanes, 32 per
+            // round, and shuffled back to their sample's lane.  One loop body
+            // keeps a single copy of the interpolant in the kernel.
             double sr = 0.0, sg = 0.0, sb = 0.0, ahat = 0.0;
-            double gx = 0.0, gy = 0.0, gz = 0.0, plus = 0.0;
+            double tp[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             bool contrib = false;
-            const int nq = cand ? (LIGHT ? 7 : 1) : 0;
+            unsigned vis = 0u;  // visible lanes up to the terminating sample
+            int ntaps = 0, rank = 0, et_lane = 32;
+            const bool any_cand = __any_sync(full, cand);
 #pragma unroll 1
-            for (int q = 0; q < nq; ++q) {
+            for (int base = -32; any_cand && base < ntaps; base += 32) {
+                bool act = cand;
                 double px = x, py = y, pz = z;
                 int qi = bi, qj = bj, qk = bk;
-                if (q > 0) {
-                    const int g = q - 1;
+                if (base >= 0) {
+                    const int id = base + lane;
+                    act = id < ntaps;
+                    const int k = id / 6, g = id - 6 * k;
+                    const int src = act ? nth_bit(vis, k) : lane;
+                    px = __shfl_sync(full, x, src);
+                    py = __shfl_sync(full, y, src);
+                    pz = __shfl_sync(full, z, src);
+                    qi = __shfl_sync(full, bi, src);
+                    qj = __shfl_sync(full, bj, src);
+                    qk = __shfl_sync(full, bk, src);
+                    // branch-free: lanes of a round take different taps, and a
+                    // divergent branch here lets the compiler split the warp
                     const double hh = (g & 1) ? -0.5 : 0.5;
-                    if (g < 2) {
-                        px = x + hh;
-                        qi = owner(a, 0, px);
-                    } else if (g < 4) {
-                        py = y + hh;
-                        qj = owner(a, 1, py);
-                    } else {
-                        pz = z + hh;
-                        qk = owner(a, 2, pz);
+                    const int axis = g >> 1;
+                    px = axis == 0 ? px + hh : px;
+                    py = axis == 1 ? py + hh : py;
+                    pz = axis == 2 ? pz + hh : pz;
+                    const int o = owner(a, axis, axis == 0 ? px : axis == 1 ? py : pz);
+                    qi = axis == 0 ? o : qi;
+                    qj = axis == 1 ? o : qj;
+                    qk = axis == 2 ? o : qk;
+                }
+                // every lane interpolates (inactive lanes at a valid position):
+                // no divergent branch around the interpolant
+                const double v = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
+                if (base < 0) {
+                    if (act) {
+                        const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
+                        const double sa = __ldg(a.lut + 4 * sbin + 3);
+                        if (sa > 0.0) {  // else transparent: nothing to composite
+                            contrib = true;
+                            sr = __ldg(a.lut + 4 * sbin);
+                            sg = __ldg(a.lut + 4 * sbin + 1);
+                            sb = __ldg(a.lut + 4 * sbin + 2);
+                            ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
+                        }
+                    }
+                    // the terminating sample (_kernels.py:531-537: A += (1 - A) * a)
+                    unsigned cm = __ballot_sync(full, contrib);
+                    double A = acc_a;
+                    while (cm) {
+                        const int src = __ffs(cm) - 1;
+                        cm &= cm - 1;
+                        const double w = (1.0 - A) * __shfl_sync(full, ahat, src);
+                        A += w;
+                        if (A >= a.term_alpha) {
+                            et_lane = src;
+                            break;
+                        }
+                    }
+                    if (LIGHT) {
+                        const unsigned upto = et_lane >= 31 ? full : ((2u << et_lane) - 1u);
+                        vis = __ballot_sync(full, contrib) & upto;
+                        ntaps = 6 * __popc(vis);
+                        rank = __popc(vis & ((1u << lane) - 1u));
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < 6; ++g) {
+                        const int s = 6 * rank + g - base;
+                        const double w = __shfl_sync(full, v, s & 31);
+                        if (s >= 0 && s < 32) tp[g] = w;
                     }
                 }
-                const double v = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
-                if (q == 0) {
-                    const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
-                    const double sa = __ldg(a.lut + 4 * sbin + 3);
-                    if (!(sa > 0.0)) break;  // transparent: nothing to composite
-                    contrib = true;
-                    sr = __ldg(a.lut + 4 * sbin);
-                    sg = __ldg(a.lut + 4 * sbin + 1);
-                    sb = __ldg(a.lut + 4 * sbin + 2);
-                    ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
-                } else if (q & 1) {
-                    plus = v;
-                } else {
-                    const double dg = plus - v;
-                    if (q == 2) gx = dg;
-                    else if (q == 4) gy = dg;
-                    else gz = dg;
-                }
             }
-            if (LIGHT && contrib) {
-                gx = divide(gx, a.dsx);
-                gy = divide(gy, a.dsy);
-                gz = divide(gz, a.dsz);
+            if (LIGHT && ((vis >> lane) & 1u)) {
+                const double gx = divide(tp[0] - tp[1], a.dsx);
+                const double gy = divide(tp[2] - tp[3], a.dsy);
+                const double gz = divide(tp[4] - tp[5], a.dsz);
                 const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
                 if (norm > 1e-12)
                     shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
             }
-            // composite in sample order, identically on every lane (_kernels.py:531-537)
-            unsigned cm = __ballot_sync(full, contrib);
-            int et_lane = 32;
-            while (cm) {
-                const int src = __ffs(cm) - 1;
-                cm &= cm - 1;
-                const double r_ = __shfl_sync(full, sr, src), g_ = __shfl_sync(full, sg, src);
-                const double b_ = __shfl_sync(full, sb, src), ah = __shfl_sync(full, ahat, src);
-                const double w = (1.0 - acc_a) * ah;
-                acc_r += w * r_;
-                acc_g += w * g_;
-                acc_b += w * b_;
-                acc_a += w;
-                if (acc_a >= a.term_alpha) {
-                    et_lane = src;
-                    break;
+            // composite up to the terminating sample, in sample order,
+            // identically on every lane (_kernels.py:531-537)
+            {
+                const unsigned upto = et_lane >= 31 ? full : ((2u << et_lane) - 1u);
+                unsigned cm = __ballot_sync(full, contrib) & upto;
+                while (cm) {
+                    const int src = __ffs(cm) - 1;
+                    cm &= cm - 1;
+                    const double r_ = __shfl_sync(full, sr, src), g_ = __shfl_sync(full, sg, src);
+                    const double b_ = __shfl_sync(full, sb, src), ah = __shfl_sync(full, ahat, src);
+                    const double w = (1.0 - acc_a) * ah;
+                    acc_r += w * r_;
+                    acc_g += w * g_;
+                    acc_b += w * b_;
+                    acc_a += w;
                 }
             }
             // counts up to and including the terminating sample
@@ -1166,6 +1224,8 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 st[2] += nc;
                 st[3] += __popc(cmask);
                 st[nc == 0 ? 10 : nc <= 4 ? 11 : nc <= 16 ? 12 : 13] += 1;
+                const int nv = __popc(__ballot_sync(full, contrib));
+                if (nv) st[nv <= 2 ? 14 : nv <= 5 ? 15 : nv <= 10 ? 16 : 17] += 1;
                 if (et_lane < 32) st[6] += 1;
             }
 #endif
@@ -1173,7 +1233,6 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
             if (et_lane < 32) break;
             // advance; a chunk with nothing to evaluate extends by a provable run
             long long next = n + 32;
-            const bool any_cand = __ballot_sync(full, cand) != 0;
             if (!any_cand && n + 31 < R.N) {
                 long long k = 1;
                 if (lane == 31) {
@@ -1213,7 +1272,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
     }
 #ifdef VR_DEBUG_TIMES
     if (a.debug_times && lane == 0)
-        for (int i = 0; i < 14; ++i) atomicAdd(a.debug_times + 4 * 148 * 64 + i, st[i]);
+        for (int i = 0; i < 18; ++i) atomicAdd(a.debug_times + 4 * 148 * 64 + i, st[i]);
     if (a.debug_times && lane == 0) {
         unsigned long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));

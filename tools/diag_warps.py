@@ -38,7 +38,8 @@ def main(config="c3"):
     names = ["chunks", "chunks_cand", "cands", "contribs", "leaps", "leapt", "et_rays", "rays", "left",
              "h0", "h1-4", "h5-16", "h17-32"]
     print("heavy stats:", {n: int(v) for n, v in zip(names[:9], st[:9])},
-          "cands/chunk hist:", {n: int(v) for n, v in zip(names[9:], st[10:14])})
+          "cands/chunk hist:", {n: int(v) for n, v in zip(names[9:], st[10:14])},
+          "visible/chunk hist:", {n: int(v) for n, v in zip(["1-2", "3-5", "6-10", "11-32"], st[14:18])})
     allt = host[: 4 * 148 * 64].reshape(-1, 4)
     t = allt[: 148 * 32]
     t = t[t[:, 1] > 0]
