@@ -133,6 +133,21 @@ int vr_event_elapsed_ms(void *start, void *stop, float *ms); /* synchronizes on 
 int vr_volume_create(int device, int64_t nx, int64_t ny, int64_t nz, double sx, double sy,
                      double sz, const int16_t *src, int src_on_device, void *stream,
                      vr_volume **out);
+/* Ingest raw samples (host or device pointer) into a device volume, converting
+ * on the device.  format: VR_SAMPLE_U8 / _I16 / _U16 / _I32, samples
+ * little-endian (nz,ny,nx) x fastest.  Replaces volume.py:85-109 load_raw (u16
+ * values > 32767 clamped and counted) and, with calib = nz (slope, intercept)
+ * pairs, the calibration of dicom.py:254-295 assemble_volume (slope*s +
+ * intercept in float64, counted when outside int16, rint(clip)); the geometry
+ * checks and slice ordering stay on the host.  *clamp_count (optional) receives
+ * the number of clamped samples.  Synchronous. */
+#define VR_SAMPLE_U8 0
+#define VR_SAMPLE_I16 1
+#define VR_SAMPLE_U16 2
+#define VR_SAMPLE_I32 3 /* calibrated only: a series mixing signed and unsigned slices */
+int vr_volume_ingest(int device, int format, int64_t nx, int64_t ny, int64_t nz, double sx, double sy,
+                     double sz, const void *src, int src_on_device, const double *calib, void *stream,
+                     vr_volume **out, uint64_t *clamp_count);
 /* Generate a synthetic CT phantom on the device, bit-identical to
  * phantoms.py:98-111 generate_phantom(kind, (nx,ny,nz), spacing).  Synchronous. */
 int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, double sx,
@@ -224,6 +239,18 @@ int vr_threshold_count(const vr_volume *vol, int32_t thr, uint64_t *count, void 
 int vr_ball_counts(const vr_volume *vol, int32_t thr, const double *centres,
                    const double *radii, int64_t nballs, uint64_t *counts, uint64_t *faces,
                    void *stream);
+
+/* ---- image metrics (quality.py:37-79), device pointers, stream-ordered ----
+ * a, b: uint8 (h, w, ca|cb) images, ca/cb = 3 or 4 (alpha ignored).
+ * vr_image_sse: *sse (device) = sum over pixels and RGB of (a - b)^2, exact;
+ *   psnr = 10 log10(255^2 / (sse / (3 h w))) capped at 99 dB on the host.
+ * vr_image_ssim: *sum (device) = sum of the SSIM map over the valid region of
+ *   the Rec. 601 luma planes with the 11x11 window `window` (host, float64,
+ *   quality.py:50-54); ssim = sum / ((h - 10) (w - 10)). */
+int vr_image_sse(const uint8_t *a, const uint8_t *b, int64_t h, int64_t w, int ca, int cb, uint64_t *sse,
+                 void *stream);
+int vr_image_ssim(const uint8_t *a, const uint8_t *b, int64_t h, int64_t w, int ca, int cb, const double *window,
+                  double *sum, void *stream);
 
 #ifdef __cplusplus
 }

@@ -9,15 +9,22 @@ hand-written CUDA kernels of csrc/ behind the C ABI in include/voxelray_b200.h.
 from .blocks import Block, BlockGrid, block_stats, cull_empty, decompose, traversal_order, with_visibility
 from .errors import (
     DeviceError,
+    DimensionMismatch,
+    DuplicatePosition,
     EmptyBlock,
+    InconsistentGeometry,
     InvalidBlockSpec,
     InvalidSettings,
     IsovalueOutOfRange,
+    NonUniformSpacing,
     SizeMismatch,
+    UnknownVolume,
     VoxelrayError,
 )
+from .ingest import DeviceVolumeCache, assemble_volume_device, ingest_raw, volume_id
 from .measure import ball_counts, ball_measure, threshold_count, threshold_volume_mm3
 from .phantoms import PHANTOM_NAMES, device_phantom, generate_phantom
+from .quality import convergence_study, psnr, ssim
 from .render import (
     Camera,
     ImageRGBA,

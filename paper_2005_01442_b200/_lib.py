@@ -22,15 +22,17 @@ MODE_DVR, MODE_ISO = 0, 1
 CLS_POST, CLS_PRE, CLS_PREINT = 0, 1, 2
 PINHOLE, ORTHOGRAPHIC = 0, 1
 PHANTOM_KINDS = {"sphere": 0, "shell": 1, "torso": 2}
+SAMPLE_FORMATS = {"u8": 0, "i16": 1, "u16": 2, "i32": 3}
 
 # every symbol include/voxelray_b200.h declares
 EXPORTS = (
-    "vr_last_error", "vr_abi_version", "vr_volume_create", "vr_phantom_create",
+    "vr_last_error", "vr_abi_version", "vr_volume_create", "vr_volume_ingest", "vr_phantom_create",
     "vr_volume_destroy", "vr_volume_info", "vr_volume_data", "vr_volume_download",
     "vr_grid_create", "vr_grid_destroy", "vr_grid_shape", "vr_grid_minmax",
     "vr_grid_visibility", "vr_render", "vr_render_to_host", "vr_preclassify",
     "vr_sample_points", "vr_gradient_points", "vr_threshold_count", "vr_ball_counts",
     "vr_event_create", "vr_event_destroy", "vr_event_elapsed_ms", "vr_interleave_size",
+    "vr_image_sse", "vr_image_ssim",
 )
 
 
@@ -88,6 +90,8 @@ def load() -> ctypes.CDLL:
         "vr_last_error": ([], ctypes.c_char_p),
         "vr_abi_version": ([], ctypes.c_int),
         "vr_volume_create": ([ctypes.c_int, i64, i64, i64, f64, f64, f64, P, ctypes.c_int, P, VP], ctypes.c_int),
+        "vr_volume_ingest": ([ctypes.c_int, ctypes.c_int, i64, i64, i64, f64, f64, f64, P, ctypes.c_int, P, P, VP, P],
+                             ctypes.c_int),
         "vr_phantom_create": ([ctypes.c_int, ctypes.c_int, i64, i64, i64, f64, f64, f64, P, VP], ctypes.c_int),
         "vr_volume_destroy": ([P], ctypes.c_int),
         "vr_volume_info": ([P, P, P, P, P], ctypes.c_int),
@@ -111,6 +115,8 @@ def load() -> ctypes.CDLL:
         "vr_event_destroy": ([P], ctypes.c_int),
         "vr_event_elapsed_ms": ([P, P, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
         "vr_interleave_size": ([ctypes.POINTER(Camera), P, P], ctypes.c_int),
+        "vr_image_sse": ([P, P, i64, i64, ctypes.c_int, ctypes.c_int, P, P], ctypes.c_int),
+        "vr_image_ssim": ([P, P, i64, i64, ctypes.c_int, ctypes.c_int, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

@@ -248,6 +248,58 @@ int vr_volume_create(int device, int64_t nx, int64_t ny, int64_t nz, double sx, 
     return finish_volume(v, s, out);
 }
 
+int vr_volume_ingest(int device, int format, int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz,
+                     const void *src, int src_on_device, const double *calib, void *stream, vr_volume **out,
+                     uint64_t *clamp_count) {
+    if (!out || !src) return fail(VR_EINVALID, "null pointer");
+    if (format < vr::kFormatU8 || format > vr::kFormatI32) return fail(VR_EINVALID, "unknown sample format");
+    if (format == vr::kFormatI32 && !calib) return fail(VR_EINVALID, "i32 samples need a calibration table");
+    int rc = check_volume_args(nx, ny, nz, sx, sy, sz);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    configure_pool(device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n = (size_t)(nx * ny * nz);
+    const size_t src_bytes = n * (format == vr::kFormatU8 ? 1 : format == vr::kFormatI32 ? 4 : 2);
+    vr_volume *v = new vr_volume{device, nx, ny, nz, sx, sy, sz, nullptr, 0, 0};
+    cudaError_t e = cudaMalloc((void **)&v->data, n * sizeof(int16_t) + 16);
+    if (e != cudaSuccess) {
+        delete v;
+        return fail(VR_ENOMEM, std::string("cudaMalloc volume: ") + cudaGetErrorString(e));
+    }
+    // staging for host samples, the calibration table and the clamp counter
+    void *stage = nullptr;
+    double *d_calib = nullptr;
+    unsigned long long *d_count = nullptr;
+    const size_t calib_bytes = calib ? 2 * sizeof(double) * (size_t)nz : 0;
+    e = cudaMallocAsync((void **)&d_count, sizeof(unsigned long long) + calib_bytes, s);
+    if (e == cudaSuccess) {
+        d_calib = calib ? reinterpret_cast<double *>(d_count + 1) : nullptr;
+        e = cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
+    }
+    if (e == cudaSuccess && calib) e = cudaMemcpyAsync(d_calib, calib, calib_bytes, cudaMemcpyHostToDevice, s);
+    const void *dsrc = src;
+    if (e == cudaSuccess && !src_on_device) {
+        e = cudaMallocAsync(&stage, src_bytes, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(stage, src, src_bytes, cudaMemcpyHostToDevice, s);
+        dsrc = stage;
+    }
+    if (e == cudaSuccess)
+        e = vr::launch_ingest(dsrc, format, nx * ny, (int)nz, d_calib, v->data, d_count, s);
+    unsigned long long h_count = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h_count, d_count, sizeof(h_count), cudaMemcpyDeviceToHost, s);
+    if (stage) cudaFreeAsync(stage, s);
+    if (d_count) cudaFreeAsync(d_count, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        cudaFree(v->data);
+        delete v;
+        return cuda_fail(e, "volume ingest");
+    }
+    if (clamp_count) *clamp_count = h_count;
+    return finish_volume(v, s, out);
+}
+
 int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz,
                       void *stream, vr_volume **out) {
     if (!out) return fail(VR_EINVALID, "null pointer");
@@ -729,6 +781,32 @@ int vr_ball_counts(const vr_volume *vol, int32_t thr, const double *centres, con
     VR_CUDA(vr::launch_ball_counts(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, vol->sx, vol->sy, vol->sz,
                                    thr, centres, radii, (int)nballs, (unsigned long long *)counts,
                                    (unsigned long long *)faces, (cudaStream_t)stream));
+    return VR_OK;
+}
+
+int vr_image_sse(const uint8_t *a, const uint8_t *b, int64_t h, int64_t w, int ca, int cb, uint64_t *sse,
+                 void *stream) {
+    if (!a || !b || !sse) return fail(VR_EINVALID, "null pointer");
+    if (h < 1 || w < 1 || (ca != 3 && ca != 4) || (cb != 3 && cb != 4))
+        return fail(VR_EINVALID, "DimensionMismatch: expected (h, w, 3|4) images");
+    VR_CUDA(vr::launch_image_sse(a, b, h * w, ca, cb, (unsigned long long *)sse, (cudaStream_t)stream));
+    return VR_OK;
+}
+
+int vr_image_ssim(const uint8_t *a, const uint8_t *b, int64_t h, int64_t w, int ca, int cb, const double *window,
+                  double *sum, void *stream) {
+    if (!a || !b || !sum || !window) return fail(VR_EINVALID, "null pointer");
+    if ((ca != 3 && ca != 4) || (cb != 3 && cb != 4))
+        return fail(VR_EINVALID, "DimensionMismatch: expected (h, w, 3|4) images");
+    if (h < 11 || w < 11 || h > (1 << 20) || w > (1 << 20))
+        return fail(VR_EINVALID, "DimensionMismatch: images must be at least 11x11 for SSIM");
+    cudaStream_t s = (cudaStream_t)stream;
+    void *scratch = nullptr;
+    VR_CUDA(cudaMallocAsync(&scratch, vr::image_ssim_scratch((int)h, (int)w), s));
+    cudaError_t e = vr::launch_image_ssim(a, b, (int)h, (int)w, ca, cb, window, scratch, sum, s);
+    cudaError_t e2 = cudaFreeAsync(scratch, s);
+    VR_CUDA(e);
+    VR_CUDA(e2);
     return VR_OK;
 }
 

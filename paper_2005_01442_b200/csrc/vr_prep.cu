@@ -462,6 +462,30 @@ __global__ void __launch_bounds__(kBlock) threshold_kernel(const int16_t *__rest
     }
 }
 
+// K0: one thread per sample, grid-stride (HBM-bound, runs once per volume)
+template <typename T>
+__global__ void __launch_bounds__(kBlock) ingest_kernel(const T *__restrict__ src, long long nxy, long long n,
+                                                        const double *__restrict__ calib, int16_t *__restrict__ out,
+                                                        unsigned long long *clamped) {
+    unsigned long long c = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int v = (int)__ldg(src + i);
+        int16_t r;
+        if (calib) {
+            const long long z = i / nxy;
+            const double cal = __ldg(calib + 2 * z) * (double)v + __ldg(calib + 2 * z + 1);
+            c += (cal < -32768.0 || cal > 32767.0) ? 1 : 0;
+            r = (int16_t)rint(cal < -32768.0 ? -32768.0 : (cal > 32767.0 ? 32767.0 : cal));
+        } else {
+            c += v > 32767 ? 1 : 0;  // u16 only; u8 / i16 never exceed (i32 is always calibrated)
+            r = (int16_t)(v > 32767 ? 32767 : v);
+        }
+        out[i] = r;
+    }
+    c = warp_sum(c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(clamped, c);
+}
+
 // one CTA per ball; voxels of the ball's bounding box, exact membership test
 __global__ void __launch_bounds__(kBlock) ball_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
                                                       double sx, double sy, double sz, int thr,
@@ -644,6 +668,21 @@ cudaError_t launch_sample_points(const int16_t *vol, int nx, int ny, int nz, con
 cudaError_t launch_threshold_count(const int16_t *vol, long long n, int thr, unsigned long long *count,
                                    cudaStream_t s) {
     threshold_kernel<<<grid_for(n / 8 + 1, kBlock, 148 * 8), kBlock, 0, s>>>(vol, n, thr, count);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ingest(const void *src, int format, long long nxy, int nz, const double *calib,
+                          int16_t *out, unsigned long long *clamped, cudaStream_t s) {
+    const long long n = nxy * nz;
+    const int grid = grid_for(n, kBlock, 148 * 16);
+    if (format == kFormatU8)
+        ingest_kernel<<<grid, kBlock, 0, s>>>(static_cast<const uint8_t *>(src), nxy, n, calib, out, clamped);
+    else if (format == kFormatI16)
+        ingest_kernel<<<grid, kBlock, 0, s>>>(static_cast<const int16_t *>(src), nxy, n, calib, out, clamped);
+    else if (format == kFormatU16)
+        ingest_kernel<<<grid, kBlock, 0, s>>>(static_cast<const uint16_t *>(src), nxy, n, calib, out, clamped);
+    else
+        ingest_kernel<<<grid, kBlock, 0, s>>>(static_cast<const int32_t *>(src), nxy, n, calib, out, clamped);
     return cudaGetLastError();
 }
 

@@ -65,6 +65,17 @@ cudaError_t launch_sample_points(const int16_t *vol, int nx, int ny, int nz, con
                                  long long n, int cubic, int gradient, double sx, double sy,
                                  double sz, double *out, cudaStream_t s);
 
+// K0 ingest: samples as read from a raw file or DICOM slices -> int16 volume.
+// format 0 = u8, 1 = i16, 2 = u16 (volume.py:85-109 load_raw: u16 values above
+// 32767 clamped and counted), 3 = i32 (a DICOM series mixing signed and
+// unsigned slices, widened on the host; calibrated only).  With calib (2 doubles per z-slice: slope,
+// intercept) every sample is calibrated as in dicom.py:287-290 instead:
+// slope * s + intercept in float64, counted when outside [-32768, 32767],
+// rint(clip) -> int16.
+constexpr int kFormatU8 = 0, kFormatI16 = 1, kFormatU16 = 2, kFormatI32 = 3;
+cudaError_t launch_ingest(const void *src, int format, long long nxy, int nz, const double *calib,
+                          int16_t *out, unsigned long long *clamped, cudaStream_t s);
+
 // K4: voxels >= thr
 cudaError_t launch_threshold_count(const int16_t *vol, long long n, int thr,
                                    unsigned long long *count, cudaStream_t s);
@@ -73,5 +84,13 @@ cudaError_t launch_ball_counts(const int16_t *vol, int nx, int ny, int nz, doubl
                                double sz, int thr, const double *centres, const double *radii,
                                int nballs, unsigned long long *counts, unsigned long long *faces,
                                cudaStream_t s);
+
+// image metrics (vr_quality.cu; quality.py:37-79): exact sum of squared RGB
+// differences, and the sum of the SSIM map over the valid region
+cudaError_t launch_image_sse(const uint8_t *a, const uint8_t *b, long long npix, int ca, int cb,
+                             unsigned long long *sse, cudaStream_t s);
+size_t image_ssim_scratch(int h, int w);
+cudaError_t launch_image_ssim(const uint8_t *a, const uint8_t *b, int h, int w, int ca, int cb, const double *win_host,
+                              void *scratch, double *out_sum, cudaStream_t s);
 
 }  // namespace vr

@@ -40,6 +40,7 @@ class DeviceVolume:
         self.spacing = tuple(float(s) for s in sp)
         self.value_range = (int(vr[0]), int(vr[1]))
         self.device = int(dev.value)
+        self.clamp_count = 0  # samples clamped at ingest (ingest.py)
         self._finalizer = weakref.finalize(self, L.vr_volume_destroy, handle)
 
     @property
