@@ -706,20 +706,29 @@ struct HeavyRay {
     long long n;
     double acc[4];
     long long taken, skipped;
+    double o[3], d[3];  // the ray and its clipped sample range, so the
+    double t0;          // cooperative kernel does not redo make_ray / clip
+    long long N;
 };
 static_assert(sizeof(HeavyRay) == kHeavyRayBytes, "HeavyRay layout");
 
 // Work item -> pixel.  Items are numbered cell slot by cell slot, 128 per
 // slot, each 32-item group one 8x4 warp tile (the layout of raycast_kernel).
-VR_D bool start_ray(const RenderArgs &a, long long item, PostRay &R) {
+// (cx, cy) in the rectangle and the output index; false for padding items
+VR_D bool item_pixel(const RenderArgs &a, long long item, int &cx, int &cy, long long &out) {
     const int slot = (int)(item >> 7), local = (int)(item & 127);
     const int w = local >> 5, l = local & 31;
     const int lx = (w & 1) * 8 + (l & 7), ly = (w >> 1) * 4 + (l >> 3);
     const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
-    const int cx = (cell % a.cells_x) * kTileW + lx;
-    const int cy = (cell / a.cells_x) * kTileH + ly;
-    if (cell >= a.ncells || cx >= a.tw || cy >= a.th) return false;
-    R.out = a.il_n > 1 ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx : (long long)cy * a.tw + cx;
+    cx = (cell % a.cells_x) * kTileW + lx;
+    cy = (cell / a.cells_x) * kTileH + ly;
+    out = a.il_n > 1 ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx : (long long)cy * a.tw + cx;
+    return !(cell >= a.ncells || cx >= a.tw || cy >= a.th);
+}
+
+VR_D bool start_ray(const RenderArgs &a, long long item, PostRay &R) {
+    int cx, cy;
+    if (!item_pixel(a, item, cx, cy, R.out)) return false;
     R.r = make_ray(a, a.tx + cx, a.ty + cy);
     double t0, t1;
     clip_to_bounds(R.r, a.ext_mm, t0, t1);
@@ -835,6 +844,14 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
                 h.acc[3] = R.acc_a;
                 h.taken = R.taken;
                 h.skipped = R.skipped;
+                h.o[0] = R.r.ox;
+                h.o[1] = R.r.oy;
+                h.o[2] = R.r.oz;
+                h.d[0] = R.r.dx;
+                h.d[1] = R.r.dy;
+                h.d[2] = R.r.dz;
+                h.t0 = R.t0;
+                h.N = R.N;
                 static_cast<HeavyRay *>(a.heavy)[slot] = h;
                 R.live = false;
                 continue;
@@ -1063,7 +1080,21 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
         if ((long long)idx >= count) break;
         const HeavyRay h = static_cast<const HeavyRay *>(a.heavy)[idx];
         PostRay R;
-        start_ray(a, h.item, R);
+        {
+            int cx, cy;
+            item_pixel(a, h.item, cx, cy, R.out);
+        }
+        R.r.ox = h.o[0];
+        R.r.oy = h.o[1];
+        R.r.oz = h.o[2];
+        R.r.dx = h.d[0];
+        R.r.dy = h.d[1];
+        R.r.dz = h.d[2];
+        R.t0 = h.t0;
+        R.N = h.N;
+        R.inv[0] = R.r.dx != 0.0 ? 1.0 / R.r.dx : 0.0;  // as start_ray
+        R.inv[1] = R.r.dy != 0.0 ? 1.0 / R.r.dy : 0.0;
+        R.inv[2] = R.r.dz != 0.0 ? 1.0 / R.r.dz : 0.0;
         long long n = h.n;
         double acc_r = h.acc[0], acc_g = h.acc[1], acc_b = h.acc[2], acc_a = h.acc[3];
         long long taken = h.taken, skipped = h.skipped;

@@ -77,7 +77,7 @@ struct RenderArgs {
 constexpr int kTileW = 16;
 constexpr int kTileH = 8;
 constexpr int kThreads = 128;
-constexpr size_t kHeavyRayBytes = 64;  // sizeof(HeavyRay) in vr_raycast.cu
+constexpr size_t kHeavyRayBytes = 128;  // sizeof(HeavyRay) in vr_raycast.cu
 
 cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream);
 
