@@ -25,7 +25,16 @@ struct vr_volume {
     int ncx, ncy, ncz;
     int16_t *bricks;  // K1: the voxels in 4^3 bricks (what the ray caster reads)
     int bnx, bny, bnz;
+    short2 *win;      // per-voxel [g-1, g+2]^3 tap-window min/max, brick order
 };
+
+static void free_volume(vr_volume *v) {
+    cudaFree(v->data);
+    cudaFree(v->cells);
+    cudaFree(v->bricks);
+    cudaFree(v->win);
+    delete v;
+}
 
 struct vr_grid {
     vr_volume *vol;
@@ -192,6 +201,13 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     if (e == cudaSuccess) e = cudaMalloc((void **)&v->bricks, sizeof(int16_t) * 64 * (size_t)v->bnx * v->bny * v->bnz);
     if (e == cudaSuccess) e = vr::launch_brick_volume(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bricks, s);
     if (e == cudaSuccess) e = vr::launch_cell_minmax(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->cells, s);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&v->win, sizeof(short2) * 64 * (size_t)v->bnx * v->bny * v->bnz);
+    short2 *wtmp = nullptr;
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&wtmp, 2 * sizeof(short2) * (size_t)n, s);
+    if (e == cudaSuccess)
+        e = vr::launch_window_minmax(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bnx, v->bny, wtmp, wtmp + n,
+                                     v->win, s);
+    if (wtmp) cudaFreeAsync(wtmp, s);
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
     if (e == cudaSuccess) e = vr::launch_value_range(v->data, n, d_range, s);
     int h[2] = {0, 0};
@@ -199,10 +215,7 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     if (d_range) cudaFreeAsync(d_range, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
-        cudaFree(v->data);
-        cudaFree(v->cells);
-        cudaFree(v->bricks);
-        delete v;
+        free_volume(v);
         return cuda_fail(e, "volume value range");
     }
     v->vmin = h[0];
@@ -239,10 +252,7 @@ int vr_volume_create(int device, int64_t nx, int64_t ny, int64_t nz, double sx, 
     }
     e = cudaMemcpyAsync(v->data, src, bytes, src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) {
-        cudaFree(v->data);
-        cudaFree(v->cells);
-        cudaFree(v->bricks);
-        delete v;
+        free_volume(v);
         return cuda_fail(e, "volume upload");
     }
     return finish_volume(v, s, out);
@@ -319,10 +329,7 @@ int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, 
     }
     e = vr::launch_phantom(kind, (int)nx, (int)ny, (int)nz, v->data, s);
     if (e != cudaSuccess) {
-        cudaFree(v->data);
-        cudaFree(v->cells);
-        cudaFree(v->bricks);
-        delete v;
+        free_volume(v);
         return cuda_fail(e, "phantom kernel");
     }
     return finish_volume(v, s, out);
@@ -331,10 +338,7 @@ int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, 
 int vr_volume_destroy(vr_volume *v) {
     if (!v) return VR_OK;
     DeviceGuard g(v->device);
-    cudaFree(v->data);
-    cudaFree(v->cells);
-    cudaFree(v->bricks);
-    delete v;
+    free_volume(v);
     return VR_OK;
 }
 
@@ -649,6 +653,9 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.ncx = vol->ncx;
         a.ncy = vol->ncy;
         a.cull = 1;
+        // per-voxel window bounds behind the cell bounds (development knob VR_NO_WINDOW=1 disables)
+        const char *nw = getenv("VR_NO_WINDOW");
+        a.win = (nw && atoi(nw)) ? nullptr : vol->win;
     }
     VisScratch vs(s);
     if (grid) {

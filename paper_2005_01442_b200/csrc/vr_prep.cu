@@ -359,6 +359,42 @@ __global__ void __launch_bounds__(kBlock) cell_minmax_kernel(const int16_t *__re
     }
 }
 
+// One pass of the separable [g-1, g+2] window min/max (clamped to the
+// volume) along `axis`; the first pass reads the int16 volume, the last one
+// writes the brick layout (4^3 short2 bricks, the volume's brick order).
+template <bool FIRST, bool BRICKED>
+__global__ void __launch_bounds__(kBlock) window_pass_kernel(const void *__restrict__ in, short2 *__restrict__ out,
+                                                             int nx, int ny, int nz, int axis, int bnx, int bny) {
+    const long long n = (long long)nx * ny * nz;
+    const long long stride = axis == 0 ? 1 : axis == 1 ? (long long)nx : (long long)nx * ny;
+    const int len = axis == 0 ? nx : axis == 1 ? ny : nz;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(e % nx);
+        const long long r = e / nx;
+        const int y = (int)(r % ny), z = (int)(r / ny);
+        const int c = axis == 0 ? x : axis == 1 ? y : z;
+        const int c0 = max(c - 1, 0), c1 = min(c + 2, len - 1);
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int k = c0; k <= c1; ++k) {
+            const long long q = e + (long long)(k - c) * stride;
+            if (FIRST) {
+                const int v = __ldg(static_cast<const int16_t *>(in) + q);
+                lo = min(lo, v);
+                hi = max(hi, v);
+            } else {
+                const short2 v = __ldg(static_cast<const short2 *>(in) + q);
+                lo = min(lo, (int)v.x);
+                hi = max(hi, (int)v.y);
+            }
+        }
+        long long o = e;
+        if (BRICKED)
+            o = ((((long long)(z >> 2) * bny + (y >> 2)) * bnx + (x >> 2)) << 6) + ((z & 3) << 4) + ((y & 3) << 2) +
+                (x & 3);
+        out[o] = make_short2((short)lo, (short)hi);
+    }
+}
+
 __global__ void lut_range_kernel(const double *lut, int nbins, int *range) {
     __shared__ int first, last;
     if (threadIdx.x == 0) {
@@ -637,6 +673,16 @@ cudaError_t launch_cell_minmax(const int16_t *vol, int nx, int ny, int nz, short
     int ncx = (nx + kCell - 1) / kCell, ncy = (ny + kCell - 1) / kCell, ncz = (nz + kCell - 1) / kCell;
     long long n = (long long)ncx * ncy * ncz;
     cell_minmax_kernel<<<grid_for(n, kBlock, 148 * 32), kBlock, 0, s>>>(vol, nx, ny, nz, ncx, ncy, ncz, cells);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_window_minmax(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *tmp0,
+                                 short2 *tmp1, short2 *win, cudaStream_t s) {
+    const long long n = (long long)nx * ny * nz;
+    const int grid = grid_for(n, kBlock, 148 * 32);
+    window_pass_kernel<true, false><<<grid, kBlock, 0, s>>>(vol, tmp0, nx, ny, nz, 0, bnx, bny);
+    window_pass_kernel<false, false><<<grid, kBlock, 0, s>>>(tmp0, tmp1, nx, ny, nz, 1, bnx, bny);
+    window_pass_kernel<false, true><<<grid, kBlock, 0, s>>>(tmp1, win, nx, ny, nz, 2, bnx, bny);
     return cudaGetLastError();
 }
 

@@ -49,6 +49,15 @@ cudaError_t launch_brick_volume(const int16_t *vol, int nx, int ny, int nz, int1
 constexpr int kCell = 4;
 cudaError_t launch_cell_minmax(const int16_t *vol, int nx, int ny, int nz, short2 *cells, cudaStream_t s);
 
+// Per-voxel tap window bounds: win[g] = (min, max) of the voxels in
+// [g-1, g+2] per axis (clamped to the volume), in the volume's 4^3 brick
+// order (bnx, bny as the int16 bricks; padding entries are left unwritten and
+// never read).  Every tap of a sample whose base index is g lies in that
+// window, including block-local clamping (taps move inwards).  tmp0 / tmp1:
+// two scratch buffers of nx*ny*nz short2.
+cudaError_t launch_window_minmax(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *tmp0,
+                                 short2 *tmp1, short2 *win, cudaStream_t s);
+
 // range[0] = first LUT bin with nonzero opacity (nbins if none),
 // range[1] = last such bin (-1 if none)
 cudaError_t launch_lut_range(const double *lut, int nbins, int *range, cudaStream_t s);

@@ -47,6 +47,7 @@ struct RenderArgs {
     // the LUT's first/last bins with nonzero opacity
     const short2 *cells;
     int ncx, ncy;
+    const short2 *win;  // optional per-voxel tap-window (min, max), 4^3 brick order (bv.bpy / bv.bpz / 2)
     const int *lut_range;
     int cull;
 
