@@ -15,6 +15,7 @@ from __future__ import annotations
 import ctypes
 import math
 import time
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -253,6 +254,49 @@ class _Resolved:
     table: np.ndarray | None
 
 
+_lut_cache: dict = {}
+
+
+def _lut_for(tf: TransferFunction):
+    """build_lut(tf), memoised per TransferFunction object: its control-point
+    arrays are read-only (transfer.py) so the LUT cannot go stale."""
+    hit = _lut_cache.get(id(tf))
+    if hit is not None and hit[0]() is tf:
+        return hit[1]
+    lut = build_lut(tf)
+    if len(_lut_cache) > 64:
+        _lut_cache.clear()
+    _lut_cache[id(tf)] = (weakref.ref(tf), lut)
+    return lut
+
+
+_lut_pinned: dict = {}
+
+
+def _lut_host_copy(lut):
+    """The LUT's float64 table in pinned memory (uploaded every frame), kept per LUT object."""
+    hit = _lut_pinned.get(id(lut))
+    if hit is not None and hit[0]() is lut:
+        return hit[1]
+    buf = _pinned_empty(lut.rgba.shape, np.float64)
+    buf[...] = lut.rgba
+    if len(_lut_pinned) > 64:
+        _lut_pinned.clear()
+    _lut_pinned[id(lut)] = (weakref.ref(lut), buf)
+    return buf
+
+
+def _pinned_empty(shape, dtype):
+    """Host output buffer in page-locked memory (torch's caching host
+    allocator), so the device-to-host copy of a frame is a full-speed DMA
+    (4 MiB: 0.09 ms pinned vs 0.41 ms pageable on the B200 box)."""
+    import torch
+
+    n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    buf = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    return buf.numpy().view(dtype).reshape(shape)
+
+
 def _resolve(volume_spacing, value_range, tf: TransferFunction, settings: RenderSettings) -> _Resolved:
     """render.py:354-425: step, ref_step, LUT, mode/classification, tables."""
     lo_v, hi_v = value_range
@@ -261,7 +305,7 @@ def _resolve(volume_spacing, value_range, tf: TransferFunction, settings: Render
             f"isovalue {settings.isovalue} outside value range [{lo_v}, {hi_v}]")
     ref_step = 0.5 * min(volume_spacing)
     step = settings.step if settings.step is not None else ref_step
-    lut = build_lut(tf)
+    lut = _lut_for(tf)
     iso = settings.mode == "isosurface"
     classify = {"post": _lib.CLS_POST, "pre": _lib.CLS_PRE,
                 "preintegrated": _lib.CLS_PREINT}[settings.classification]
@@ -342,12 +386,12 @@ def render(target, camera, tf: TransferFunction, settings: RenderSettings = Rend
     dgrid = device_grid(volume, block_size, overlap, device) if use_blocks else None
     cam = camera_struct(camera, tile)
     npix = cam.tile_w * cam.tile_h
-    pixels = np.empty((cam.tile_h, cam.tile_w, 4), dtype=np.uint8)
+    pixels = _pinned_empty((cam.tile_h, cam.tile_w, 4), np.uint8)
     premult = np.empty((npix, 4)) if return_premultiplied else None
     iso = settings.mode == "isosurface"
     depth = np.empty(npix) if iso else None
     totals = np.zeros(8, dtype=np.uint64)
-    lut = np.ascontiguousarray(res.lut.rgba, dtype=np.float64)
+    lut = _lut_host_copy(res.lut)
     _lib.check(_lib.load().vr_render_to_host(
         dvol.handle, dgrid.handle if dgrid else None, ctypes.byref(cam), ctypes.byref(res.params),
         _lib.ptr(lut), _lib.ptr(res.table), _lib.ptr(pixels), _lib.ptr(premult), _lib.ptr(depth),
