@@ -24,6 +24,7 @@ reference's goldens) on all host threads.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -418,16 +419,30 @@ def run_ours(args):
 
             def call():
                 return render_sharded(host_vol, cam, tf, settings)[0]
-        for _ in range(3):
-            call()
+        for _ in range(max(args.warmup, 3)):  # the timed loop's pattern: the last frame stays alive
+            px = call()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        # as timeit does: no cyclic-GC pass inside the timed calls (a full
+        # collection of this process's heap is tens of ms, one per ~20 calls)
+        gc.collect()
+        gc.disable()
         t0 = time.perf_counter()
+        per_call = []
         for _ in range(args.steps):
+            tc = time.perf_counter()
             px = call()
+            per_call.append(time.perf_counter() - tc)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
+        gc.enable()
+        if os.environ.get("VR_E2E_DEBUG"):
+            import numpy as np
+
+            pc = np.array(per_call) * 1e3
+            print(f"e2e per call ms: mean {pc.mean():.3f} p50 {np.median(pc):.3f} max {pc.max():.3f} "
+                  f"first {pc[:5].round(3).tolist()}", file=sys.stderr)
         if world > 1:
             t = torch.tensor([e2e_s], dtype=torch.float64)
             t = t if args.dist_backend == "gloo" else t.to(dev)

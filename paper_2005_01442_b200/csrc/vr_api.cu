@@ -467,7 +467,8 @@ struct VisScratch {
         size_t off_glob = off_box + (size_t)nb * 6 * 8;
         size_t off_cnt = off_glob + (want_global ? (size_t)nb * 6 * 8 : 0);
         size_t off_uni = off_cnt + 2 * 8;
-        size_t total = off_uni + 6 * 4;
+        size_t off_list = off_uni + 8 * 4;
+        size_t total = off_list + (size_t)(nb + 1) * 4;
         cudaError_t e = mem.alloc(total);
         if (e != cudaSuccess) return e;
         char *base = (char *)mem.p;
@@ -485,6 +486,7 @@ struct VisScratch {
         v.aabb_global = want_global ? (long long *)(base + off_glob) : nullptr;
         v.counters = (unsigned long long *)(base + off_cnt);
         v.uni = (int *)(base + off_uni);
+        v.list = (int *)(base + off_list);
         v.margin = margin;
         return cudaSuccess;
     }

@@ -179,58 +179,85 @@ VR_D int classified_bin(double s, double lo, double bin_width, int nbins) {
     return (int)f;
 }
 
+// The same bin with the quotient estimated by a reciprocal multiply; the
+// exact division only runs when the estimate lies within 1e-9 of an integer
+// (the estimate is within a few ulp of the correctly rounded quotient).
+VR_D int classified_bin_fast(double s, double lo, double bin_width, double inv_width, int nbins) {
+    const double q = (s - lo) * inv_width;
+    double f = floor(q);
+    const double fr = q - f;
+    if (fr < 1e-9 || fr > 1.0 - 1e-9) f = floor((s - lo) / bin_width);
+    if (f < 0.0) return 0;
+    if (f > (double)(nbins - 1)) return nbins - 1;
+    return (int)f;
+}
+
 constexpr int kSetupThreads = 1024;
 
 // cull_empty (blocks.py:161-173) + the per-value visibility bitmask that
-// fit_bounding_box (blocks.py:176-199) tests per voxel.
+// fit_bounding_box (blocks.py:176-199) tests per voxel, and the list of
+// non-empty blocks the AABB fit walks.  One CTA.
 __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs v) {
     extern __shared__ int prefix[];  // nbins + 1
-    __shared__ int chunk_sum[kSetupThreads];
+    __shared__ int warp_tot[kSetupThreads / 32];
     __shared__ unsigned int n_empty;
-    const int tid = threadIdx.x;
-    // flags and an exclusive prefix over the bins with nonzero opacity
-    // (ClassifiedLUT.opacity_prefix, transfer.py:131-133)
-    int per = (v.nbins + kSetupThreads - 1) / kSetupThreads;
-    int b0 = tid * per, b1 = min(b0 + per, v.nbins);
+    __shared__ int n_list;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    // exclusive prefix over the bins with nonzero opacity
+    // (ClassifiedLUT.opacity_prefix, transfer.py:131-133): block-wide scan
+    const int per = (v.nbins + kSetupThreads - 1) / kSetupThreads;
+    const int b0 = min(tid * per, v.nbins), b1 = min(b0 + per, v.nbins);
     int s = 0;
     for (int i = b0; i < b1; ++i) s += (__ldg(v.lut + 4 * i + 3) > 0.0) ? 1 : 0;
-    chunk_sum[tid] = s;
-    if (tid == 0) n_empty = 0;
-    __syncthreads();
+    int incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[wid] = incl;
     if (tid == 0) {
-        int run = 0;
-        for (int i = 0; i < kSetupThreads; ++i) {
-            int c = chunk_sum[i];
-            chunk_sum[i] = run;
-            run += c;
-        }
-        prefix[v.nbins] = run;
+        n_empty = 0;
+        n_list = 0;
     }
     __syncthreads();
-    int run = chunk_sum[tid];
+    if (wid == 0) {
+        const int w = warp_tot[lane];
+        int inc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        warp_tot[lane] = inc - w;
+    }
+    __syncthreads();
+    int run = warp_tot[wid] + incl - s;
     for (int i = b0; i < b1; ++i) {
         prefix[i] = run;
         run += (__ldg(v.lut + 4 * i + 3) > 0.0) ? 1 : 0;
     }
+    if (b1 == v.nbins && b0 < b1) prefix[v.nbins] = run;
     __syncthreads();
-    // visibility bit per int16 value: lut.rgba[bin_index(v), 3] > 0
-    for (int w = tid; w < 2048; w += kSetupThreads) {
-        unsigned int bits = 0;
-        for (int k = 0; k < 32; ++k) {
-            int val = w * 32 + k - 32768;
-            int bin = classified_bin((double)val, v.lut_lo, v.bin_width, v.nbins);
-            int vis = (prefix[bin + 1] - prefix[bin]) > 0;
-            bits |= (unsigned int)vis << k;
-        }
-        v.visbits[w] = bits;
+    // visibility bit per int16 value: lut.rgba[bin_index(v), 3] > 0; one
+    // warp builds a 32-value word per ballot
+    const double inv_w = 1.0 / v.bin_width;
+    for (int w = wid; w < 2048; w += kSetupThreads / 32) {
+        const int val = w * 32 + lane - 32768;
+        const int bin = classified_bin_fast((double)val, v.lut_lo, v.bin_width, inv_w, v.nbins);
+        const unsigned int bits = __ballot_sync(0xffffffffu, (prefix[bin + 1] - prefix[bin]) > 0);
+        if (lane == 0) v.visbits[w] = bits;
     }
     // interval test per block, sentinel AABB for the fit kernel
     for (int b = tid; b < v.nblocks; b += kSetupThreads) {
-        int lo = classified_bin((double)v.vmin[b], v.lut_lo, v.bin_width, v.nbins);
-        int hi = classified_bin((double)v.vmax[b], v.lut_lo, v.bin_width, v.nbins);
+        int lo = classified_bin_fast((double)v.vmin[b], v.lut_lo, v.bin_width, inv_w, v.nbins);
+        int hi = classified_bin_fast((double)v.vmax[b], v.lut_lo, v.bin_width, inv_w, v.nbins);
         bool visible = (prefix[hi + 1] - prefix[lo]) > 0;
         v.empty[b] = visible ? 0 : 1;
-        if (!visible) atomicAdd(&n_empty, 1u);
+        if (!visible)
+            atomicAdd(&n_empty, 1u);
+        else
+            v.list[1 + atomicAdd(&n_list, 1)] = b;
         int *ab = v.aabb + 6 * b;
         ab[0] = ab[1] = ab[2] = INT_MAX;
         ab[3] = ab[4] = ab[5] = -1;
@@ -239,43 +266,50 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
     if (tid == 0) {
         v.counters[0] = n_empty;
         v.counters[1] = 0;
+        v.list[0] = n_list;
     }
     if (tid < 6) v.uni[tid] = tid < 3 ? INT_MAX : INT_MIN;
 }
 
-// fit_bounding_box (blocks.py:176-199): local min/max of visible voxels
-__global__ void __launch_bounds__(kBlock) aabb_kernel(const int16_t *__restrict__ vol, const Layout L, const VisArgs v) {
+// fit_bounding_box (blocks.py:176-199): local min/max of visible voxels.
+// Persistent: each CTA walks (non-empty block, z-slice) items; the value
+// bitmask is staged in shared memory once per CTA.
+__global__ void __launch_bounds__(kBlock) aabb_kernel(const int16_t *__restrict__ vol, const Layout L, const VisArgs v,
+                                                      int zmax) {
     __shared__ unsigned int bits[2048];
-    int b = blockIdx.x;
-    if (v.empty[b]) return;
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) bits[i] = v.visbits[i];
     __syncthreads();
-    int bi, bj, bk;
-    block_coords(L, b, bi, bj, bk);
-    int ox = block_origin(L, bi), oy = block_origin(L, bj), oz = block_origin(L, bk);
-    int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj), ez = block_extent(L, 2, bk);
-    int mnx = INT_MAX, mny = INT_MAX, mnz = INT_MAX, mxx = -1, mxy = -1, mxz = -1;
+    const int count = v.list[0];
+    const long long items = (long long)count * zmax;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int z = blockIdx.y; z < ez; z += gridDim.y) {
+    for (long long it = blockIdx.x; it < items; it += gridDim.x) {
+        const int b = v.list[1 + (int)(it / zmax)];
+        const int z = (int)(it % zmax);
+        int bi, bj, bk;
+        block_coords(L, b, bi, bj, bk);
+        const int ez = block_extent(L, 2, bk);
+        if (z >= ez) continue;
+        const int ox = block_origin(L, bi), oy = block_origin(L, bj), oz = block_origin(L, bk);
+        const int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj);
+        int mnx = INT_MAX, mny = INT_MAX, mxx = -1, mxy = -1;
         const int16_t *plane = vol + (long long)(oz + z) * L.pz + (long long)oy * L.py + ox;
         for (int y = wid; y < ey; y += nw) {
             const int16_t *row = plane + (long long)y * L.py;
             for (int x = lane; x < ex; x += 32) {
-                unsigned int u = (unsigned int)(__ldg(row + x) + 32768);
+                const unsigned int u = (unsigned int)(__ldg(row + x) + 32768);
                 if ((bits[u >> 5] >> (u & 31)) & 1u) {
                     mnx = min(mnx, x); mxx = max(mxx, x);
                     mny = min(mny, y); mxy = max(mxy, y);
-                    mnz = min(mnz, z); mxz = max(mxz, z);
                 }
             }
         }
-    }
-    mnx = warp_min(mnx); mny = warp_min(mny); mnz = warp_min(mnz);
-    mxx = warp_max(mxx); mxy = warp_max(mxy); mxz = warp_max(mxz);
-    if ((threadIdx.x & 31) == 0 && mxx >= 0) {
-        int *ab = v.aabb + 6 * b;
-        atomicMin(ab + 0, mnx); atomicMin(ab + 1, mny); atomicMin(ab + 2, mnz);
-        atomicMax(ab + 3, mxx); atomicMax(ab + 4, mxy); atomicMax(ab + 5, mxz);
+        mnx = warp_min(mnx); mny = warp_min(mny);
+        mxx = warp_max(mxx); mxy = warp_max(mxy);
+        if (lane == 0 && mxx >= 0) {
+            int *ab = v.aabb + 6 * b;
+            atomicMin(ab + 0, mnx); atomicMin(ab + 1, mny); atomicMin(ab + 2, z);
+            atomicMax(ab + 3, mxx); atomicMax(ab + 4, mxy); atomicMax(ab + 5, z);
+        }
     }
 }
 
@@ -656,8 +690,7 @@ cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs
         if (e != cudaSuccess) return e;
     }
     vis_setup_kernel<<<1, kSetupThreads, smem, s>>>(v);
-    dim3 grid(v.nblocks, zsplit_for(L));
-    aabb_kernel<<<grid, kBlock, 0, s>>>(vol, L, v);
+    aabb_kernel<<<148 * 6, kBlock, 0, s>>>(vol, L, v, zsplit_for(L));
     box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
     return cudaGetLastError();
 }

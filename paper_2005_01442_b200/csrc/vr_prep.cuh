@@ -32,6 +32,7 @@ struct VisArgs {
     long long *aabb_global;  // optional nblocks x 6 int64 inclusive global aabb (lo xyz, hi xyz)
     unsigned long long *counters;  // [0] empty blocks, [1] non-empty blocks without a visible voxel
     int *uni;                // 6: union of the fitted global AABBs (lo xyz, hi xyz)
+    int *list;               // nblocks + 1: [0] = count, then the non-empty block ids (any order)
     double margin;
 };
 cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,

@@ -477,8 +477,12 @@ class Renderer:
     def __del__(self):
         evs = getattr(self, "_events", None)
         if evs:
-            for e in evs:
-                _lib.load().vr_event_destroy(e)
+            try:
+                L = _lib.load()
+                for e in evs:
+                    L.vr_event_destroy(e)
+            except Exception:  # interpreter shutdown: module globals already torn down
+                pass
 
     def set_camera(self, camera, tile=None):
         """Point at a new view (same rectangle size); buffers are reused."""
