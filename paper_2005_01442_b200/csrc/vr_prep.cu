@@ -239,15 +239,7 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
     }
     if (b1 == v.nbins && b0 < b1) prefix[v.nbins] = run;
     __syncthreads();
-    // visibility bit per int16 value: lut.rgba[bin_index(v), 3] > 0; one
-    // warp builds a 32-value word per ballot
     const double inv_w = 1.0 / v.bin_width;
-    for (int w = wid; w < 2048; w += kSetupThreads / 32) {
-        const int val = w * 32 + lane - 32768;
-        const int bin = classified_bin_fast((double)val, v.lut_lo, v.bin_width, inv_w, v.nbins);
-        const unsigned int bits = __ballot_sync(0xffffffffu, (prefix[bin + 1] - prefix[bin]) > 0);
-        if (lane == 0) v.visbits[w] = bits;
-    }
     // interval test per block, sentinel AABB for the fit kernel
     for (int b = tid; b < v.nblocks; b += kSetupThreads) {
         int lo = classified_bin_fast((double)v.vmin[b], v.lut_lo, v.bin_width, inv_w, v.nbins);
@@ -271,6 +263,20 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
     if (tid < 6) v.uni[tid] = tid < 3 ? INT_MAX : INT_MIN;
 }
 
+// Visibility bit per int16 value, lut.rgba[bin_index(v), 3] > 0 (the test
+// fit_bounding_box applies per voxel): one warp per 32-value word, spread
+// over the GPU (65536 bins on a single SM were 12 us of issue time).
+__global__ void __launch_bounds__(kBlock) visbits_kernel(const VisArgs v) {
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (w >= 2048) return;
+    const double inv_w = 1.0 / v.bin_width;
+    const int val = w * 32 + lane - 32768;
+    const int bin = classified_bin_fast((double)val, v.lut_lo, v.bin_width, inv_w, v.nbins);
+    const unsigned int bits = __ballot_sync(0xffffffffu, __ldg(v.lut + 4 * bin + 3) > 0.0);
+    if (lane == 0) v.visbits[w] = bits;
+}
+
 // fit_bounding_box (blocks.py:176-199): local min/max of visible voxels.
 // Persistent: each CTA walks (non-empty block, z-slice) items; the value
 // bitmask is staged in shared memory once per CTA.
@@ -281,7 +287,7 @@ __global__ void __launch_bounds__(kBlock) aabb_kernel(const int16_t *__restrict_
     __syncthreads();
     const int count = v.list[0];
     const long long items = (long long)count * zmax;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31;
     for (long long it = blockIdx.x; it < items; it += gridDim.x) {
         const int b = v.list[1 + (int)(it / zmax)];
         const int z = (int)(it % zmax);
@@ -293,13 +299,26 @@ __global__ void __launch_bounds__(kBlock) aabb_kernel(const int16_t *__restrict_
         const int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj);
         int mnx = INT_MAX, mny = INT_MAX, mxx = -1, mxy = -1;
         const int16_t *plane = vol + (long long)(oz + z) * L.pz + (long long)oy * L.py + ox;
-        for (int y = wid; y < ey; y += nw) {
-            const int16_t *row = plane + (long long)y * L.py;
-            for (int x = lane; x < ex; x += 32) {
-                const unsigned int u = (unsigned int)(__ldg(row + x) + 32768);
-                if ((bits[u >> 5] >> (u & 31)) & 1u) {
-                    mnx = min(mnx, x); mxx = max(mxx, x);
-                    mny = min(mny, y); mxy = max(mxy, y);
+        // thread -> column x = tid % 64, rows y = tid / 64 + 4k: the 16 loads
+        // of a 64x64 slice are issued before any test (memory-level parallelism)
+        const int x = threadIdx.x & 63;
+        for (int x0 = 0; x0 < ex; x0 += 64) {
+            const int xx = x0 + x;
+            for (int y0 = threadIdx.x >> 6; y0 < ey; y0 += 64) {
+                int16_t val[16];
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int y = y0 + 4 * k;
+                    val[k] = (xx < ex && y < ey) ? __ldg(plane + (long long)y * L.py + xx) : (int16_t)-32768;
+                }
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int y = y0 + 4 * k;
+                    const unsigned int u = (unsigned int)((int)val[k] + 32768);
+                    if (xx < ex && y < ey && ((bits[u >> 5] >> (u & 31)) & 1u)) {
+                        mnx = min(mnx, xx); mxx = max(mxx, xx);
+                        mny = min(mny, y); mxy = max(mxy, y);
+                    }
                 }
             }
         }
@@ -689,6 +708,7 @@ cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs
         cudaError_t e = cudaFuncSetAttribute(vis_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
+    visbits_kernel<<<2048 * 32 / kBlock, kBlock, 0, s>>>(v);
     vis_setup_kernel<<<1, kSetupThreads, smem, s>>>(v);
     aabb_kernel<<<148 * 6, kBlock, 0, s>>>(vol, L, v, zsplit_for(L));
     box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
