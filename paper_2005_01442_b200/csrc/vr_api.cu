@@ -21,11 +21,11 @@ struct vr_volume {
     double sx, sy, sz;
     int16_t *data;
     int32_t vmin, vmax;
-    short2 *cells;  // dilated 4^3 cell min/max for transparency culling
+    short2 *cells;  // per 4^3 cell: union of the cube bounds below (transparency culling)
     int ncx, ncy, ncz;
     int16_t *bricks;  // K1: the voxels in 4^3 bricks (what the ray caster reads)
     int bnx, bny, bnz;
-    short2 *win;      // per-voxel [g-1, g+2]^3 tap-window min/max, brick order
+    short2 *win;      // per unit cube: bounds of the interpolant (vr_prep.cuh launch_interp_bounds), brick order
 };
 
 static void free_volume(vr_volume *v) {
@@ -200,14 +200,10 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     cudaError_t e = cudaMalloc((void **)&v->cells, sizeof(short2) * (size_t)v->ncx * v->ncy * v->ncz);
     if (e == cudaSuccess) e = cudaMalloc((void **)&v->bricks, sizeof(int16_t) * 64 * (size_t)v->bnx * v->bny * v->bnz);
     if (e == cudaSuccess) e = vr::launch_brick_volume(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bricks, s);
-    if (e == cudaSuccess) e = vr::launch_cell_minmax(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->cells, s);
     if (e == cudaSuccess) e = cudaMalloc((void **)&v->win, sizeof(short2) * 64 * (size_t)v->bnx * v->bny * v->bnz);
-    short2 *wtmp = nullptr;
-    if (e == cudaSuccess) e = cudaMallocAsync((void **)&wtmp, 2 * sizeof(short2) * (size_t)n, s);
     if (e == cudaSuccess)
-        e = vr::launch_window_minmax(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bnx, v->bny, wtmp, wtmp + n,
-                                     v->win, s);
-    if (wtmp) cudaFreeAsync(wtmp, s);
+        e = vr::launch_interp_bounds(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bnx, v->bny, v->win, v->ncx,
+                                     v->ncy, v->ncz, v->cells, s);
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
     if (e == cudaSuccess) e = vr::launch_value_range(v->data, n, d_range, s);
     int h[2] = {0, 0};
@@ -655,7 +651,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.ncx = vol->ncx;
         a.ncy = vol->ncy;
         a.cull = 1;
-        // per-voxel window bounds behind the cell bounds (development knob VR_NO_WINDOW=1 disables)
+        // per-cube bounds behind the cell bounds (development knob VR_NO_WINDOW=1 disables)
         const char *nw = getenv("VR_NO_WINDOW");
         a.win = (nw && atoi(nw)) ? nullptr : vol->win;
     }

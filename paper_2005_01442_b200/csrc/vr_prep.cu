@@ -387,64 +387,99 @@ __global__ void __launch_bounds__(kBlock) brick_kernel(const int16_t *__restrict
 
 // ------------------------------------------------------- transparency culling
 
-__global__ void __launch_bounds__(kBlock) cell_minmax_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
-                                                             int ncx, int ncy, int ncz, short2 *cells) {
-    long long n = (long long)ncx * ncy * ncz;
-    long long py = nx, pz = (long long)nx * ny;
-    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
-        int cx = (int)(c % ncx);
-        long long r = c / ncx;
-        int cy = (int)(r % ncy), cz = (int)(r / ncy);
-        int x0 = max(cx * kCell - 1, 0), x1 = min(cx * kCell + kCell + 1, nx - 1);
-        int y0 = max(cy * kCell - 1, 0), y1 = min(cy * kCell + kCell + 1, ny - 1);
-        int z0 = max(cz * kCell - 1, 0), z1 = min(cz * kCell + kCell + 1, nz - 1);
-        int lo = INT_MAX, hi = INT_MIN;
-        for (int z = z0; z <= z1; ++z)
-            for (int y = y0; y <= y1; ++y) {
-                const int16_t *row = vol + z * pz + y * py;
-                for (int x = x0; x <= x1; ++x) {
-                    int v = __ldg(row + x);
-                    lo = min(lo, v);
-                    hi = max(hi, v);
-                }
-            }
-        cells[c] = make_short2((short)lo, (short)hi);
-    }
+// ---------------------------------------------- interpolant bounds per cube
+// Bounds of the Catmull-Rom (and trilinear) interpolant over each unit cube
+// g = (gx, gy, gz) + [0,1)^3, i.e. of every sample whose base index is g,
+// under any block-local clamping of its taps.  Separable and rigorous: along
+// x each row of four taps (a, b, c, d) is a Catmull-Rom segment whose Bezier
+// control points are b, b + (c-a)/6, c - (d-b)/6, c, so the segment lies in
+// their hull (convex hull property); clamping replaces a by b or d by c, which
+// adds two control points.  Along y (then z) the rows are intervals [L, H];
+// since w0, w3 <= 0 <= w1, w2 on [0,1] the interpolant is at most the
+// segment through (L0, H1, H2, L3) and at least the one through (H0, L1, L2,
+// H3), bounded again by their hulls (clamping: L0 -> L1, L3 -> L2, ...).
+// Trilinear values are convex combinations of the cube's corners, which the
+// hulls contain.  Evaluated in float32 and rounded outwards by one unit.
+struct Span {
+    float lo, hi;
+};
+
+VR_D Span row_hull(float a, float b, float c, float d) {
+    const float k = 1.0f / 6.0f;
+    const float p1 = b + (c - a) * k, p1c = b + (c - b) * k;
+    const float p2 = c - (d - b) * k, p2c = c - (c - b) * k;
+    Span s;
+    s.lo = fminf(fminf(fminf(b, c), fminf(p1, p1c)), fminf(p2, p2c));
+    s.hi = fmaxf(fmaxf(fmaxf(b, c), fmaxf(p1, p1c)), fmaxf(p2, p2c));
+    return s;
 }
 
-// One pass of the separable [g-1, g+2] window min/max (clamped to the
-// volume) along `axis`; the first pass reads the int16 volume, the last one
-// writes the brick layout (4^3 short2 bricks, the volume's brick order).
-template <bool FIRST, bool BRICKED>
-__global__ void __launch_bounds__(kBlock) window_pass_kernel(const void *__restrict__ in, short2 *__restrict__ out,
-                                                             int nx, int ny, int nz, int axis, int bnx, int bny) {
-    const long long n = (long long)nx * ny * nz;
-    const long long stride = axis == 0 ? 1 : axis == 1 ? (long long)nx : (long long)nx * ny;
-    const int len = axis == 0 ? nx : axis == 1 ? ny : nz;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-        const int x = (int)(e % nx);
-        const long long r = e / nx;
-        const int y = (int)(r % ny), z = (int)(r / ny);
-        const int c = axis == 0 ? x : axis == 1 ? y : z;
-        const int c0 = max(c - 1, 0), c1 = min(c + 2, len - 1);
-        int lo = INT_MAX, hi = INT_MIN;
-        for (int k = c0; k <= c1; ++k) {
-            const long long q = e + (long long)(k - c) * stride;
-            if (FIRST) {
-                const int v = __ldg(static_cast<const int16_t *>(in) + q);
-                lo = min(lo, v);
-                hi = max(hi, v);
-            } else {
-                const short2 v = __ldg(static_cast<const short2 *>(in) + q);
-                lo = min(lo, (int)v.x);
-                hi = max(hi, (int)v.y);
-            }
+VR_D Span span_hull(Span s0, Span s1, Span s2, Span s3) {
+    const float k = 1.0f / 6.0f;
+    const float l0 = fminf(s0.lo, s1.lo), l3 = fminf(s3.lo, s2.lo);  // clamped variants
+    const float h0 = fmaxf(s0.hi, s1.hi), h3 = fmaxf(s3.hi, s2.hi);
+    Span r;
+    r.hi = fmaxf(fmaxf(s1.hi, s2.hi), fmaxf(s1.hi + (s2.hi - l0) * k, s2.hi - (l3 - s1.hi) * k));
+    r.lo = fminf(fminf(s1.lo, s2.lo), fminf(s1.lo + (s2.lo - h0) * k, s2.lo - (h3 - s1.lo) * k));
+    return r;
+}
+
+constexpr int kCubeTile = 8;
+constexpr int kCubeHalo = kCubeTile + 3;
+
+// one CTA = 8^3 cubes; the taps [g-1, g+2] of the tile staged in shared memory
+__global__ void __launch_bounds__(512) cube_bound_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
+                                                         int bnx, int bny, short2 *__restrict__ cubes) {
+    __shared__ float tile[kCubeHalo][kCubeHalo][kCubeHalo];
+    const int x0 = blockIdx.x * kCubeTile, y0 = blockIdx.y * kCubeTile, z0 = blockIdx.z * kCubeTile;
+    const long long py = nx, pz = (long long)nx * ny;
+    for (int i = threadIdx.x; i < kCubeHalo * kCubeHalo * kCubeHalo; i += blockDim.x) {
+        const int lx = i % kCubeHalo, ly = (i / kCubeHalo) % kCubeHalo, lz = i / (kCubeHalo * kCubeHalo);
+        const int gx = min(max(x0 - 1 + lx, 0), nx - 1);
+        const int gy = min(max(y0 - 1 + ly, 0), ny - 1);
+        const int gz = min(max(z0 - 1 + lz, 0), nz - 1);
+        tile[lz][ly][lx] = (float)__ldg(vol + gz * pz + gy * py + gx);
+    }
+    __syncthreads();
+    const int cx = threadIdx.x & 7, cy = (threadIdx.x >> 3) & 7, cz = threadIdx.x >> 6;
+    const int gx = x0 + cx, gy = y0 + cy, gz = z0 + cz;
+    if (gx >= nx || gy >= ny || gz >= nz) return;
+    Span planes[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        Span rows[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float *r = &tile[cz + k][cy + j][cx];
+            rows[j] = row_hull(r[0], r[1], r[2], r[3]);
         }
-        long long o = e;
-        if (BRICKED)
-            o = ((((long long)(z >> 2) * bny + (y >> 2)) * bnx + (x >> 2)) << 6) + ((z & 3) << 4) + ((y & 3) << 2) +
-                (x & 3);
-        out[o] = make_short2((short)lo, (short)hi);
+        planes[k] = span_hull(rows[0], rows[1], rows[2], rows[3]);
+    }
+    const Span v = span_hull(planes[0], planes[1], planes[2], planes[3]);
+    const float lo = fmaxf(floorf(v.lo) - 1.0f, -32768.0f), hi = fminf(ceilf(v.hi) + 1.0f, 32767.0f);
+    const long long o = ((((long long)(gz >> 2) * bny + (gy >> 2)) * bnx + (gx >> 2)) << 6) + ((gz & 3) << 4) +
+                        ((gy & 3) << 2) + (gx & 3);
+    cubes[o] = make_short2((short)lo, (short)hi);
+}
+
+// cells[c] = union of the bounds of the cubes in the 4^3 cell c (= one brick
+// of the cube table)
+__global__ void __launch_bounds__(kBlock) cell_from_cubes_kernel(const short2 *__restrict__ cubes, int nx, int ny,
+                                                                 int nz, int ncx, int ncy, int ncz, short2 *cells) {
+    const long long n = (long long)ncx * ncy * ncz;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+        const int cx = (int)(c % ncx);
+        const long long r = c / ncx;
+        const int cy = (int)(r % ncy), cz = (int)(r / ncy);
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int i = 0; i < 64; ++i) {
+            const int x = cx * 4 + (i & 3), y = cy * 4 + ((i >> 2) & 3), z = cz * 4 + (i >> 4);
+            if (x >= nx || y >= ny || z >= nz) continue;  // padding entries are never written
+            const short2 b = __ldg(cubes + c * 64 + i);
+            lo = min(lo, (int)b.x);
+            hi = max(hi, (int)b.y);
+        }
+        cells[c] = make_short2((short)lo, (short)hi);
     }
 }
 
@@ -722,20 +757,12 @@ cudaError_t launch_brick_volume(const int16_t *vol, int nx, int ny, int nz, int1
     return cudaGetLastError();
 }
 
-cudaError_t launch_cell_minmax(const int16_t *vol, int nx, int ny, int nz, short2 *cells, cudaStream_t s) {
-    int ncx = (nx + kCell - 1) / kCell, ncy = (ny + kCell - 1) / kCell, ncz = (nz + kCell - 1) / kCell;
-    long long n = (long long)ncx * ncy * ncz;
-    cell_minmax_kernel<<<grid_for(n, kBlock, 148 * 32), kBlock, 0, s>>>(vol, nx, ny, nz, ncx, ncy, ncz, cells);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_window_minmax(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *tmp0,
-                                 short2 *tmp1, short2 *win, cudaStream_t s) {
-    const long long n = (long long)nx * ny * nz;
-    const int grid = grid_for(n, kBlock, 148 * 32);
-    window_pass_kernel<true, false><<<grid, kBlock, 0, s>>>(vol, tmp0, nx, ny, nz, 0, bnx, bny);
-    window_pass_kernel<false, false><<<grid, kBlock, 0, s>>>(tmp0, tmp1, nx, ny, nz, 1, bnx, bny);
-    window_pass_kernel<false, true><<<grid, kBlock, 0, s>>>(tmp1, win, nx, ny, nz, 2, bnx, bny);
+cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *cubes,
+                                 int ncx, int ncy, int ncz, short2 *cells, cudaStream_t s) {
+    dim3 grid((nx + kCubeTile - 1) / kCubeTile, (ny + kCubeTile - 1) / kCubeTile, (nz + kCubeTile - 1) / kCubeTile);
+    cube_bound_kernel<<<grid, 512, 0, s>>>(vol, nx, ny, nz, bnx, bny, cubes);
+    const long long nc = (long long)ncx * ncy * ncz;
+    cell_from_cubes_kernel<<<grid_for(nc, kBlock, 148 * 32), kBlock, 0, s>>>(cubes, nx, ny, nz, ncx, ncy, ncz, cells);
     return cudaGetLastError();
 }
 

@@ -43,21 +43,16 @@ cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs
 // to whole bricks; bn* = ceil(n*/4).
 cudaError_t launch_brick_volume(const int16_t *vol, int nx, int ny, int nz, int16_t *bricks, cudaStream_t s);
 
-// Transparency culling support.  cells[c] = (min, max) of the voxels whose
-// index lies in [4c-1, 4c+5) per axis (clamped to the volume): every tap of a
-// trilinear or Catmull-Rom sample whose clamped base index floor(x) falls in
-// cell c is one of them.  TF-independent, built once per volume.
-constexpr int kCell = 4;
-cudaError_t launch_cell_minmax(const int16_t *vol, int nx, int ny, int nz, short2 *cells, cudaStream_t s);
+constexpr int kCell = 4;  // culling cell = 4^3 unit cubes
 
-// Per-voxel tap window bounds: win[g] = (min, max) of the voxels in
-// [g-1, g+2] per axis (clamped to the volume), in the volume's 4^3 brick
-// order (bnx, bny as the int16 bricks; padding entries are left unwritten and
-// never read).  Every tap of a sample whose base index is g lies in that
-// window, including block-local clamping (taps move inwards).  tmp0 / tmp1:
-// two scratch buffers of nx*ny*nz short2.
-cudaError_t launch_window_minmax(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *tmp0,
-                                 short2 *tmp1, short2 *win, cudaStream_t s);
+// Interpolant bounds (TF-independent, once per volume).  cubes[g] (brick
+// order, bnx/bny as the int16 bricks) = (lo, hi) such that every trilinear or
+// Catmull-Rom value of a sample whose base index is g -- under any block-local
+// clamping of its taps -- lies in [lo, hi]; a bound at the int16 limit is
+// saturated and proves nothing on that side.  cells[c] = union over the 4^3
+// cubes of cell c (ncx = ceil(nx/4), ...).
+cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *cubes,
+                                 int ncx, int ncy, int ncz, short2 *cells, cudaStream_t s);
 
 // range[0] = first LUT bin with nonzero opacity (nbins if none),
 // range[1] = last such bin (-1 if none)

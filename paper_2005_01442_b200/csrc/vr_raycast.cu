@@ -198,49 +198,34 @@ VR_D bool dvr_skippable(const BlockRec &r, double x, double y, double z) {
            y > (double)r.hi.y || z < (double)r.lo.z || z > (double)r.hi.z;
 }
 
-// True when the interpolated value at (x, y, z) provably classifies to a
+// Whether the interpolated value at (x, y, z) provably classifies to a
 // zero-opacity LUT bin, so the reference's sample would contribute nothing
-// (_kernels.py:513-515: alpha == 0 -> no compositing).  Every tap of the
-// sample lies in [g-1, g+2] per axis, g = floor(clamp(coordinate)) (block-
-// local clamping only moves taps inwards), all of which the dilated cell of g
-// covers; a Catmull-Rom value lies within [min - K(max-min), max + K(max-min)]
-// with K = (1.25^3 - 1)/2 < 0.5 (per axis the negative weights sum to
-// -t(1-t)/2 >= -1/8), trilinear within [min, max].  Two stages: the 4^3 cell
-// table (8 MB at 512^3, cache-resident) and, when that is inconclusive, the
-// per-voxel window table (exactly the [g-1, g+2]^3 taps' range; at C3 it
-// removes a third of the interpolations, at C2 seven eighths).  The 1e-3
-// slack dwarfs the float64 rounding of the 64-term sum (~1e-12).
-// Returns 0 (not provably transparent), 1 (by the dilated 4^3 cell: every
-// sample in the cell is, so culled_run may leap to the cell exit) or 2 (by
-// the sample's own tap window [g-1, g+2]^3, K as above: this sample only).
+// (_kernels.py:513-515: alpha == 0 -> no compositing).  The bounds come from
+// K1 (launch_interp_bounds): per unit cube g = floor(clamp(coordinate)) the
+// range of the trilinear / Catmull-Rom interpolant under any block-local tap
+// clamping, and per 4^3 cell the union of its cubes' ranges.  Returns 0 (not
+// provable), 1 (the whole cell is transparent: culled_run may leap to the
+// cell exit) or 2 (this sample's cube is: this sample only).  A bound at the
+// int16 limit is saturated and proves nothing on that side.
+VR_D bool bounds_transparent(const RenderArgs &a, short2 b, int first_vis, int last_vis) {
+    const double up = b.y >= 32767 ? 1e9 : (double)b.y;
+    const double dn = b.x <= -32768 ? -1e9 : (double)b.x;
+    return lut_bin(up, a.lut_lo, a.lut_inv_w, a.nlut) < first_vis ||
+           lut_bin(dn, a.lut_lo, a.lut_inv_w, a.nlut) > last_vis;
+}
+
 template <bool CUBIC>
 VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z, int first_vis, int last_vis) {
     const int gx = (int)clampf(x, 0.0, (double)(a.L.n[0] - 1));
     const int gy = (int)clampf(y, 0.0, (double)(a.L.n[1] - 1));
     const int gz = (int)clampf(z, 0.0, (double)(a.L.n[2] - 1));
-    const short2 mm = __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2));
-    const double k = CUBIC ? 0.5 : 0.0;
-    {
-        const double lo = (double)mm.x, hi = (double)mm.y;
-        const double up = hi + k * (hi - lo) + 1e-3;
-        const double dn = lo - k * (hi - lo) - 1e-3;
-        if (lut_bin(up, a.lut_lo, a.lut_inv_w, a.nlut) < first_vis ||
-            lut_bin(dn, a.lut_lo, a.lut_inv_w, a.nlut) > last_vis)
-            return 1;
-    }
+    if (bounds_transparent(a, __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2)),
+                           first_vis, last_vis))
+        return 1;
     if (!a.win) return 0;
-    // second stage: the sample's own tap window [g-1, g+2]^3, a 4-byte load
-    // in the brick order of the volume (64 entries per brick)
     const short2 w = __ldg(a.win + (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
                            ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3));
-    const double kw = CUBIC ? 0.4767 : 0.0;  // (1.25^3 - 1) / 2 = 0.476563
-    const double lo = (double)w.x, hi = (double)w.y;
-    const double up = hi + kw * (hi - lo) + 1e-3;
-    const double dn = lo - kw * (hi - lo) - 1e-3;
-    return (lut_bin(up, a.lut_lo, a.lut_inv_w, a.nlut) < first_vis ||
-            lut_bin(dn, a.lut_lo, a.lut_inv_w, a.nlut) > last_vis)
-               ? 2
-               : 0;
+    return bounds_transparent(a, w, first_vis, last_vis) ? 2 : 0;
 }
 
 // Parameter interval in which the (exact) ray lies inside the box [lo, hi]
