@@ -153,6 +153,14 @@ int vr_volume_ingest(int device, int format, int64_t nx, int64_t ny, int64_t nz,
 int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, double sx,
                       double sy, double sz, void *stream, vr_volume **out);
 int vr_volume_destroy(vr_volume *vol);
+/* Copy the transparency-culling tables K1 built (host buffers, synchronous):
+ * cubes = ceil(nx/4)*ceil(ny/4)*ceil(nz/4)*64 (lo, hi) int16 pairs in 4^3 brick
+ * order (entry of voxel g: brick (gz/4, gy/4, gx/4) x-fastest, then
+ * (gz%4, gy%4, gx%4) x-fastest; padding entries undefined): every trilinear or
+ * Catmull-Rom value of a sample whose base index is g lies in [lo, hi] unless
+ * saturated at the int16 limit; cells = ceil(n/4)^3 pairs, the union over
+ * each brick.  Either pointer may be NULL.  (Test / inspection entry point.) */
+int vr_volume_culling_tables(const vr_volume *vol, int16_t *cubes, int16_t *cells);
 /* dims = (nx, ny, nz), spacing = (sx, sy, sz), value_range = (min, max) */
 int vr_volume_info(const vr_volume *vol, int64_t dims[3], double spacing[3],
                    int32_t value_range[2], int *device);

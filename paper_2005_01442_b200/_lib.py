@@ -27,7 +27,7 @@ SAMPLE_FORMATS = {"u8": 0, "i16": 1, "u16": 2, "i32": 3}
 # every symbol include/voxelray_b200.h declares
 EXPORTS = (
     "vr_last_error", "vr_abi_version", "vr_volume_create", "vr_volume_ingest", "vr_phantom_create",
-    "vr_volume_destroy", "vr_volume_info", "vr_volume_data", "vr_volume_download",
+    "vr_volume_destroy", "vr_volume_culling_tables", "vr_volume_info", "vr_volume_data", "vr_volume_download",
     "vr_grid_create", "vr_grid_destroy", "vr_grid_shape", "vr_grid_minmax",
     "vr_grid_visibility", "vr_render", "vr_render_to_host", "vr_preclassify",
     "vr_sample_points", "vr_gradient_points", "vr_threshold_count", "vr_ball_counts",
@@ -94,6 +94,7 @@ def load() -> ctypes.CDLL:
                              ctypes.c_int),
         "vr_phantom_create": ([ctypes.c_int, ctypes.c_int, i64, i64, i64, f64, f64, f64, P, VP], ctypes.c_int),
         "vr_volume_destroy": ([P], ctypes.c_int),
+        "vr_volume_culling_tables": ([P, P, P], ctypes.c_int),
         "vr_volume_info": ([P, P, P, P, P], ctypes.c_int),
         "vr_volume_data": ([P], P),
         "vr_volume_download": ([P, P, P], ctypes.c_int),

@@ -331,6 +331,17 @@ int vr_phantom_create(int device, int kind, int64_t nx, int64_t ny, int64_t nz, 
     return finish_volume(v, s, out);
 }
 
+int vr_volume_culling_tables(const vr_volume *v, int16_t *cubes, int16_t *cells) {
+    if (!v || (!cubes && !cells)) return fail(VR_EINVALID, "null pointer");
+    DeviceGuard g(v->device);
+    if (cubes)
+        VR_CUDA(cudaMemcpy(cubes, v->win, sizeof(short2) * 64 * (size_t)v->bnx * v->bny * v->bnz,
+                           cudaMemcpyDeviceToHost));
+    if (cells)
+        VR_CUDA(cudaMemcpy(cells, v->cells, sizeof(short2) * (size_t)v->ncx * v->ncy * v->ncz, cudaMemcpyDeviceToHost));
+    return VR_OK;
+}
+
 int vr_volume_destroy(vr_volume *v) {
     if (!v) return VR_OK;
     DeviceGuard g(v->device);

@@ -88,6 +88,17 @@ class DeviceVolume:
             float(spacing[2]), _stream_ptr(stream), ctypes.byref(h)))
         return cls(h)
 
+    def culling_tables(self):
+        """K1's transparency-culling tables as (nz, ny, nx, 2) per-cube and
+        (ncz, ncy, ncx, 2) per-cell int16 (lo, hi) arrays (vr_volume_culling_tables)."""
+        nx, ny, nz = self.dims
+        bx, by, bz = (nx + 3) // 4, (ny + 3) // 4, (nz + 3) // 4
+        cubes = np.empty((bz, by, bx, 4, 4, 4, 2), dtype=np.int16)
+        cells = np.empty((bz, by, bx, 2), dtype=np.int16)
+        _lib.check(_lib.load().vr_volume_culling_tables(self._h, _lib.ptr(cubes), _lib.ptr(cells)))
+        lin = cubes.transpose(0, 3, 1, 4, 2, 5, 6).reshape(bz * 4, by * 4, bx * 4, 2)
+        return np.ascontiguousarray(lin[:nz, :ny, :nx]), cells
+
     def download(self) -> np.ndarray:
         nx, ny, nz = self.dims
         out = np.empty((nz, ny, nx), dtype=np.int16)
