@@ -757,12 +757,36 @@ cudaError_t launch_brick_volume(const int16_t *vol, int nx, int ny, int nz, int1
     return cudaGetLastError();
 }
 
+// mcells[m] = union of the cells of the 16^3 macro cell m (4^3 cells)
+__global__ void __launch_bounds__(kBlock) macro_from_cells_kernel(const short2 *__restrict__ cells, int ncx, int ncy,
+                                                                  int ncz, int nmx, int nmy, int nmz, short2 *mcells) {
+    const long long n = (long long)nmx * nmy * nmz;
+    for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < n; m += (long long)gridDim.x * blockDim.x) {
+        const int mx = (int)(m % nmx);
+        const long long r = m / nmx;
+        const int my = (int)(r % nmy), mz = (int)(r / nmy);
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int i = 0; i < 64; ++i) {
+            const int x = mx * 4 + (i & 3), y = my * 4 + ((i >> 2) & 3), z = mz * 4 + (i >> 4);
+            if (x >= ncx || y >= ncy || z >= ncz) continue;
+            const short2 b = __ldg(cells + ((long long)z * ncy + y) * ncx + x);
+            lo = min(lo, (int)b.x);
+            hi = max(hi, (int)b.y);
+        }
+        mcells[m] = make_short2((short)lo, (short)hi);
+    }
+}
+
 cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *cubes,
-                                 int ncx, int ncy, int ncz, short2 *cells, cudaStream_t s) {
+                                 int ncx, int ncy, int ncz, short2 *cells, int nmx, int nmy, int nmz, short2 *mcells,
+                                 cudaStream_t s) {
     dim3 grid((nx + kCubeTile - 1) / kCubeTile, (ny + kCubeTile - 1) / kCubeTile, (nz + kCubeTile - 1) / kCubeTile);
     cube_bound_kernel<<<grid, 512, 0, s>>>(vol, nx, ny, nz, bnx, bny, cubes);
     const long long nc = (long long)ncx * ncy * ncz;
     cell_from_cubes_kernel<<<grid_for(nc, kBlock, 148 * 32), kBlock, 0, s>>>(cubes, nx, ny, nz, ncx, ncy, ncz, cells);
+    const long long nm = (long long)nmx * nmy * nmz;
+    macro_from_cells_kernel<<<grid_for(nm, kBlock, 148 * 32), kBlock, 0, s>>>(cells, ncx, ncy, ncz, nmx, nmy, nmz,
+                                                                             mcells);
     return cudaGetLastError();
 }
 

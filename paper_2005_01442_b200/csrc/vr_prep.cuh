@@ -50,9 +50,11 @@ constexpr int kCell = 4;  // culling cell = 4^3 unit cubes
 // Catmull-Rom value of a sample whose base index is g -- under any block-local
 // clamping of its taps -- lies in [lo, hi]; a bound at the int16 limit is
 // saturated and proves nothing on that side.  cells[c] = union over the 4^3
-// cubes of cell c (ncx = ceil(nx/4), ...).
+// cubes of cell c (ncx = ceil(nx/4), ...); mcells[m] = union over the 4^3
+// cells of the 16^3 macro cell m (nmx = ceil(nx/16), ...).
 cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *cubes,
-                                 int ncx, int ncy, int ncz, short2 *cells, cudaStream_t s);
+                                 int ncx, int ncy, int ncz, short2 *cells, int nmx, int nmy, int nmz, short2 *mcells,
+                                 cudaStream_t s);
 
 // range[0] = first LUT bin with nonzero opacity (nbins if none),
 // range[1] = last such bin (-1 if none)

@@ -206,7 +206,9 @@ VR_D bool dvr_skippable(const BlockRec &r, double x, double y, double z) {
 // clamping, and per 4^3 cell the union of its cubes' ranges.  Returns 0 (not
 // provable), 1 (the whole cell is transparent: culled_run may leap to the
 // cell exit) or 2 (this sample's cube is: this sample only).  A bound at the
-// int16 limit is saturated and proves nothing on that side.
+// int16 limit is saturated and proves nothing on that side.  Before the cell,
+// the 16^3 macro cell (union of 64 cells) is tried: 3 = transparent there,
+// culled_run may leap to the macro-cell exit.
 VR_D bool bounds_transparent(const RenderArgs &a, short2 b, int first_vis, int last_vis) {
     const double up = b.y >= 32767 ? 1e9 : (double)b.y;
     const double dn = b.x <= -32768 ? -1e9 : (double)b.x;
@@ -219,6 +221,9 @@ VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z,
     const int gx = (int)clampf(x, 0.0, (double)(a.L.n[0] - 1));
     const int gy = (int)clampf(y, 0.0, (double)(a.L.n[1] - 1));
     const int gz = (int)clampf(z, 0.0, (double)(a.L.n[2] - 1));
+    if (a.mcells && bounds_transparent(a, __ldg(a.mcells + ((long long)(gz >> 4) * a.nmy + (gy >> 4)) * a.nmx + (gx >> 4)),
+                                       first_vis, last_vis))
+        return 3;
     if (bounds_transparent(a, __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2)),
                            first_vis, last_vis))
         return 1;
@@ -318,7 +323,7 @@ VR_D long long leap_count(const RenderArgs &a, const Ray &r, const double inv[3]
 // slack absorbs the rounding of t.
 template <bool SKIP>
 VR_D long long culled_run(const RenderArgs &a, const Ray &r, const double inv[3], double t0, long long n, double t,
-                          const double p[3], const int bidx[3], const BlockRec &rec) {
+                          const double p[3], const int bidx[3], const BlockRec &rec, int shift) {
     const double delta = 1e-6;
     const double d[3] = {r.dx, r.dy, r.dz};
     const double o[3] = {r.ox, r.oy, r.oz};
@@ -328,9 +333,10 @@ VR_D long long culled_run(const RenderArgs &a, const Ray &r, const double inv[3]
     for (int k = 0; k < 3; ++k) {
         if (d[k] == 0.0) continue;
         const int g = (int)clampf(p[k], 0.0, (double)(a.L.n[k] - 1));
-        const int c = g >> 2, clast = (a.L.n[k] - 1) >> 2;
-        if (d[k] > 0.0 && c < clast) t_safe = dmin(t_safe, ((4.0 * (c + 1) - delta) * s[k] - o[k]) * inv[k]);
-        if (d[k] < 0.0 && c > 0) t_safe = dmin(t_safe, ((4.0 * c + delta) * s[k] - o[k]) * inv[k]);
+        const int c = g >> shift, clast = (a.L.n[k] - 1) >> shift;
+        const double size = (double)(1 << shift);
+        if (d[k] > 0.0 && c < clast) t_safe = dmin(t_safe, ((size * (c + 1) - delta) * s[k] - o[k]) * inv[k]);
+        if (d[k] < 0.0 && c > 0) t_safe = dmin(t_safe, ((size * c + delta) * s[k] - o[k]) * inv[k]);
         if (SKIP) {
             if (d[k] > 0.0 && bidx[k] < a.L.nb[k] - 1) {
                 double X = (1.0 + (double)((bidx[k] + 1) * a.L.stride)) - delta;
@@ -511,7 +517,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 if (pt) {
                     const double p[3] = {x, y, z};
                     const int bidx[3] = {bi, bj, bk};
-                    long long k = pt == 1 ? culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, rec) : 1;
+                    long long k = pt != 2 ? culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, rec, pt == 3 ? 4 : 2) : 1;
                     if (k > N - n) k = N - n;
                     n_taken += k - 1;
                     n += k;
@@ -901,7 +907,8 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
             }
             const int pt = cull ? provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis) : 0;
             if (pt) {
-                long long k = pt == 1 ? culled_run<SKIP>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec) : 1;
+                long long k =
+                    pt != 2 ? culled_run<SKIP>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec, pt == 3 ? 4 : 2) : 1;
                 if (k > R.N - n) k = R.N - n;
                 R.taken += k;
                 R.n = n + k;
@@ -1112,7 +1119,8 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
             ++c_iter;
             const long long m = n + lane;
             const bool valid = m < R.N;
-            bool skippable = false, cell_only = true, cand = false, cell_run = false;
+            bool skippable = false, cell_only = true, cand = false;
+            int run_shift = 0;  // culled run leapable to the exit of a 2^run_shift cell (0: none)
             double x = 0.0, y = 0.0, z = 0.0, t = 0.0;
             int bi = 0, bj = 0, bk = 0, b = 0;
             BlockRec rec = {};
@@ -1133,7 +1141,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 if (!skippable) {
                     const int pt = cull ? provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis) : 0;
                     cand = pt == 0;
-                    cell_run = pt == 1;
+                    run_shift = pt == 3 ? 4 : pt == 1 ? 2 : 0;
                 }
             }
             // Evaluate the chunk.  Round 0 interpolates every candidate sample
@@ -1284,7 +1292,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                     const double p[3] = {x, y, z};
                     const int bidx[3] = {bi, bj, bk};
                     k = skippable ? leap_count<kPost>(a, R.r, R.inv, R.t0, m, t, p, bidx, rec, cell_only)
-                        : cell_run ? culled_run<SKIP>(a, R.r, R.inv, R.t0, m, t, p, bidx, rec)
+                        : run_shift ? culled_run<SKIP>(a, R.r, R.inv, R.t0, m, t, p, bidx, rec, run_shift)
                                    : 1;
                 }
                 k = __shfl_sync(full, k, 31);

@@ -47,7 +47,9 @@ struct RenderArgs {
     // the LUT's first/last bins with nonzero opacity
     const short2 *cells;
     int ncx, ncy;
-    const short2 *win;  // optional per-voxel tap-window (min, max), 4^3 brick order (bv.bpy / bv.bpz / 2)
+    const short2 *win;     // optional per unit cube interpolant bounds, 4^3 brick order (index as bv)
+    const short2 *mcells;  // optional per 16^3 macro cell: union of its cells' bounds
+    int nmx, nmy;
     const int *lut_range;
     int cull;
 
