@@ -7,7 +7,9 @@ reference (run in the build container, never on the GPU box):
   for shuffled series with per-slice rescale (incl. clamping, half-way rounding
   and a mixed signed/unsigned series), ``store.volume_id``;
 * quality: ``quality.psnr`` / ``quality.ssim`` on image pairs and
-  ``quality.convergence_study`` on a small phantom render.
+  ``quality.convergence_study`` on a small phantom render;
+* service: ``service.render_request`` (PNG bytes + stats dict) for request
+  bodies covering the render modes, on a small phantom.
 
 Output: tests/golden/aux.npz + aux.json.
 """
@@ -29,6 +31,7 @@ import numpy as np  # noqa: E402
 
 from voxelray import quality  # noqa: E402
 from voxelray.dicom import SliceImage, assemble_volume  # noqa: E402
+from voxelray.service import render_request  # noqa: E402
 from voxelray.phantoms import generate_phantom  # noqa: E402
 from voxelray.render import Camera, RenderSettings  # noqa: E402
 from voxelray.store import volume_id  # noqa: E402
@@ -123,6 +126,29 @@ def quality_cases(rng):
     return arrays, meta, study
 
 
+PAYLOADS = {
+    "bone_tricubic": {"camera": {"position": [100.0, 18.0, 16.0], "look_at": [18.0, 17.0, 15.0], "width": 40,
+                                 "height": 32}, "transfer": "bone",
+                      "settings": {"interpolation": "tricubic", "use_blocks": True, "block_size": 16}},
+    "soft_preint": {"camera": {"position": [18.0, 100.0, 20.0], "look_at": [18.0, 17.0, 15.0], "width": 36,
+                               "height": 36}, "transfer": "soft-tissue",
+                    "settings": {"classification": "preintegrated", "lighting": False}},
+    "iso": {"camera": {"position": [100.0, 18.0, 16.0], "look_at": [18.0, 17.0, 15.0], "width": 32, "height": 30},
+            "settings": {"mode": "isosurface", "isovalue": 600}},
+}
+
+
+def service_cases():
+    vol = generate_phantom("torso", (36, 34, 30))
+    arrays, meta = {}, []
+    for name, body in PAYLOADS.items():
+        png, stats = render_request(vol, body)
+        arrays[f"svc_{name}"] = np.frombuffer(png, dtype=np.uint8)
+        stats = {k: v for k, v in stats.items() if k != "wall_time_s"}
+        meta.append(dict(name=name, payload=body, stats=stats))
+    return arrays, dict(dims=[36, 34, 30], cases=meta)
+
+
 def main():
     rng = np.random.default_rng(20260417)
     arrays, meta = {}, {}
@@ -136,6 +162,9 @@ def main():
     arrays.update(a)
     meta["quality"] = m
     meta["convergence"] = study
+    a, m = service_cases()
+    arrays.update(a)
+    meta["service"] = m
     np.savez_compressed(OUT / "aux.npz", **arrays)
     (OUT / "aux.json").write_text(json.dumps(meta, indent=1))
     print(json.dumps(meta["quality"], indent=1), json.dumps(study["records"], indent=1))

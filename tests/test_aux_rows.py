@@ -216,3 +216,44 @@ def test_convergence_study_matches_reference(aux):
     for got, want in zip(rec, study["records"]):
         assert got["psnr_db"] == want["psnr_db"]
         assert abs(got["ssim"] - want["ssim"]) <= 1e-12
+
+
+# ------------------------------------------------ service path (§8(f) row 3)
+
+def test_request_validation_errors():
+    from paper_2005_01442_b200 import errors, service
+
+    with pytest.raises(errors.InvalidSettings, match="camera"):
+        service.prepare_render(None, {"transfer": "bone"})
+    with pytest.raises(errors.InvalidSettings, match="camera:"):
+        service.prepare_render(None, {"camera": {"position": [0, 0, 1]}})
+    with pytest.raises(errors.InvalidSettings, match="transfer:"):
+        service.prepare_render(None, {"camera": {"position": [1, 0, 0], "look_at": [0, 0, 0], "width": 4,
+                                                 "height": 4}, "transfer": "no-such-preset"})
+    assert service.status_for(errors.UnknownVolume("x")) == 404
+    assert service.status_for(errors.InvalidSettings("x")) == 422
+    assert service.status_for(errors.SizeMismatch("x")) == 400
+
+
+def test_ppm_encoding():
+    from paper_2005_01442_b200 import imageio
+
+    px = np.arange(2 * 3 * 4, dtype=np.uint8).reshape(2, 3, 4)
+    ppm = imageio.encode_ppm(px)
+    assert ppm.startswith(b"P6\n3 2\n255\n") and ppm[11:] == px[..., :3].tobytes()
+    np.testing.assert_array_equal(imageio.decode_png(imageio.encode_png(px)), px)
+
+
+@pytest.mark.gpu
+def test_render_request_bytes_match_reference(aux):
+    import paper_2005_01442_b200 as vr
+    from paper_2005_01442_b200 import service
+
+    meta, arrays = aux
+    svc = meta["service"]
+    vol = vr.generate_phantom("torso", tuple(svc["dims"]))
+    for case in svc["cases"]:
+        png, stats = service.render_request(vol, case["payload"])
+        assert png == arrays[f"svc_{case['name']}"].tobytes(), case["name"]
+        assert {k: v for k, v in stats.items() if k != "wall_time_s"} == case["stats"]
+        assert json.loads(service.stats_header(stats)[service.STATS_HEADER]) == stats
