@@ -707,6 +707,7 @@ struct PostRay {
     int stage;     // -1 none pending, 0 sample, 1..6 gradient taps
     int last_hit;
     int work;      // steps spent on this ray by this lane
+    int nvis;      // samples composited so far
     long long out;  // output index of the pixel
     long long item; // work item (pixel) the ray came from
     bool live;
@@ -765,6 +766,7 @@ VR_D bool start_ray(const RenderArgs &a, long long item, PostRay &R) {
     R.stage = -1;
     R.last_hit = -1;
     R.work = 0;
+    R.nvis = 0;
     R.item = item;
     R.live = true;
     return true;
@@ -800,13 +802,18 @@ template <bool CUBIC, bool LIGHT, bool SKIP>
 #define VR_POST_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (latency-bound; swept 1..5)
 #endif
 __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_kernel(const __grid_constant__ RenderArgs a) {
+#ifdef VR_DEBUG_TIMES
+    // rays finished here without / with taken samples (count, trip-steps), rays handed over (count, trip-steps)
+    unsigned long long dbg[6] = {};
+#endif
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const long long total = (long long)a.slots * (kTileW * kTileH);
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
-    const bool cull = a.cull != 0;
-    const int first_vis = cull ? __ldg(a.lut_range) : 0;
-    const int last_vis = cull ? __ldg(a.lut_range + 1) : 0;
+    const int first_vis = a.cull ? __ldg(a.lut_range) : 0;
+    const int last_vis = a.cull ? __ldg(a.lut_range + 1) : 0;
+    // a LUT whose first and last bins are visible can never prove a sample transparent
+    const bool cull = a.cull != 0 && (first_vis > 0 || last_vis < a.nlut - 1);
     unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
     PostRay R;
     R.live = false;
@@ -846,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
         // warp-cooperative kernel (at a clean point, nothing pending): the
         // frame would otherwise end with a few warps finishing grazing rays
         // of ~700 samples while every other SM idles
-        if (a.heavy && (drained || R.work > a.heavy_after) && R.work >= 0 && R.stage < 0 &&
+        if (a.heavy && (drained || R.work > a.heavy_after || R.nvis >= a.heavy_vis) && R.work >= 0 && R.stage < 0 &&
             R.N - R.n >= a.heavy_min_left) {
             const unsigned long long slot = atomicAdd(a.heavy_count, 1ull);
             if (slot < (unsigned long long)a.heavy_cap) {
@@ -869,6 +876,10 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
                 h.N = R.N;
                 static_cast<HeavyRay *>(a.heavy)[slot] = h;
                 R.live = false;
+#ifdef VR_DEBUG_TIMES
+                dbg[4] += 1;
+                dbg[5] += (unsigned long long)R.work;
+#endif
                 continue;
             }
             R.work = INT_MIN;  // queue full: keep it here
@@ -984,6 +995,7 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
                 }
             }
             if (composite) {
+                ++R.nvis;
                 const double w = (1.0 - R.acc_a) * R.ahat;
                 R.acc_r += w * R.sr;
                 R.acc_g += w * R.sg;
@@ -1003,8 +1015,16 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
             c_taken += (unsigned long long)R.taken;
             c_skip += (unsigned long long)R.skipped;
             R.live = false;
+#ifdef VR_DEBUG_TIMES
+            dbg[R.taken == 0 ? 0 : 2] += 1;
+            dbg[R.taken == 0 ? 1 : 3] += (unsigned long long)R.work;
+#endif
         }
     }
+#ifdef VR_DEBUG_TIMES
+    if (a.debug_times)
+        for (int i = 0; i < 6; ++i) atomicAdd(a.debug_times + 4 * 148 * 64 + 20 + i, dbg[i]);
+#endif
 #ifdef VR_DEBUG_TIMES
     if (a.debug_times) {
         unsigned long long t_end;
@@ -1076,9 +1096,10 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
-    const bool cull = a.cull != 0;
-    const int first_vis = cull ? __ldg(a.lut_range) : 0;
-    const int last_vis = cull ? __ldg(a.lut_range + 1) : 0;
+    const int first_vis = a.cull ? __ldg(a.lut_range) : 0;
+    const int last_vis = a.cull ? __ldg(a.lut_range + 1) : 0;
+    // a LUT whose first and last bins are visible can never prove a sample transparent
+    const bool cull = a.cull != 0 && (first_vis > 0 || last_vis < a.nlut - 1);
     unsigned long long pushed = *a.heavy_count;
     const long long count = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
     unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;

@@ -40,6 +40,9 @@ def main(config="c3"):
     print("heavy stats:", {n: int(v) for n, v in zip(names[:9], st[:9])},
           "cands/chunk hist:", {n: int(v) for n, v in zip(names[9:], st[10:14])},
           "visible/chunk hist:", {n: int(v) for n, v in zip(["1-2", "3-5", "6-10", "11-32"], st[14:18])})
+    pst = host[4 * 148 * 64 + 20: 4 * 148 * 64 + 26] // 3
+    print("post rays: no-sample", int(pst[0]), "work", int(pst[1]), "| sampled", int(pst[2]), "work", int(pst[3]),
+          "| handed over", int(pst[4]), "work", int(pst[5]))
     allt = host[: 4 * 148 * 64].reshape(-1, 4)
     t = allt[: 148 * 32]
     t = t[t[:, 1] > 0]

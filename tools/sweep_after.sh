@@ -1,5 +1,6 @@
-for h in 1073741824 512 256 128 64 32; do
-  for c in c3 c3soft c2 c3stress; do
-    VR_HEAVY_AFTER=$h timeout 300 python bench.py --config $c --steps 10 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('after=$h', d['config']['workload'], round(d['value'],1), 'fps', round(d['roofline']['kernel_ms'],3), 'ms')"
-  done
+# sweep VR_HEAVY_VIS (hand rays over before the queue drains once they composited this many samples)
+for c in ${CONFIGS:-c3 c2 c3soft}; do
+ for v in ${VALS:-1073741824 32 16 8 4 2}; do
+  VR_HEAVY_VIS=$v timeout 300 python bench.py --config $c --steps 10 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('vis=$v', d['config']['workload'], round(d['value'],1), 'fps')"
+ done
 done
