@@ -713,7 +713,10 @@ struct PostRay {
     bool live;
 };
 
-constexpr int kPhaseACap = 8;      // cheap steps a lane may take per trip
+#ifndef VR_PHASE_A_CAP
+#define VR_PHASE_A_CAP 32  // swept 4..64: 32 best (C2 1656 -> 2279 fps vs 8; C3 +1 %)
+#endif
+constexpr int kPhaseACap = VR_PHASE_A_CAP;  // cheap steps a lane may take per trip
 
 // A long ray handed from the per-lane kernel to the warp-cooperative one:
 // everything needed to continue it exactly where it stopped.
@@ -1090,7 +1093,7 @@ VR_D int nth_bit(unsigned m, int k) {
 
 template <bool CUBIC, bool LIGHT, bool SKIP>
 #ifndef VR_HEAVY_MIN_BLOCKS
-#define VR_HEAVY_MIN_BLOCKS 5  // <= 102 registers: 20 warps/SM (swept 1..8)
+#define VR_HEAVY_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (swept 3..8 with phase-A cap 32)
 #endif
 __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_kernel(const __grid_constant__ RenderArgs a) {
     const int lane = threadIdx.x & 31;
