@@ -37,12 +37,30 @@ SKIP_MARGIN = {"trilinear": 2.0, "tricubic": 3.0}
 
 
 def _basis(position, look_at, up):
-    """Orthonormal (forward, right, true_up), computed as render.py:78-85 does."""
+    """Orthonormal (forward, right, true_up), computed as render.py:78-85 does
+    (numpy's own norm and cross, so the rays match the reference bit for bit);
+    memoised per view because numpy's small-vector overhead is ~0.1 ms."""
+    try:
+        key = (tuple(map(float, position)), tuple(map(float, look_at)), tuple(map(float, up)))
+    except TypeError:
+        key = None
+    if key is not None:
+        hit = _basis_cache.get(key)
+        if hit is not None:
+            return tuple(v.copy() for v in hit)
     fwd = np.subtract(look_at, position, dtype=np.float64)
     fwd /= np.linalg.norm(fwd)
     right = np.cross(fwd, np.asarray(up, dtype=np.float64))
     right /= np.linalg.norm(right)
-    return fwd, right, np.cross(right, fwd)
+    out = (fwd, right, np.cross(right, fwd))
+    if key is not None:
+        if len(_basis_cache) > 4096:
+            _basis_cache.clear()
+        _basis_cache[key] = tuple(v.copy() for v in out)
+    return out
+
+
+_basis_cache: dict = {}
 
 
 @dataclass(frozen=True)

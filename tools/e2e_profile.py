@@ -65,5 +65,54 @@ def main(config="c3"):
     del lut
 
 
+
+
+def host_overhead(config="c3"):
+    """render() wall time vs the bare vr_render_to_host call it makes."""
+    import ctypes
+
+    from paper_2005_01442_b200 import _lib
+    from paper_2005_01442_b200.render import _lut_host_copy, _pinned_empty, _resolve, camera_struct
+
+    cfg = bench.CONFIGS[config]
+    dvol = vr.device_phantom("torso", cfg["dims"])
+    host = vr.ScalarVolume(dvol.download(), (1.0, 1.0, 1.0), dvol.value_range)
+    host._attach_device(dvol)
+    nx, ny, nz = dvol.dims
+    cam = bench.make_camera(vr, cfg, (nx - 1.0, ny - 1.0, nz - 1.0))
+    tf, st = vr.get_preset(cfg["tf"]), vr.RenderSettings(**cfg["settings"])
+    for _ in range(5):
+        vr.render(host, cam, tf, st)
+    res = _resolve(host.spacing, host.value_range, tf, st)
+    dgrid = vr.blocks.device_grid(host, st.block_size, st.overlap, 0)
+    c = camera_struct(cam)
+    pixels = _pinned_empty((c.tile_h, c.tile_w, 4), np.uint8)
+    totals = np.zeros(8, dtype=np.uint64)
+    lut = _lut_host_copy(res.lut)
+    L = _lib.load()
+    n = 100
+
+    def bare():
+        _lib.check(L.vr_render_to_host(dvol.handle, dgrid.handle, ctypes.byref(c), ctypes.byref(res.params),
+                                       _lib.ptr(lut), None, _lib.ptr(pixels), None, None, _lib.ptr(totals), None))
+
+    for f, name in ((bare, "vr_render_to_host"), (lambda: vr.render(host, cam, tf, st), "render()")):
+        for _ in range(5):
+            f()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            f()
+        print(f"{name}: {1e3 * (time.perf_counter() - t0) / n:.3f} ms")
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(n):
+        vr.render(host, cam, tf, st)
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(15)
+
+
 if __name__ == "__main__":
-    main(*sys.argv[1:])
+    if sys.argv[1:2] == ["host"]:
+        host_overhead(*sys.argv[2:])
+    else:
+        main(*sys.argv[1:])
