@@ -407,7 +407,8 @@ def run_ours(args):
         host_vol._attach_device(dvol)
         cam = cameras[0]
         api = ("paper_2005_01442_b200.render(ScalarVolume, Camera, TF, RenderSettings) -> ImageRGBA "
-               "(C-ABI vr_render_to_host; volume cached on device)")
+               "(C-ABI vr_render_to_host; volume cached on device; LUT uploaded and the uint8 frame "
+               "written to page-locked host memory by the kernels over PCIe every step)")
         if world == 1:
             def call():
                 return vr.render(host_vol, cam, tf, settings).pixels
