@@ -74,6 +74,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
+    p.add_argument("--transport", choices=("shared", "gather"), default=None,
+                   help="N>1 frame exchange: ranks store cells into rank 0's frame over NVLink "
+                        "(shared, default with nccl) or one NCCL/gloo gather (default with gloo)")
     p.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
                    help="override a RenderSettings field of the config (ablations)")
     args = p.parse_args()
@@ -318,8 +321,19 @@ def run_ours(args):
     cameras = orbit_cameras(vr, extent, cfg["size"], views) if views > 1 else [make_camera(vr, cfg, extent)]
     tf = vr.get_preset(cfg["tf"])
     settings = vr.RenderSettings(**cfg["settings"])
+    transport = args.transport or ("shared" if args.dist_backend == "nccl" else "gather")
+    shared = None
+    if world > 1 and transport == "shared":
+        from paper_2005_01442_b200.distributed import SharedFrame
+
+        try:
+            shared = SharedFrame(cameras[0].height, cameras[0].width, device=dev.index)
+        except Exception as exc:  # no peer access between these GPUs: fall back to the gather
+            print(f"shared frame unavailable ({exc}); using the gather", file=sys.stderr)
+            transport = "gather"
     rend = vr.Renderer(dvol, cameras[0], tf, settings, device=dev.index,
-                       interleave=(world, rank) if world > 1 else None, time_kernel=True)
+                       interleave=(world, rank) if world > 1 else None, time_kernel=True,
+                       frame_out=shared.frame if shared is not None else None)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     # read after the write flush so L2 holds clean lines: the timed frame then
@@ -342,7 +356,9 @@ def run_ours(args):
             if views > 1:
                 rend.set_camera(cam)
             rend.render_async(stream)
-            if world > 1:
+            if shared is not None:
+                shared.publish()
+            elif world > 1:
                 packed = rend.pixels.reshape(-1, 4)
                 gather_frame(packed if args.dist_backend == "nccl" else packed.cpu(), W, H)
         if measure:
@@ -416,10 +432,10 @@ def run_ours(args):
             import torch.distributed as dist
 
             api = ("paper_2005_01442_b200.distributed.render_sharded(volume, camera, TF, settings) -> "
-                   "host frame on rank 0 (sort-first cells, NCCL gather)")
+                   f"host frame on rank 0 (sort-first cells, {transport})")
 
             def call():
-                return render_sharded(host_vol, cam, tf, settings)[0]
+                return render_sharded(host_vol, cam, tf, settings, shared=shared)[0]
         for _ in range(max(args.warmup, 3)):  # the timed loop's pattern: the last frame stays alive
             px = call()
         torch.cuda.synchronize()
@@ -480,7 +496,8 @@ def run_ours(args):
         "march_iterations": st.get("march_iterations"),
         "config": {"workload": args.config, "desc": cfg["desc"], "volume": list(cfg["dims"]),
                    "image": [W, H], "views_per_step": views, "tf": cfg["tf"],
-                   "parallelism": f"sort-first x{world} ({args.dist_backend if world > 1 else 'single GPU'})",
+                   "parallelism": (f"sort-first x{world} ({args.dist_backend}, {transport})" if world > 1
+                                   else "single GPU"),
                    "l2": "flushed between steps (512 MiB write, then 512 MiB read)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,

@@ -66,14 +66,18 @@ typedef struct vr_grid vr_grid;     /* overlapping block decomposition of a volu
  * c with c % interleave_n == interleave_k are rendered; outputs are then
  * packed cell after cell (cell c at slot c / interleave_n, 128 pixels each,
  * row-major inside the cell), so equal-size buffers from every rank
- * reassemble the frame with one gather.  interleave_n <= 1 renders the
- * rectangle with row-major outputs. */
+ * reassemble the frame with one gather.  With interleave_frame = 1 the cells
+ * are instead written at their row-major positions of the whole rectangle
+ * (buffers sized tile_w * tile_h), so every rank can store straight into one
+ * shared frame -- e.g. rank 0's, mapped into the others over NVLink (CUDA IPC)
+ * -- and the gather disappears into the kernels' epilogue.  interleave_n <= 1
+ * renders the rectangle with row-major outputs. */
 typedef struct {
     int32_t projection; /* vr_projection */
     int32_t width, height;
     int32_t tile_x, tile_y, tile_w, tile_h;
     int32_t interleave_n, interleave_k;
-    int32_t _pad;
+    int32_t interleave_frame; /* 1: interleaved cells at full-frame positions */
     double position[3];
     double fwd[3], right[3], up[3];
     double half_w, half_h;
@@ -247,6 +251,11 @@ int vr_threshold_count(const vr_volume *vol, int32_t thr, uint64_t *count, void 
 int vr_ball_counts(const vr_volume *vol, int32_t thr, const double *centres,
                    const double *radii, int64_t nballs, uint64_t *counts, uint64_t *faces,
                    void *stream);
+
+/* Let kernels running on `device` read and write `peer`'s memory (NVLink P2P),
+ * e.g. a frame of rank 0 mapped into another rank with interleave_frame = 1.
+ * Idempotent; VR_EINVALID when the pair has no peer access. */
+int vr_enable_peer_access(int device, int peer);
 
 /* ---- image metrics (quality.py:37-79), device pointers, stream-ordered ----
  * a, b: uint8 (h, w, ca|cb) images, ca/cb = 3 or 4 (alpha ignored).

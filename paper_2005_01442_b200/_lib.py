@@ -32,7 +32,7 @@ EXPORTS = (
     "vr_grid_visibility", "vr_render", "vr_render_to_host", "vr_preclassify",
     "vr_sample_points", "vr_gradient_points", "vr_threshold_count", "vr_ball_counts",
     "vr_event_create", "vr_event_destroy", "vr_event_elapsed_ms", "vr_interleave_size",
-    "vr_image_sse", "vr_image_ssim",
+    "vr_image_sse", "vr_image_ssim", "vr_enable_peer_access",
 )
 
 
@@ -41,7 +41,7 @@ class Camera(ctypes.Structure):
         ("projection", ctypes.c_int32), ("width", ctypes.c_int32), ("height", ctypes.c_int32),
         ("tile_x", ctypes.c_int32), ("tile_y", ctypes.c_int32), ("tile_w", ctypes.c_int32),
         ("tile_h", ctypes.c_int32), ("interleave_n", ctypes.c_int32),
-        ("interleave_k", ctypes.c_int32), ("_pad", ctypes.c_int32),
+        ("interleave_k", ctypes.c_int32), ("interleave_frame", ctypes.c_int32),
         ("position", ctypes.c_double * 3), ("fwd", ctypes.c_double * 3),
         ("right", ctypes.c_double * 3), ("up", ctypes.c_double * 3),
         ("half_w", ctypes.c_double), ("half_h", ctypes.c_double),
@@ -117,6 +117,7 @@ def load() -> ctypes.CDLL:
         "vr_event_elapsed_ms": ([P, P, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),
         "vr_interleave_size": ([ctypes.POINTER(Camera), P, P], ctypes.c_int),
         "vr_image_sse": ([P, P, i64, i64, ctypes.c_int, ctypes.c_int, P, P], ctypes.c_int),
+        "vr_enable_peer_access": ([ctypes.c_int, ctypes.c_int], ctypes.c_int),
         "vr_image_ssim": ([P, P, i64, i64, ctypes.c_int, ctypes.c_int, P, P, P], ctypes.c_int),
     }
     for name, (args, res) in sig.items():

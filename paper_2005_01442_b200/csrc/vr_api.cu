@@ -136,7 +136,7 @@ void cell_counts(const vr_camera *c, int &cells_x, int &ncells, int &slots, long
     ncells = cells_x * cells_y;
     if (c->interleave_n > 1) {
         slots = (ncells + c->interleave_n - 1) / c->interleave_n;
-        npix = (long long)slots * vr::kTileW * vr::kTileH;
+        npix = c->interleave_frame ? (long long)c->tile_w * c->tile_h : (long long)slots * vr::kTileW * vr::kTileH;
     } else {
         slots = ncells;
         npix = (long long)c->tile_w * c->tile_h;
@@ -596,6 +596,7 @@ static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
     cell_counts(cam, a.cells_x, a.ncells, a.slots, npix_unused);
     a.il_n = cam->interleave_n > 1 ? cam->interleave_n : 1;
     a.il_k = cam->interleave_n > 1 ? cam->interleave_k : 0;
+    a.il_packed = cam->interleave_n > 1 && !cam->interleave_frame;
     a.step = prm->step;
     a.ref_step = prm->ref_step;
     a.corr = vr::make_pow(prm->step / prm->ref_step);  // _kernels.py:338
@@ -828,6 +829,21 @@ int vr_ball_counts(const vr_volume *vol, int32_t thr, const double *centres, con
     VR_CUDA(vr::launch_ball_counts(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, vol->sx, vol->sy, vol->sz,
                                    thr, centres, radii, (int)nballs, (unsigned long long *)counts,
                                    (unsigned long long *)faces, (cudaStream_t)stream));
+    return VR_OK;
+}
+
+int vr_enable_peer_access(int device, int peer) {
+    if (device == peer) return VR_OK;
+    DeviceGuard g(device);
+    int can = 0;
+    VR_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+    if (!can) return fail(VR_EINVALID, "peer access not supported between these devices");
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return VR_OK;
+    }
+    VR_CUDA(e);
     return VR_OK;
 }
 

@@ -637,7 +637,7 @@ __global__ void __launch_bounds__(kThreads, VR_RAYCAST_MIN_BLOCKS) raycast_kerne
         double t0, t1;
         clip_to_bounds(r, a.ext_mm, t0, t1);
         RayResult res = march<KIND, CUBIC, LIGHT, SKIP>(a, r, t0, t1);
-        const long long p = a.il_n > 1 ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx
+        const long long p = a.il_packed ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx
                                         : (long long)cy * a.tw + cx;
         if (a.premult) {
             double4 *o = reinterpret_cast<double4 *>(a.premult) + p;
@@ -741,7 +741,7 @@ VR_D bool item_pixel(const RenderArgs &a, long long item, int &cx, int &cy, long
     const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
     cx = (cell % a.cells_x) * kTileW + lx;
     cy = (cell / a.cells_x) * kTileH + ly;
-    out = a.il_n > 1 ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx : (long long)cy * a.tw + cx;
+    out = a.il_packed ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx : (long long)cy * a.tw + cx;
     return !(cell >= a.ncells || cx >= a.tw || cy >= a.th);
 }
 

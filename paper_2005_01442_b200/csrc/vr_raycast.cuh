@@ -15,6 +15,7 @@ struct RenderArgs {
     // camera (render.py:125-156 or the orthographic variant)
     int projection, W, H, tx, ty, tw, th;
     int il_n, il_k;        // sort-first interleave: render cells c % il_n == il_k
+    int il_packed;         // outputs packed slot after slot (else at row-major rectangle positions)
     int cells_x, ncells;   // 16x8 cells across the rectangle, total
     int slots;             // CTAs launched (cells rendered by this call)
     double pos[3], fwd[3], right[3], up[3];

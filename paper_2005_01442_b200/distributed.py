@@ -1,4 +1,5 @@
-"""Sort-first multi-GPU rendering: interleaved 16x8 cells per rank, one gather.
+"""Sort-first multi-GPU rendering: interleaved 16x8 cells per rank, one gather
+(or none: the cells stored straight into rank 0's frame over NVLink).
 
 The frame is cut into 16x8-pixel cells numbered row-major; rank k of n renders
 cells c with c % n == k (the kernel's interleave mode, include/voxelray_b200.h)
@@ -9,6 +10,12 @@ uint8 cells to rank 0 (NCCL over NVLink on the GPU box, gloo in the CPU
 tests), where ``unpack_cells`` restores the row-major frame.  Pixels are
 independent (reference SPEC.md:354, _kernels.py:13-14), so the gathered frame
 equals the single-GPU frame bit for bit.
+
+``SharedFrame`` fuses the exchange into the render: rank 0's frame is mapped
+into every rank (CUDA IPC, peer access over NVLink/NVSwitch) and each rank's
+ray-cast kernels store their cells at their frame positions
+(``interleave_frame``), so after a barrier rank 0 holds the frame with no
+gather, no packing and no unpack pass.
 """
 
 from __future__ import annotations
@@ -91,10 +98,52 @@ def gather_frame(packed, width: int, height: int, group=None):
     return None
 
 
-def render_sharded(volume, camera, tf, settings, *, group=None, device=None):
+class SharedFrame:
+    """An (H, W, C) uint8 frame in rank 0's HBM that every rank of ``group``
+    can store into.  Collective: every rank constructs it with the same size.
+    Rank 0 allocates and exports a CUDA IPC handle (torch.multiprocessing's
+    reduction); the others map it and enable peer access from their device.
+    ``publish()`` (collective) orders every rank's stores before rank 0 reads.
+    """
+
+    def __init__(self, height: int, width: int, channels: int = 4, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        from . import _lib
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        dev = torch.cuda.current_device() if device is None else device
+        if self.rank == 0:
+            self.frame = torch.zeros((height, width, channels), dtype=torch.uint8, device=dev)
+            msg = [reduce_tensor(self.frame)]
+        else:
+            msg = [None]
+        dist.broadcast_object_list(msg, src=0, group=group)
+        if self.rank != 0:
+            rebuild, args = msg[0]
+            self.frame = rebuild(*args)
+            owner = self.frame.device.index
+            if owner != dev:
+                _lib.check(_lib.load().vr_enable_peer_access(dev, owner))
+
+    def publish(self):
+        """Every rank's stores into the frame are complete and visible to rank 0."""
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+
+
+def render_sharded(volume, camera, tf, settings, *, group=None, device=None, shared: SharedFrame | None = None):
     """Multi-GPU render of one frame: every rank calls this with the same
     arguments; rank 0 returns the (H, W, 4) uint8 frame as a host array and
-    the summed stats, other ranks return (None, stats)."""
+    the summed stats, other ranks return (None, stats).  With ``shared`` (a
+    SharedFrame of the frame's size) the cells are stored straight into rank
+    0's frame instead of gathered."""
     import torch
     import torch.distributed as dist
 
@@ -103,13 +152,20 @@ def render_sharded(volume, camera, tf, settings, *, group=None, device=None):
     n = dist.get_world_size(group) if dist.is_initialized() else 1
     k = dist.get_rank(group) if dist.is_initialized() else 0
     dev = torch.cuda.current_device() if device is None else device
-    r = Renderer(volume, camera, tf, settings, device=dev, interleave=(n, k) if n > 1 else None)
+    frame_out = shared.frame if (shared is not None and n > 1) else None
+    r = Renderer(volume, camera, tf, settings, device=dev, interleave=(n, k) if n > 1 else None,
+                 frame_out=frame_out)
     r.render_async()
-    packed = r.pixels.reshape(-1, 4)
     totals = r.totals[:2].clone()
     if n > 1:
+        if dist.get_backend(group) == "gloo":
+            totals = totals.cpu()
         dist.all_reduce(totals, group=group)
-        frame = gather_frame(packed, camera.width, camera.height, group)
+        if shared is not None:
+            shared.publish()
+            frame = shared.frame if k == 0 else None
+        else:
+            frame = gather_frame(r.pixels.reshape(-1, 4), camera.width, camera.height, group)
     else:
         frame = r.pixels
     stats = totals.cpu().tolist()

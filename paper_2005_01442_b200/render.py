@@ -435,7 +435,7 @@ class Renderer:
 
     def __init__(self, volume, camera, tf: TransferFunction, settings: RenderSettings = RenderSettings(),
                  *, device: int = 0, tile=None, interleave=None, keep_premultiplied: bool = False,
-                 per_pixel_counts: bool = False, time_kernel: bool = False):
+                 per_pixel_counts: bool = False, time_kernel: bool = False, frame_out=None):
         import torch
 
         settings.validate()
@@ -470,13 +470,22 @@ class Renderer:
                 self.dvol.handle, _lib.ptr(self.lut), p.nlut, p.lut_lo, p.lut_hi, _lib.ptr(self.rgba),
                 _lib.ptr_stream(torch.cuda.current_stream(self.device))))
         self.interleave = interleave
+        # frame_out: a (tile_h, tile_w, 4) uint8 CUDA tensor -- possibly another
+        # GPU's memory mapped here (distributed.SharedFrame) -- that this
+        # rank's interleaved cells are stored into at their frame positions
+        self.frame_out = frame_out
         self.set_camera(camera, tile)
         nblocks = self.dgrid.count if self.dgrid else 1
         n = output_pixels(self.cam)
         self.npix = n
-        shape = (self.cam.tile_h, self.cam.tile_w, 4) if n == self.cam.tile_h * self.cam.tile_w and not (
-            interleave and interleave[0] > 1) else (n, 4)
-        self.pixels = torch.empty(shape, dtype=torch.uint8, device=self.device)
+        if frame_out is not None:
+            if tuple(frame_out.shape) != (self.cam.tile_h, self.cam.tile_w, 4) or frame_out.dtype != torch.uint8:
+                raise ValueError(f"frame_out must be a ({self.cam.tile_h}, {self.cam.tile_w}, 4) uint8 tensor")
+            self.pixels = frame_out
+        else:
+            shape = (self.cam.tile_h, self.cam.tile_w, 4) if n == self.cam.tile_h * self.cam.tile_w and not (
+                interleave and interleave[0] > 1) else (n, 4)
+            self.pixels = torch.empty(shape, dtype=torch.uint8, device=self.device)
         self.premult = torch.empty((n, 4), dtype=torch.float64, device=self.device) if keep_premultiplied else None
         self.depth = torch.empty(n, dtype=torch.float64, device=self.device) if settings.mode == "isosurface" else None
         self.taken = torch.empty(n, dtype=torch.int64, device=self.device) if per_pixel_counts else None
@@ -506,6 +515,8 @@ class Renderer:
         """Point at a new view (same rectangle size); buffers are reused."""
         self.camera = camera
         self.cam = camera_struct(camera, tile, self.interleave)
+        if getattr(self, "frame_out", None) is not None:
+            self.cam.interleave_frame = 1
 
     def kernel_ms(self) -> float:
         """Duration of the last ray-cast kernel launch (CUDA events on its stream)."""
