@@ -805,7 +805,7 @@ template <bool CUBIC, bool LIGHT, bool SKIP>
 #define VR_POST_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (latency-bound; swept 1..5)
 #endif
 __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_kernel(const __grid_constant__ RenderArgs a) {
-#ifdef VR_DEBUG_TIMES
+#ifdef VR_DEBUG_STATS
     // rays finished here without / with taken samples (count, trip-steps), rays handed over (count, trip-steps)
     unsigned long long dbg[6] = {};
 #endif
@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
     R.live = false;
     bool exhausted = false;
 #ifdef VR_DEBUG_TIMES
-    unsigned long long t_begin;
+    unsigned long long t_begin, t_drain = 0, n_trips_after = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
     unsigned long long n_rays = 0;
 #endif
@@ -850,6 +850,10 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
         if (lane == 0 && a.heavy)
             head_done = *reinterpret_cast<volatile unsigned long long *>(a.work_counter) >= (unsigned long long)total;
         const bool drained = __shfl_sync(full, head_done, 0) != 0 || __any_sync(full, exhausted);
+#ifdef VR_DEBUG_TIMES
+        if (drained && t_drain == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_drain));
+        n_trips_after += drained ? 1 : 0;
+#endif
         if (!R.live) continue;
 
         // ---- once the ray queue has drained, hand long rays to the
@@ -879,7 +883,7 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
                 h.N = R.N;
                 static_cast<HeavyRay *>(a.heavy)[slot] = h;
                 R.live = false;
-#ifdef VR_DEBUG_TIMES
+#ifdef VR_DEBUG_STATS
                 dbg[4] += 1;
                 dbg[5] += (unsigned long long)R.work;
 #endif
@@ -1018,13 +1022,13 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
             c_taken += (unsigned long long)R.taken;
             c_skip += (unsigned long long)R.skipped;
             R.live = false;
-#ifdef VR_DEBUG_TIMES
+#ifdef VR_DEBUG_STATS
             dbg[R.taken == 0 ? 0 : 2] += 1;
             dbg[R.taken == 0 ? 1 : 3] += (unsigned long long)R.work;
 #endif
         }
     }
-#ifdef VR_DEBUG_TIMES
+#ifdef VR_DEBUG_STATS
     if (a.debug_times)
         for (int i = 0; i < 6; ++i) atomicAdd(a.debug_times + 4 * 148 * 64 + 20 + i, dbg[i]);
 #endif
@@ -1039,8 +1043,10 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
             a.debug_times[4 * w] = t_begin;
             a.debug_times[4 * w + 1] = t_end;
-            a.debug_times[4 * w + 2] = sm;
-            a.debug_times[4 * w + 3] = rays;
+            a.debug_times[4 * w + 2] = t_drain;
+            a.debug_times[4 * w + 3] = n_trips_after;
+            (void)sm;
+            (void)rays;
         }
     }
 #endif
@@ -1109,6 +1115,8 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
 #ifdef VR_DEBUG_TIMES
     unsigned long long t_begin, n_rays = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
+#endif
+#ifdef VR_DEBUG_STATS
     // warp statistics (lane 0): chunks, chunks with candidates, candidates,
     // contributions, leaps, leapt samples, ET rays, rays, samples left at
     // hand-off, then a histogram of candidates per chunk: 0, 1-4, 5-16, 17-32
@@ -1293,7 +1301,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 c_eval += __popc(emask);
                 if (LIGHT) c_shaded += __popc(cmask);
             }
-#ifdef VR_DEBUG_TIMES
+#ifdef VR_DEBUG_STATS
             {
                 const int nc = __popc(__ballot_sync(full, cand));
                 st[0] += 1;
@@ -1329,7 +1337,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                     else
                         taken += k - 1;
                     next = last + k;
-#ifdef VR_DEBUG_TIMES
+#ifdef VR_DEBUG_STATS
                     st[4] += 1;
                     st[5] += k - 1;
 #endif
@@ -1344,13 +1352,17 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
         }
 #ifdef VR_DEBUG_TIMES
         ++n_rays;
+#endif
+#ifdef VR_DEBUG_STATS
         st[7] += 1;
         st[8] += (unsigned long long)(R.N - h.n);
 #endif
     }
-#ifdef VR_DEBUG_TIMES
+#ifdef VR_DEBUG_STATS
     if (a.debug_times && lane == 0)
         for (int i = 0; i < 18; ++i) atomicAdd(a.debug_times + 4 * 148 * 64 + i, st[i]);
+#endif
+#ifdef VR_DEBUG_TIMES
     if (a.debug_times && lane == 0) {
         unsigned long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));

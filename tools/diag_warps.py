@@ -1,7 +1,7 @@
 """Per-warp timeline of the persistent ray-cast kernel (needs a library built
 with -DVR_DEBUG_TIMES):
 
-    python paper_2005_01442_b200/_build.py build_variants/dbg.so VR_DEBUG_TIMES
+    python paper_2005_01442_b200/_build.py build_variants/dbg.so VR_DEBUG_TIMES [VR_DEBUG_STATS]
     VR_LIB=build_variants/dbg.so python tools/diag_warps.py c3
 """
 
@@ -59,12 +59,19 @@ def main(config="c3"):
     print(f"warps {len(t)}  start max {start.max():.1f} us  end: min {end.min():.1f} "
           f"p10 {np.percentile(end, 10):.1f} p50 {np.percentile(end, 50):.1f} p90 {np.percentile(end, 90):.1f} "
           f"p99 {np.percentile(end, 99):.1f} max {end.max():.1f} us")
+    dr = t[:, 2]
+    has = dr > 0
+    if has.any():
+        tail = (t[has, 1] - dr[has]) / 1e3
+        print(f"post warps: drained seen at {((dr[has] - t0) / 1e3).min():.1f}..{((dr[has] - t0) / 1e3).max():.1f} us; "
+              f"end - drain p50 {np.percentile(tail, 50):.1f} p90 {np.percentile(tail, 90):.1f} max {tail.max():.1f} us; "
+              f"trips after drain p50 {np.percentile(t[has, 3], 50):.0f} max {t[has, 3].max()}")
     busy = np.zeros(400)
     for e in end:
         busy[: int(e / (end.max() / 400)) + 0] += 1
     print("warps alive over time (10 buckets):", [int(busy[i * 40]) for i in range(10)])
     order = np.argsort(-end)[:10]
-    print("latest warps (end us, sm):", [(round(end[i], 1), int(t[i, 2])) for i in order])
+    print("latest warps (end us, trips after drain):", [(round(end[i], 1), int(t[i, 3])) for i in order])
 
 
 if __name__ == "__main__":
