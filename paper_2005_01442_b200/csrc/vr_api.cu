@@ -482,7 +482,8 @@ struct VisScratch {
         size_t off_cnt = off_glob + (want_global ? (size_t)nb * 6 * 8 : 0);
         size_t off_uni = off_cnt + 2 * 8;
         size_t off_list = off_uni + 8 * 4;
-        size_t total = off_list + (size_t)(nb + 1) * 4;
+        size_t off_vp = off_list + (size_t)(nb + 1) * 4;
+        size_t total = off_vp + 2049 * 4;
         cudaError_t e = mem.alloc(total);
         if (e != cudaSuccess) return e;
         char *base = (char *)mem.p;
@@ -501,6 +502,11 @@ struct VisScratch {
         v.counters = (unsigned long long *)(base + off_cnt);
         v.uni = (int *)(base + off_uni);
         v.list = (int *)(base + off_list);
+        v.visprefix = (int *)(base + off_vp);
+        v.cells = gr->vol->cells;
+        v.ncx = gr->vol->ncx;
+        v.ncy = gr->vol->ncy;
+        v.ncz = gr->vol->ncz;
         v.margin = margin;
         return cudaSuccess;
     }

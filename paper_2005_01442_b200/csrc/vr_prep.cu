@@ -239,6 +239,34 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
     }
     if (b1 == v.nbins && b0 < b1) prefix[v.nbins] = run;
     __syncthreads();
+    // visible values before each visbits word (for the AABB fit's cell test)
+    {
+        int c0 = __popc(v.visbits[2 * tid]), c1 = __popc(v.visbits[2 * tid + 1]);
+        int sum = c0 + c1, inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        __syncthreads();  // warp_tot reused
+        if (lane == 31) warp_tot[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            const int w = warp_tot[lane];
+            int x = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            warp_tot[lane] = x - w;
+        }
+        __syncthreads();
+        const int ex = warp_tot[wid] + inc - sum;
+        v.visprefix[2 * tid] = ex;
+        v.visprefix[2 * tid + 1] = ex + c0;
+        if (tid == kSetupThreads - 1) v.visprefix[2048] = ex + sum;
+    }
     const double inv_w = 1.0 / v.bin_width;
     // interval test per block, sentinel AABB for the fit kernel
     for (int b = tid; b < v.nblocks; b += kSetupThreads) {
@@ -277,57 +305,92 @@ __global__ void __launch_bounds__(kBlock) visbits_kernel(const VisArgs v) {
     if (lane == 0) v.visbits[w] = bits;
 }
 
+// number of visible int16 values in [lo, hi]
+VR_D int count_visible(const unsigned int *bits, const int *prefix, int lo, int hi) {
+    const unsigned u0 = (unsigned)(lo + 32768), u1 = (unsigned)(hi + 32768);
+    const unsigned w0 = u0 >> 5, w1 = u1 >> 5;
+    const unsigned m0 = 0xffffffffu << (u0 & 31u), m1 = 0xffffffffu >> (31u - (u1 & 31u));
+    if (w0 == w1) return __popc(bits[w0] & m0 & m1);
+    return __popc(bits[w0] & m0) + __popc(bits[w1] & m1) + (prefix[w1] - prefix[w0 + 1]);
+}
+
 // fit_bounding_box (blocks.py:176-199): local min/max of visible voxels.
-// Persistent: each CTA walks (non-empty block, z-slice) items; the value
-// bitmask is staged in shared memory once per CTA.
-__global__ void __launch_bounds__(kBlock) aabb_kernel(const int16_t *__restrict__ vol, const Layout L, const VisArgs v,
-                                                      int zmax) {
+// Persistent: each CTA walks (non-empty block, 4-voxel z-layer of cells)
+// items: the layer's cells whose value bound
+// (the volume's 4^3 cell table, which covers every voxel value in the cell)
+// holds a visible value are collected, then their voxels tested one per
+// thread -- the other cells cannot hold a visible voxel.  Exact: the result is
+// that of a full scan.
+constexpr int kAabbThreads = 256;
+constexpr int kCand = 1024;  // cells examined per pass
+__global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__restrict__ vol, const Layout L,
+                                                            const VisArgs v, int zmax) {
     __shared__ unsigned int bits[2048];
-    for (int i = threadIdx.x; i < 2048; i += blockDim.x) bits[i] = v.visbits[i];
-    __syncthreads();
+    __shared__ int prefix[2049];
+    __shared__ int cand[kCand];
+    __shared__ int ncand;
     const int count = v.list[0];
-    const long long items = (long long)count * zmax;
+    const int layers = (zmax + 3) / 4 + 1;  // cell layers a block can touch
+    const long long items = (long long)count * layers;
+    if ((long long)blockIdx.x >= items) return;  // before staging 16 KB for nothing
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) bits[i] = v.visbits[i];
+    for (int i = threadIdx.x; i < 2049; i += blockDim.x) prefix[i] = v.visprefix[i];
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     for (long long it = blockIdx.x; it < items; it += gridDim.x) {
-        const int b = v.list[1 + (int)(it / zmax)];
-        const int z = (int)(it % zmax);
+        const int b = v.list[1 + (int)(it / layers)];
         int bi, bj, bk;
         block_coords(L, b, bi, bj, bk);
-        const int ez = block_extent(L, 2, bk);
-        if (z >= ez) continue;
         const int ox = block_origin(L, bi), oy = block_origin(L, bj), oz = block_origin(L, bk);
-        const int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj);
-        int mnx = INT_MAX, mny = INT_MAX, mxx = -1, mxy = -1;
-        const int16_t *plane = vol + (long long)(oz + z) * L.pz + (long long)oy * L.py + ox;
-        // thread -> column x = tid % 64, rows y = tid / 64 + 4k: the 16 loads
-        // of a 64x64 slice are issued before any test (memory-level parallelism)
-        const int x = threadIdx.x & 63;
-        for (int x0 = 0; x0 < ex; x0 += 64) {
-            const int xx = x0 + x;
-            for (int y0 = threadIdx.x >> 6; y0 < ey; y0 += 64) {
-                int16_t val[16];
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const int y = y0 + 4 * k;
-                    val[k] = (xx < ex && y < ey) ? __ldg(plane + (long long)y * L.py + xx) : (int16_t)-32768;
-                }
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const int y = y0 + 4 * k;
-                    const unsigned int u = (unsigned int)((int)val[k] + 32768);
-                    if (xx < ex && y < ey && ((bits[u >> 5] >> (u & 31)) & 1u)) {
-                        mnx = min(mnx, xx); mxx = max(mxx, xx);
-                        mny = min(mny, y); mxy = max(mxy, y);
-                    }
+        const int ex = block_extent(L, 0, bi), ey = block_extent(L, 1, bj), ez = block_extent(L, 2, bk);
+        const int cz = (oz >> 2) + (int)(it % layers);
+        if (cz > (oz + ez - 1) >> 2) continue;
+        const int cx0 = ox >> 2, cx1 = (ox + ex - 1) >> 2, cy0 = oy >> 2, cy1 = (oy + ey - 1) >> 2;
+        const int ncx = cx1 - cx0 + 1, ncells = ncx * (cy1 - cy0 + 1);
+        int mnx = INT_MAX, mny = INT_MAX, mnz = INT_MAX, mxx = -1, mxy = -1, mxz = -1;
+        // in chunks of kCand cells: (1) collect the cells that may hold a
+        // visible voxel, (2) test their voxels, one per thread
+        for (int c0 = 0; c0 < ncells; c0 += kCand) {
+            if (threadIdx.x == 0) ncand = 0;
+            __syncthreads();
+            for (int c = c0 + threadIdx.x; c < min(ncells, c0 + kCand); c += blockDim.x) {
+                const int cx = cx0 + c % ncx, cy = cy0 + c / ncx;
+                const short2 cb = __ldg(v.cells + ((long long)cz * v.ncy + cy) * v.ncx + cx);
+                const int nv = count_visible(bits, prefix, cb.x, cb.y);
+                if (nv == (int)cb.y - (int)cb.x + 1) {
+                    // every value the cell can hold is visible: all its voxels
+                    // in the block are, no scan needed
+                    mnx = min(mnx, max(cx * 4, ox) - ox); mxx = max(mxx, min(cx * 4 + 3, ox + ex - 1) - ox);
+                    mny = min(mny, max(cy * 4, oy) - oy); mxy = max(mxy, min(cy * 4 + 3, oy + ey - 1) - oy);
+                    mnz = min(mnz, max(cz * 4, oz) - oz); mxz = max(mxz, min(cz * 4 + 3, oz + ez - 1) - oz);
+                } else if (nv > 0) {
+                    cand[atomicAdd(&ncand, 1)] = c;
                 }
             }
+            __syncthreads();
+            const int nvox = ncand * 64;
+            for (int e = threadIdx.x; e < nvox; e += blockDim.x) {
+                const int c = cand[e >> 6], w = e & 63;
+                const int x = (cx0 + c % ncx) * 4 + (w & 3) - ox;
+                const int y = (cy0 + c / ncx) * 4 + ((w >> 2) & 3) - oy;
+                const int z = cz * 4 + (w >> 4) - oz;
+                if (x < 0 || x >= ex || y < 0 || y >= ey || z < 0 || z >= ez) continue;
+                const unsigned int u = (unsigned int)(__ldg(vol + (long long)(oz + z) * L.pz +
+                                                            (long long)(oy + y) * L.py + ox + x) + 32768);
+                if ((bits[u >> 5] >> (u & 31)) & 1u) {
+                    mnx = min(mnx, x); mxx = max(mxx, x);
+                    mny = min(mny, y); mxy = max(mxy, y);
+                    mnz = min(mnz, z); mxz = max(mxz, z);
+                }
+            }
+            __syncthreads();  // cand / ncand reused
         }
-        mnx = warp_min(mnx); mny = warp_min(mny);
-        mxx = warp_max(mxx); mxy = warp_max(mxy);
+        mnx = warp_min(mnx); mny = warp_min(mny); mnz = warp_min(mnz);
+        mxx = warp_max(mxx); mxy = warp_max(mxy); mxz = warp_max(mxz);
         if (lane == 0 && mxx >= 0) {
             int *ab = v.aabb + 6 * b;
-            atomicMin(ab + 0, mnx); atomicMin(ab + 1, mny); atomicMin(ab + 2, z);
-            atomicMax(ab + 3, mxx); atomicMax(ab + 4, mxy); atomicMax(ab + 5, z);
+            atomicMin(ab + 0, mnx); atomicMin(ab + 1, mny); atomicMin(ab + 2, mnz);
+            atomicMax(ab + 3, mxx); atomicMax(ab + 4, mxy); atomicMax(ab + 5, mxz);
         }
     }
 }
@@ -745,7 +808,7 @@ cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs
     }
     visbits_kernel<<<2048 * 32 / kBlock, kBlock, 0, s>>>(v);
     vis_setup_kernel<<<1, kSetupThreads, smem, s>>>(v);
-    aabb_kernel<<<148 * 6, kBlock, 0, s>>>(vol, L, v, zsplit_for(L));
+    aabb_kernel<<<148 * 8, kAabbThreads, 0, s>>>(vol, L, v, zsplit_for(L));
     box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
     return cudaGetLastError();
 }

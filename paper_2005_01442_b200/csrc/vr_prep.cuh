@@ -33,6 +33,9 @@ struct VisArgs {
     unsigned long long *counters;  // [0] empty blocks, [1] non-empty blocks without a visible voxel
     int *uni;                // 6: union of the fitted global AABBs (lo xyz, hi xyz)
     int *list;               // nblocks + 1: [0] = count, then the non-empty block ids (any order)
+    int *visprefix;          // 2049: visible values in visbits words [0, w)
+    const short2 *cells;     // the volume's 4^3 cell bounds (cover every voxel value of the cell)
+    int ncx, ncy, ncz;
     double margin;
 };
 cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,
