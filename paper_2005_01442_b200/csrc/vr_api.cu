@@ -653,13 +653,18 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     if (a.blocks_hit) VR_CUDA(cudaMemsetAsync(a.blocks_hit, 0, nblocks, s));
     Scratch lut_range(s), heavy(s);
     if (a.mode == VR_MODE_DVR && a.classify == VR_CLS_POST && vol->cells) {
-        // [lut first/last visible bin][ray queue head][heavy pushed][heavy claimed]
-        VR_CUDA(lut_range.alloc(32));
+        // [lut first/last visible bin][ray queue head][heavy pushed][heavy claimed][heavy pushed, long queue]
+        VR_CUDA(lut_range.alloc(48));
         VR_CUDA(vr::launch_lut_range(lut, prm->nlut, (int *)lut_range.p, s));
         a.lut_range = (const int *)lut_range.p;
         a.work_counter = (unsigned long long *)((char *)lut_range.p + 8);
         a.heavy_count = a.work_counter + 1;
         a.heavy_head = a.work_counter + 2;
+        a.heavy_count_long = a.work_counter + 3;
+        // rays with >= 256 samples left are queued apart and taken first by
+        // the cooperative kernel (sweep 128..512: C3 +5 %, C2 +5 %)
+        const char *hl = getenv("VR_HEAVY_LONG");
+        a.heavy_long = hl ? atoll(hl) : 256;
         const long long items = (long long)a.slots * vr::kTileW * vr::kTileH;
         a.heavy_cap = items < (1LL << 20) ? items : (1LL << 20);
         // development knob: VR_HEAVY_MIN_LEFT (default 64, the best of a
@@ -677,7 +682,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         const char *hv = getenv("VR_HEAVY_VIS");
         a.heavy_vis = hv ? atoi(hv) : (prm->lighting && prm->term_alpha < 1.0 ? 4 : 1 << 30);
         if (a.heavy_min_left > 0) {
-            VR_CUDA(heavy.alloc((size_t)a.heavy_cap * vr::kHeavyRayBytes));
+            VR_CUDA(heavy.alloc(2 * (size_t)a.heavy_cap * vr::kHeavyRayBytes));  // short + long queue
             a.heavy = heavy.p;
         }
         a.cells = vol->cells;

@@ -862,7 +862,10 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
         // of ~700 samples while every other SM idles
         if (a.heavy && (drained || R.work > a.heavy_after || R.nvis >= a.heavy_vis) && R.work >= 0 && R.stage < 0 &&
             R.N - R.n >= a.heavy_min_left) {
-            const unsigned long long slot = atomicAdd(a.heavy_count, 1ull);
+            // long rays go to their own queue, which the cooperative kernel
+            // drains first (longest work first shortens its tail)
+            const bool lng = R.N - R.n >= a.heavy_long;
+            const unsigned long long slot = atomicAdd(lng ? a.heavy_count_long : a.heavy_count, 1ull);
             if (slot < (unsigned long long)a.heavy_cap) {
                 HeavyRay h;
                 h.item = R.item;
@@ -881,7 +884,7 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
                 h.d[2] = R.r.dz;
                 h.t0 = R.t0;
                 h.N = R.N;
-                static_cast<HeavyRay *>(a.heavy)[slot] = h;
+                static_cast<HeavyRay *>(a.heavy)[lng ? a.heavy_cap + slot : slot] = h;
                 R.live = false;
 #ifdef VR_DEBUG_STATS
                 dbg[4] += 1;
@@ -1109,8 +1112,10 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
     const int last_vis = a.cull ? __ldg(a.lut_range + 1) : 0;
     // a LUT whose first and last bins are visible can never prove a sample transparent
     const bool cull = a.cull != 0 && (first_vis > 0 || last_vis < a.nlut - 1);
-    unsigned long long pushed = *a.heavy_count;
-    const long long count = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
+    const unsigned long long pushed = *a.heavy_count, pushed_long = *a.heavy_count_long;
+    const long long n_short = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
+    const long long n_long = (long long)(pushed_long < (unsigned long long)a.heavy_cap ? pushed_long : a.heavy_cap);
+    const long long count = n_long + n_short;
     unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
 #ifdef VR_DEBUG_TIMES
     unsigned long long t_begin, n_rays = 0;
@@ -1127,7 +1132,9 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
         if (lane == 0) idx = atomicAdd(a.heavy_head, 1ull);
         idx = __shfl_sync(full, idx, 0);
         if ((long long)idx >= count) break;
-        const HeavyRay h = static_cast<const HeavyRay *>(a.heavy)[idx];
+        // the long queue (stored after the short one) first
+        const long long rec = (long long)idx < n_long ? a.heavy_cap + (long long)idx : (long long)idx - n_long;
+        const HeavyRay h = static_cast<const HeavyRay *>(a.heavy)[rec];
         PostRay R;
         {
             int cx, cy;
@@ -1369,7 +1376,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
         const long long w = 148 * 32 + (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
         a.debug_times[4 * w] = t_begin;
         a.debug_times[4 * w + 1] = t_end;
-        a.debug_times[4 * w + 2] = count;
+        a.debug_times[4 * w + 2] = count;  // rays handed over
         a.debug_times[4 * w + 3] = n_rays;
     }
 #endif
@@ -1454,7 +1461,7 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
         long long ctas = (long long)sms * (per_sm > 0 ? per_sm : 1);
         if (ctas > a.slots) ctas = a.slots;
-        cudaError_t e = cudaMemsetAsync(a.work_counter, 0, 3 * sizeof(unsigned long long), stream);
+        cudaError_t e = cudaMemsetAsync(a.work_counter, 0, 4 * sizeof(unsigned long long), stream);
         if (e != cudaSuccess) return e;
         k<<<(unsigned)ctas, kThreads, 0, stream>>>(a);
         if (a.heavy) {

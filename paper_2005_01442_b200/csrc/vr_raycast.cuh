@@ -61,6 +61,8 @@ struct RenderArgs {
     void *heavy;
     unsigned long long *heavy_count;  // records pushed (zeroed per launch)
     unsigned long long *heavy_head;   // records claimed by the cooperative kernel
+    unsigned long long *heavy_count_long;  // records pushed to the long-ray queue (stored after the short one)
+    long long heavy_long;      // rays with at least this many samples left use the long queue
     long long heavy_cap;
     long long heavy_min_left;  // tail rays with at least this many samples left are handed over
     int heavy_after;           // ... and, before the queue drains, rays that took more steps than this
