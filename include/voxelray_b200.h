@@ -105,15 +105,16 @@ typedef struct {
     int64_t *taken;      /* per-pixel samples taken */
     int64_t *skipped;    /* per-pixel samples skipped */
     uint8_t *blocks_hit; /* grid block count (1 when monolithic) */
-    uint64_t *totals;    /* [5]: samples_taken, samples_skipped (accumulated: zero
-                            them first, or use vr_render_to_host which does),
+    uint64_t *totals;    /* [5]: samples_taken, samples_skipped,
                             blocks_visited, blocks_empty, and the number of
                             non-empty blocks without a visible voxel (the
                             reference raises EmptyBlock for those,
                             blocks.py:186-187) -- the last three written, and
                             blocks_visited only when blocks_hit is given */
-    uint64_t *work;      /* [3] optional, accumulated: gradient evaluations (shaded samples),
-                            interpolated samples (taken minus culled), march-loop iterations */
+    uint64_t *work;      /* [3] optional: gradient evaluations (shaded samples),
+                            interpolated samples (taken minus culled), march-loop iterations.
+                            totals, work and blocks_hit are zeroed by the call itself
+                            (in its first kernel) */
     void *ev_start;      /* optional cudaEvent_t recorded just before the ray-cast kernel */
     void *ev_stop;       /* optional cudaEvent_t recorded just after it */
 } vr_render_outputs;

@@ -650,14 +650,30 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     a.totals = (unsigned long long *)out->totals;
     a.work = (unsigned long long *)out->work;
     int nblocks = grid ? grid->nblocks : 1;
-    if (a.blocks_hit) VR_CUDA(cudaMemsetAsync(a.blocks_hit, 0, nblocks, s));
+    // per-frame zeroing (totals, work, blocks_hit, the ray queues' counters)
+    // is done by the frame's first kernel rather than by memset launches
+    vr::ZeroSpec zero{};
+    if (a.totals) {
+        zero.p[1] = a.totals;
+        zero.n[1] = 5;
+    }
+    if (a.work) {
+        zero.p[2] = a.work;
+        zero.n[2] = 3;
+    }
+    if (a.blocks_hit) {
+        zero.b = a.blocks_hit;
+        zero.nb = nblocks;
+    }
+    const bool post = a.mode == VR_MODE_DVR && a.classify == VR_CLS_POST && vol->cells;
     Scratch lut_range(s), heavy(s);
-    if (a.mode == VR_MODE_DVR && a.classify == VR_CLS_POST && vol->cells) {
+    if (post) {
         // [lut first/last visible bin][ray queue head][heavy pushed][heavy claimed][heavy pushed, long queue]
         VR_CUDA(lut_range.alloc(48));
-        VR_CUDA(vr::launch_lut_range(lut, prm->nlut, (int *)lut_range.p, s));
         a.lut_range = (const int *)lut_range.p;
         a.work_counter = (unsigned long long *)((char *)lut_range.p + 8);
+        zero.p[0] = a.work_counter;
+        zero.n[0] = 4;
         a.heavy_count = a.work_counter + 1;
         a.heavy_head = a.work_counter + 2;
         a.heavy_count_long = a.work_counter + 3;
@@ -700,12 +716,20 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     VisScratch vs(s);
     if (grid) {
         VR_CUDA(vs.init(grid, lut, prm->nlut, prm->lut_lo, prm->lut_hi, prm->margin, false));
+        vs.v.zero = zero;
+        vs.v.lut_range = post ? (int *)lut_range.p : nullptr;
         VR_CUDA(vr::launch_visibility(vol->data, grid->L, vs.v, s));
         a.empty = vs.v.empty;
         a.box = vs.v.box;
         a.vmin = grid->vmin;
         a.vmax = grid->vmax;
         a.uni = vs.v.uni;
+    } else if (post) {
+        VR_CUDA(vr::launch_lut_range(lut, prm->nlut, (int *)lut_range.p, zero, s));
+    } else {
+        for (int k = 1; k < 3; ++k)
+            if (zero.n[k]) VR_CUDA(cudaMemsetAsync(zero.p[k], 0, sizeof(unsigned long long) * zero.n[k], s));
+        if (zero.nb) VR_CUDA(cudaMemsetAsync(zero.b, 0, zero.nb, s));
     }
 #ifdef VR_DEBUG_TIMES
     a.debug_times = g_debug_times;
@@ -714,13 +738,12 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     VR_CUDA(vr::launch_raycast(a, s));
     if (out->ev_stop) VR_CUDA(cudaEventRecord((cudaEvent_t)out->ev_stop, s));
     if (out->totals) {
-        if (a.blocks_hit) VR_CUDA(vr::launch_count_hits(a.blocks_hit, nblocks, a.totals + 2, s));
-        if (grid) {
-            VR_CUDA(cudaMemcpyAsync(a.totals + 3, vs.v.counters, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-            VR_CUDA(cudaMemcpyAsync(a.totals + 4, vs.v.counters + 1, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
-        } else {
-            VR_CUDA(cudaMemsetAsync(a.totals + 3, 0, 2 * sizeof(unsigned long long), s));
-        }
+        // totals[2] = blocks_visited; totals[3..4] = the visibility counters (zero without a grid)
+        if (a.blocks_hit)
+            VR_CUDA(vr::launch_count_hits(a.blocks_hit, nblocks, a.totals + 2, grid ? vs.v.counters : nullptr, s));
+        else if (grid)
+            VR_CUDA(cudaMemcpyAsync(a.totals + 3, vs.v.counters, 2 * sizeof(unsigned long long),
+                                    cudaMemcpyDeviceToDevice, s));
     }
     return VR_OK;
 }
@@ -756,7 +779,6 @@ int vr_render_to_host(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
     char *base = (char *)mem.p;
     VR_CUDA(cudaMemcpyAsync(base + o_lut, lut_host, lut_b, cudaMemcpyHostToDevice, s));
     if (tbl_b) VR_CUDA(cudaMemcpyAsync(base + o_tbl, table_host, tbl_b, cudaMemcpyHostToDevice, s));
-    VR_CUDA(cudaMemsetAsync(base + o_tot, 0, 8 * 8, s));
     Scratch rgba(s);
     if (classify == VR_CLS_PRE) {
         long long nvox = vol->nx * vol->ny * vol->nz;

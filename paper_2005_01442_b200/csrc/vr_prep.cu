@@ -203,6 +203,12 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
     __shared__ unsigned int n_empty;
     __shared__ int n_list;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    zero_fill(v.zero);
+    __shared__ int first_vis, last_vis;
+    if (tid == 0) {
+        first_vis = v.nbins;
+        last_vis = -1;
+    }
     // exclusive prefix over the bins with nonzero opacity
     // (ClassifiedLUT.opacity_prefix, transfer.py:131-133): block-wide scan
     const int per = (v.nbins + kSetupThreads - 1) / kSetupThreads;
@@ -235,7 +241,12 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
     int run = warp_tot[wid] + incl - s;
     for (int i = b0; i < b1; ++i) {
         prefix[i] = run;
-        run += (__ldg(v.lut + 4 * i + 3) > 0.0) ? 1 : 0;
+        const int vis = (__ldg(v.lut + 4 * i + 3) > 0.0) ? 1 : 0;
+        run += vis;
+        if (vis && v.lut_range) {
+            atomicMin(&first_vis, i);
+            atomicMax(&last_vis, i);
+        }
     }
     if (b1 == v.nbins && b0 < b1) prefix[v.nbins] = run;
     __syncthreads();
@@ -287,6 +298,10 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
         v.counters[0] = n_empty;
         v.counters[1] = 0;
         v.list[0] = n_list;
+        if (v.lut_range) {
+            v.lut_range[0] = first_vis;
+            v.lut_range[1] = last_vis;
+        }
     }
     if (tid < 6) v.uni[tid] = tid < 3 ? INT_MAX : INT_MIN;
 }
@@ -546,8 +561,9 @@ __global__ void __launch_bounds__(kBlock) cell_from_cubes_kernel(const short2 *_
     }
 }
 
-__global__ void lut_range_kernel(const double *lut, int nbins, int *range) {
+__global__ void lut_range_kernel(const double *lut, int nbins, int *range, const ZeroSpec zero) {
     __shared__ int first, last;
+    zero_fill(zero);
     if (threadIdx.x == 0) {
         first = nbins;
         last = -1;
@@ -566,7 +582,9 @@ __global__ void lut_range_kernel(const double *lut, int nbins, int *range) {
     }
 }
 
-__global__ void count_hits_kernel(const uint8_t *hits, int n, unsigned long long *out) {
+__global__ void count_hits_kernel(const uint8_t *hits, int n, unsigned long long *out,
+                                  const unsigned long long *vis_counters) {
+    if (vis_counters && threadIdx.x < 2) out[1 + threadIdx.x] = vis_counters[threadIdx.x];
     unsigned long long c = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) c += hits[i] ? 1 : 0;
     c = warp_sum(c);
@@ -853,13 +871,14 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_lut_range(const double *lut, int nbins, int *range, cudaStream_t s) {
-    lut_range_kernel<<<1, 1024, 0, s>>>(lut, nbins, range);
+cudaError_t launch_lut_range(const double *lut, int nbins, int *range, const ZeroSpec &zero, cudaStream_t s) {
+    lut_range_kernel<<<1, 1024, 0, s>>>(lut, nbins, range, zero);
     return cudaGetLastError();
 }
 
-cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out, cudaStream_t s) {
-    count_hits_kernel<<<1, 1024, 0, s>>>(hits, n, out);
+cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out,
+                              const unsigned long long *vis_counters, cudaStream_t s) {
+    count_hits_kernel<<<1, 1024, 0, s>>>(hits, n, out, vis_counters);
     return cudaGetLastError();
 }
 

@@ -17,6 +17,21 @@ cudaError_t launch_phantom(int kind, int nx, int ny, int nz, int16_t *out, cudaS
 cudaError_t launch_block_minmax(const int16_t *vol, const Layout &L, int *vmin, int *vmax,
                                 cudaStream_t s);
 
+// Per-frame zeroing folded into the first kernel of a frame (instead of a
+// memset launch each): up to three u64 ranges and one byte range.
+struct ZeroSpec {
+    unsigned long long *p[3];
+    int n[3];
+    uint8_t *b;
+    int nb;
+};
+
+VR_D void zero_fill(const ZeroSpec &z) {
+    for (int k = 0; k < 3; ++k)
+        for (int i = threadIdx.x; i < z.n[k]; i += blockDim.x) z.p[k][i] = 0ull;
+    for (int i = threadIdx.x; i < z.nb; i += blockDim.x) z.b[i] = 0;
+}
+
 // Visibility state for one LUT (blocks.py:161-220).
 struct VisArgs {
     const double *lut;  // (nbins, 4)
@@ -37,6 +52,8 @@ struct VisArgs {
     const short2 *cells;     // the volume's 4^3 cell bounds (cover every voxel value of the cell)
     int ncx, ncy, ncz;
     double margin;
+    int *lut_range;          // optional out: first / last LUT bin with nonzero opacity (as launch_lut_range)
+    ZeroSpec zero;           // zeroed by the setup kernel (frame counters, totals, blocks_hit)
 };
 cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,
                               cudaStream_t s);
@@ -61,10 +78,13 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
 
 // range[0] = first LUT bin with nonzero opacity (nbins if none),
 // range[1] = last such bin (-1 if none)
-cudaError_t launch_lut_range(const double *lut, int nbins, int *range, cudaStream_t s);
+cudaError_t launch_lut_range(const double *lut, int nbins, int *range, const ZeroSpec &zero, cudaStream_t s);
 
 // blocks_visited = sum(blocks_hit) -> *out (render.py:467)
-cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out, cudaStream_t s);
+// also copies the two visibility counters (blocks_empty, empty-block errors)
+// to out[1..2] when vis_counters is given
+cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out,
+                              const unsigned long long *vis_counters, cudaStream_t s);
 
 // preclassify_volume (transfer.py:142-145): 4 planar uint8 channels
 cudaError_t launch_preclassify(const int16_t *vol, long long n, const double *lut, int nbins,

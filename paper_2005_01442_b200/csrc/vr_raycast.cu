@@ -1461,8 +1461,7 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
         long long ctas = (long long)sms * (per_sm > 0 ? per_sm : 1);
         if (ctas > a.slots) ctas = a.slots;
-        cudaError_t e = cudaMemsetAsync(a.work_counter, 0, 4 * sizeof(unsigned long long), stream);
-        if (e != cudaSuccess) return e;
+        // (the queue counters were zeroed by the frame's setup kernel)
         k<<<(unsigned)ctas, kThreads, 0, stream>>>(a);
         if (a.heavy) {
             KernelFn h = pick_cooperative(a);

@@ -542,9 +542,7 @@ class Renderer:
         """Enqueue one frame on ``stream`` (default: torch's current stream)."""
         torch = self.torch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
-        self.totals[0:2].zero_()
-        self.totals[5:8].zero_()
-        out = self.outputs()
+        out = self.outputs()  # (totals / work / blocks_hit are zeroed by vr_render itself)
         _lib.check(_lib.load().vr_render(
             self.dvol.handle, self.dgrid.handle if self.dgrid else None, ctypes.byref(self.cam),
             ctypes.byref(self.res.params), _lib.ptr(self.lut), _lib.ptr(self.table), _lib.ptr(self.rgba),
