@@ -668,10 +668,10 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     const bool post = a.mode == VR_MODE_DVR && a.classify == VR_CLS_POST && vol->cells;
     Scratch lut_range(s), heavy(s);
     if (post) {
-        // [lut first/last visible bin][ray queue head][heavy pushed][heavy claimed][heavy pushed, long queue]
+        // [lut first/last visible bin, value thresholds][ray queue head][heavy pushed][heavy claimed][heavy long]
         VR_CUDA(lut_range.alloc(48));
         a.lut_range = (const int *)lut_range.p;
-        a.work_counter = (unsigned long long *)((char *)lut_range.p + 8);
+        a.work_counter = (unsigned long long *)((char *)lut_range.p + 16);
         zero.p[0] = a.work_counter;
         zero.n[0] = 4;
         a.heavy_count = a.work_counter + 1;
@@ -718,6 +718,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         VR_CUDA(vs.init(grid, lut, prm->nlut, prm->lut_lo, prm->lut_hi, prm->margin, false));
         vs.v.zero = zero;
         vs.v.lut_range = post ? (int *)lut_range.p : nullptr;
+        vs.v.lut_inv_w = a.lut_inv_w;
         VR_CUDA(vr::launch_visibility(vol->data, grid->L, vs.v, s));
         a.empty = vs.v.empty;
         a.box = vs.v.box;
@@ -725,7 +726,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.vmax = grid->vmax;
         a.uni = vs.v.uni;
     } else if (post) {
-        VR_CUDA(vr::launch_lut_range(lut, prm->nlut, (int *)lut_range.p, zero, s));
+        VR_CUDA(vr::launch_lut_range(lut, prm->nlut, prm->lut_lo, a.lut_inv_w, (int *)lut_range.p, zero, s));
     } else {
         for (int k = 1; k < 3; ++k)
             if (zero.n[k]) VR_CUDA(cudaMemsetAsync(zero.p[k], 0, sizeof(unsigned long long) * zero.n[k], s));

@@ -7,6 +7,7 @@
 // carry no FMA contraction.  Division and sqrt are IEEE correctly rounded on
 // the device (nvcc default -prec-div=true -prec-sqrt=true for double).
 #pragma once
+#include <climits>
 
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -80,6 +81,42 @@ VR_D int owner_block(double x, double stride, double inv_stride, int nb) {
     if (f < 0.0) return 0;
     if (f > (double)(nb - 1)) return nb - 1;
     return (int)f;
+}
+
+// _kernels.py:190-192 _lut_bin
+VR_D int lut_bin(double s, double lo, double inv_w, int nbins) {
+    double q = (s - lo) * inv_w;
+    // int() truncates toward zero; clamp in the float domain to stay in range
+    if (q <= -1.0) return 0;
+    if (q >= (double)nbins) return nbins - 1;
+    return clampi((int)q, 0, nbins - 1);
+}
+
+// Integer value thresholds of the LUT's visible bin range: every integer s
+// with s < vlo has lut_bin(s) < first_vis and every s > vhi has lut_bin(s) >
+// last_vis (lut_bin is monotone), so an integer bound can be tested without
+// floating point.  vlo = INT_MAX / vhi = INT_MIN when no bin is visible.
+VR_D void visible_value_range(double lo, double inv_w, int nbins, int first_vis, int last_vis, int &vlo,
+                              int &vhi) {
+    const int L = -(1 << 24), R = 1 << 24;
+    if (first_vis >= nbins || last_vis < 0) {
+        vlo = INT_MAX;
+        vhi = INT_MIN;
+        return;
+    }
+    int a = L, b = R;  // smallest s in [L, R] with lut_bin(s) >= first_vis (R when none... bin(R) = nbins-1)
+    while (a < b) {
+        const int m = a + (b - a) / 2;
+        if (lut_bin((double)m, lo, inv_w, nbins) >= first_vis) b = m; else a = m + 1;
+    }
+    vlo = a;
+    a = L;
+    b = R;  // largest s with lut_bin(s) <= last_vis
+    while (a < b) {
+        const int m = a + (b - a + 1) / 2;
+        if (lut_bin((double)m, lo, inv_w, nbins) <= last_vis) a = m; else b = m - 1;
+    }
+    vhi = a;
 }
 
 // ----------------------------------------------------------- Catmull-Rom

@@ -301,6 +301,8 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
         if (v.lut_range) {
             v.lut_range[0] = first_vis;
             v.lut_range[1] = last_vis;
+            visible_value_range(v.lut_lo, v.lut_inv_w, v.nbins, first_vis, last_vis, v.lut_range[2],
+                                v.lut_range[3]);
         }
     }
     if (tid < 6) v.uni[tid] = tid < 3 ? INT_MAX : INT_MIN;
@@ -561,7 +563,8 @@ __global__ void __launch_bounds__(kBlock) cell_from_cubes_kernel(const short2 *_
     }
 }
 
-__global__ void lut_range_kernel(const double *lut, int nbins, int *range, const ZeroSpec zero) {
+__global__ void lut_range_kernel(const double *lut, int nbins, double lut_lo, double lut_inv_w, int *range,
+                                 const ZeroSpec zero) {
     __shared__ int first, last;
     zero_fill(zero);
     if (threadIdx.x == 0) {
@@ -579,6 +582,7 @@ __global__ void lut_range_kernel(const double *lut, int nbins, int *range, const
     if (threadIdx.x == 0) {
         range[0] = first;
         range[1] = last;
+        visible_value_range(lut_lo, lut_inv_w, nbins, first, last, range[2], range[3]);
     }
 }
 
@@ -871,8 +875,9 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
     return cudaGetLastError();
 }
 
-cudaError_t launch_lut_range(const double *lut, int nbins, int *range, const ZeroSpec &zero, cudaStream_t s) {
-    lut_range_kernel<<<1, 1024, 0, s>>>(lut, nbins, range, zero);
+cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double lut_inv_w, int *range,
+                             const ZeroSpec &zero, cudaStream_t s) {
+    lut_range_kernel<<<1, 1024, 0, s>>>(lut, nbins, lut_lo, lut_inv_w, range, zero);
     return cudaGetLastError();
 }
 

@@ -52,7 +52,8 @@ struct VisArgs {
     const short2 *cells;     // the volume's 4^3 cell bounds (cover every voxel value of the cell)
     int ncx, ncy, ncz;
     double margin;
-    int *lut_range;          // optional out: first / last LUT bin with nonzero opacity (as launch_lut_range)
+    int *lut_range;          // optional out (4 ints): as launch_lut_range
+    double lut_inv_w;        // the march's bin scale nbins / (hi - lo) (render.py:423)
     ZeroSpec zero;           // zeroed by the setup kernel (frame counters, totals, blocks_hit)
 };
 cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,
@@ -78,7 +79,10 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
 
 // range[0] = first LUT bin with nonzero opacity (nbins if none),
 // range[1] = last such bin (-1 if none)
-cudaError_t launch_lut_range(const double *lut, int nbins, int *range, const ZeroSpec &zero, cudaStream_t s);
+// range[0..1] as above, range[2..3] = the integer value thresholds of that bin range
+// under the march's bin formula (visible_value_range, lut_inv_w = nbins / (hi - lo))
+cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double lut_inv_w, int *range,
+                             const ZeroSpec &zero, cudaStream_t s);
 
 // blocks_visited = sum(blocks_hit) -> *out (render.py:467)
 // also copies the two visibility counters (blocks_empty, empty-block errors)

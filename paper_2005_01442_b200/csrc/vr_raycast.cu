@@ -153,13 +153,6 @@ VR_D double attr_rgba(const RenderArgs &a, int bi, int bj, int bk, double x, dou
 }
 
 // _kernels.py:190-192
-VR_D int lut_bin(double s, double lo, double inv_w, int nbins) {
-    double q = (s - lo) * inv_w;
-    // int() truncates toward zero; clamp in the float domain to stay in range
-    if (q <= -1.0) return 0;
-    if (q >= (double)nbins) return nbins - 1;
-    return clampi((int)q, 0, nbins - 1);
-}
 
 // _kernels.py:195-208
 VR_D void shade(const RenderArgs &a, double &r, double &g, double &b, double nx, double ny, double nz,
@@ -209,28 +202,28 @@ VR_D bool dvr_skippable(const BlockRec &r, double x, double y, double z) {
 // int16 limit is saturated and proves nothing on that side.  Before the cell,
 // the 16^3 macro cell (union of 64 cells) is tried: 3 = transparent there,
 // culled_run may leap to the macro-cell exit.
-VR_D bool bounds_transparent(const RenderArgs &a, short2 b, int first_vis, int last_vis) {
-    const double up = b.y >= 32767 ? 1e9 : (double)b.y;
-    const double dn = b.x <= -32768 ? -1e9 : (double)b.x;
-    return lut_bin(up, a.lut_lo, a.lut_inv_w, a.nlut) < first_vis ||
-           lut_bin(dn, a.lut_lo, a.lut_inv_w, a.nlut) > last_vis;
+VR_D bool bounds_transparent(short2 b, int vlo, int vhi) {
+    // integer thresholds of the visible bins (visible_value_range); a bound at
+    // the int16 limit is saturated: unbounded on that side
+    const int up = b.y >= 32767 ? INT_MAX : (int)b.y;
+    const int dn = b.x <= -32768 ? INT_MIN : (int)b.x;
+    return up < vlo || dn > vhi;
 }
 
 template <bool CUBIC>
-VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z, int first_vis, int last_vis) {
+VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z, int vlo, int vhi) {
     const int gx = (int)clampf(x, 0.0, (double)(a.L.n[0] - 1));
     const int gy = (int)clampf(y, 0.0, (double)(a.L.n[1] - 1));
     const int gz = (int)clampf(z, 0.0, (double)(a.L.n[2] - 1));
-    if (a.mcells && bounds_transparent(a, __ldg(a.mcells + ((long long)(gz >> 4) * a.nmy + (gy >> 4)) * a.nmx + (gx >> 4)),
-                                       first_vis, last_vis))
+    if (a.mcells &&
+        bounds_transparent(__ldg(a.mcells + ((long long)(gz >> 4) * a.nmy + (gy >> 4)) * a.nmx + (gx >> 4)), vlo, vhi))
         return 3;
-    if (bounds_transparent(a, __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2)),
-                           first_vis, last_vis))
+    if (bounds_transparent(__ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2)), vlo, vhi))
         return 1;
     if (!a.win) return 0;
     const short2 w = __ldg(a.win + (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
                            ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3));
-    return bounds_transparent(a, w, first_vis, last_vis) ? 2 : 0;
+    return bounds_transparent(w, vlo, vhi) ? 2 : 0;
 }
 
 // Parameter interval in which the (exact) ray lies inside the box [lo, hi]
@@ -391,11 +384,11 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
         double prev_s = 0.0;
         bool prev_valid = false, prev_skippable = false;
         int last_hit = -1;
-        int first_vis = 0, last_vis = 0;
+        int first_vis = INT_MIN, last_vis = INT_MAX;  // value thresholds (vlo, vhi)
         const bool cull = KIND == kPost && a.cull;
         if (cull) {
-            first_vis = __ldg(a.lut_range);
-            last_vis = __ldg(a.lut_range + 1);
+            first_vis = __ldg(a.lut_range + 2);
+            last_vis = __ldg(a.lut_range + 3);
         }
         long long n = 0;
         while (n < N) {
@@ -813,10 +806,10 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
     const unsigned full = 0xffffffffu;
     const long long total = (long long)a.slots * (kTileW * kTileH);
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
-    const int first_vis = a.cull ? __ldg(a.lut_range) : 0;
-    const int last_vis = a.cull ? __ldg(a.lut_range + 1) : 0;
+    const int first_vis = a.cull ? __ldg(a.lut_range + 2) : INT_MIN;  // value thresholds (vlo, vhi)
+    const int last_vis = a.cull ? __ldg(a.lut_range + 3) : INT_MAX;
     // a LUT whose first and last bins are visible can never prove a sample transparent
-    const bool cull = a.cull != 0 && (first_vis > 0 || last_vis < a.nlut - 1);
+    const bool cull = a.cull != 0 && (first_vis > -32768 || last_vis < 32767);
     unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
     PostRay R;
     R.live = false;
@@ -1108,10 +1101,10 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
-    const int first_vis = a.cull ? __ldg(a.lut_range) : 0;
-    const int last_vis = a.cull ? __ldg(a.lut_range + 1) : 0;
+    const int first_vis = a.cull ? __ldg(a.lut_range + 2) : INT_MIN;  // value thresholds (vlo, vhi)
+    const int last_vis = a.cull ? __ldg(a.lut_range + 3) : INT_MAX;
     // a LUT whose first and last bins are visible can never prove a sample transparent
-    const bool cull = a.cull != 0 && (first_vis > 0 || last_vis < a.nlut - 1);
+    const bool cull = a.cull != 0 && (first_vis > -32768 || last_vis < 32767);
     const unsigned long long pushed = *a.heavy_count, pushed_long = *a.heavy_count_long;
     const long long n_short = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
     const long long n_long = (long long)(pushed_long < (unsigned long long)a.heavy_cap ? pushed_long : a.heavy_cap);
