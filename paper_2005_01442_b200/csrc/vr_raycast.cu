@@ -212,9 +212,10 @@ VR_D bool bounds_transparent(short2 b, int vlo, int vhi) {
 
 template <bool CUBIC>
 VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z, int vlo, int vhi) {
-    const int gx = (int)clampf(x, 0.0, (double)(a.L.n[0] - 1));
-    const int gy = (int)clampf(y, 0.0, (double)(a.L.n[1] - 1));
-    const int gz = (int)clampf(z, 0.0, (double)(a.L.n[2] - 1));
+    // == (int)clamp(v, 0, n-1): truncation then an integer clamp (|v| << 2^31)
+    const int gx = clampi((int)x, 0, a.L.n[0] - 1);
+    const int gy = clampi((int)y, 0, a.L.n[1] - 1);
+    const int gz = clampi((int)z, 0, a.L.n[2] - 1);
     if (a.mcells &&
         bounds_transparent(__ldg(a.mcells + ((long long)(gz >> 4) * a.nmy + (gy >> 4)) * a.nmx + (gx >> 4)), vlo, vhi))
         return 3;
@@ -325,7 +326,7 @@ VR_D long long culled_run(const RenderArgs &a, const Ray &r, const double inv[3]
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         if (d[k] == 0.0) continue;
-        const int g = (int)clampf(p[k], 0.0, (double)(a.L.n[k] - 1));
+        const int g = clampi((int)p[k], 0, a.L.n[k] - 1);  // == (int)clamp(p, 0, n-1)
         const int c = g >> shift, clast = (a.L.n[k] - 1) >> shift;
         const double size = (double)(1 << shift);
         if (d[k] > 0.0 && c < clast) t_safe = dmin(t_safe, ((size * (c + 1) - delta) * s[k] - o[k]) * inv[k]);
