@@ -290,12 +290,13 @@ def run_reference(args):
 
 def launches_per_frame(settings):
     """Kernels of ours in one frame (vr_render): TF visibility (4 on the block
-    path: value bits, block intervals, AABB fit, boxes), LUT opacity range +
-    per-lane ray caster + cooperative ray caster (post-classified), or the
-    one-thread-per-ray kernel, and the blocks_visited count."""
+    path: value bits, block intervals + LUT range + frame zeroing, AABB fit,
+    boxes), the LUT range kernel on the monolithic post path, the per-lane
+    and cooperative ray casters (post-classified) or the one-thread-per-ray
+    kernel, and the blocks_visited count."""
     post = settings.mode == "dvr" and settings.classification == "post"
-    n = 4 if settings.use_blocks else 0
-    n += 3 if post else 1
+    n = 4 if settings.use_blocks else (1 if post else 0)
+    n += 2 if post else 1
     return n + 1
 
 
