@@ -198,7 +198,8 @@ VR_D bool dvr_skippable(const BlockRec &r, double x, double y, double z) {
 // range of the trilinear / Catmull-Rom interpolant under any block-local tap
 // clamping, and per 4^3 cell the union of its cubes' ranges.  Returns 0 (not
 // provable), 1 (the whole cell is transparent: culled_run may leap to the
-// cell exit) or 2 (this sample's cube is: this sample only).  A bound at the
+// cell exit) or 2 (this sample's unit cube is: a leap to the cube's exit, the
+// cube bound covering every sample based in it).  A bound at the
 // int16 limit is saturated and proves nothing on that side.  Before the cell,
 // the 16^3 macro cell (union of 64 cells) is tried: 3 = transparent there,
 // culled_run may leap to the macro-cell exit.
@@ -511,7 +512,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 if (pt) {
                     const double p[3] = {x, y, z};
                     const int bidx[3] = {bi, bj, bk};
-                    long long k = pt != 2 ? culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, rec, pt == 3 ? 4 : 2) : 1;
+                    long long k = culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, rec, pt == 3 ? 4 : pt == 1 ? 2 : 0);
                     if (k > N - n) k = N - n;
                     n_taken += k - 1;
                     n += k;
@@ -923,7 +924,7 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
             const int pt = cull ? provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis) : 0;
             if (pt) {
                 long long k =
-                    pt != 2 ? culled_run<SKIP>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec, pt == 3 ? 4 : 2) : 1;
+                    culled_run<SKIP>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec, pt == 3 ? 4 : pt == 1 ? 2 : 0);
                 if (k > R.N - n) k = R.N - n;
                 R.taken += k;
                 R.n = n + k;
@@ -1153,7 +1154,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
             const long long m = n + lane;
             const bool valid = m < R.N;
             bool skippable = false, cell_only = true, cand = false;
-            int run_shift = 0;  // culled run leapable to the exit of a 2^run_shift cell (0: none)
+            int run_shift = -1;  // culled run leapable to the exit of a 2^run_shift cell (-1: none)
             double x = 0.0, y = 0.0, z = 0.0, t = 0.0;
             int bi = 0, bj = 0, bk = 0, b = 0;
             BlockRec rec = {};
@@ -1174,7 +1175,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                 if (!skippable) {
                     const int pt = cull ? provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis) : 0;
                     cand = pt == 0;
-                    run_shift = pt == 3 ? 4 : pt == 1 ? 2 : 0;
+                    run_shift = pt == 3 ? 4 : pt == 1 ? 2 : pt == 2 ? 0 : -1;
                 }
             }
             // Evaluate the chunk.  Round 0 interpolates every candidate sample
@@ -1325,7 +1326,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                     const double p[3] = {x, y, z};
                     const int bidx[3] = {bi, bj, bk};
                     k = skippable ? leap_count<kPost>(a, R.r, R.inv, R.t0, m, t, p, bidx, rec, cell_only)
-                        : run_shift ? culled_run<SKIP>(a, R.r, R.inv, R.t0, m, t, p, bidx, rec, run_shift)
+                        : run_shift >= 0 ? culled_run<SKIP>(a, R.r, R.inv, R.t0, m, t, p, bidx, rec, run_shift)
                                    : 1;
                 }
                 k = __shfl_sync(full, k, 31);
