@@ -695,6 +695,8 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         // sample (C3-soft 94 -> 145 fps; C1/C2/C3 unchanged, sweep 2..32).
         // Without, its in-order composite of a fully visible chunk is serial
         // and the per-lane kernel is faster (C3-stress 21 vs 12 fps).
+        const char *hva = getenv("VR_HEAVY_VIS_ALPHA");
+        a.heavy_vis_alpha = hva ? atof(hva) : 0.5;
         const char *hv = getenv("VR_HEAVY_VIS");
         a.heavy_vis = hv ? atoi(hv) : (prm->lighting && prm->term_alpha < 1.0 ? 4 : 1 << 30);
         if (a.heavy_min_left > 0) {

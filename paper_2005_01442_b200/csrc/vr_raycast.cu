@@ -855,7 +855,8 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
         // warp-cooperative kernel (at a clean point, nothing pending): the
         // frame would otherwise end with a few warps finishing grazing rays
         // of ~700 samples while every other SM idles
-        if (a.heavy && (drained || R.work > a.heavy_after || R.nvis >= a.heavy_vis) && R.work >= 0 && R.stage < 0 &&
+        if (a.heavy && (drained || R.work > a.heavy_after || (R.nvis >= a.heavy_vis && R.acc_a < a.heavy_vis_alpha)) &&
+            R.work >= 0 && R.stage < 0 &&
             R.N - R.n >= a.heavy_min_left) {
             // long rays go to their own queue, which the cooperative kernel
             // drains first (longest work first shortens its tail)

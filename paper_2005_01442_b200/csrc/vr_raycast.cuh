@@ -67,6 +67,7 @@ struct RenderArgs {
     long long heavy_min_left;  // tail rays with at least this many samples left are handed over
     int heavy_after;           // ... and, before the queue drains, rays that took more steps than this
     int heavy_vis;             // ... or composited at least this many samples (dense rays)
+    double heavy_vis_alpha;    // ... while still below this opacity (far from termination)
 
     // outputs (all optional)
     uint8_t *pixels;
