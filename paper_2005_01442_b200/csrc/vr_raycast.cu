@@ -1190,6 +1190,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
             double sr = 0.0, sg = 0.0, sb = 0.0, ahat = 0.0;
             double tp[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
             bool contrib = false;
+            double wself = 0.0;  // compositing weight of this lane's sample
             unsigned vis = 0u;  // visible lanes up to the terminating sample
             int ntaps = 0, rank = 0, et_lane = 32;
             const bool any_cand = __any_sync(full, cand);
@@ -1243,6 +1244,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                         const int src = __ffs(cm) - 1;
                         cm &= cm - 1;
                         const double w = (1.0 - A) * __shfl_sync(full, ahat, src);
+                        if (lane == src) wself = w;  // this sample's weight, reused by the composite
                         A += w;
                         if (A >= a.term_alpha) {
                             et_lane = src;
@@ -1281,8 +1283,10 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
                     const int src = __ffs(cm) - 1;
                     cm &= cm - 1;
                     const double r_ = __shfl_sync(full, sr, src), g_ = __shfl_sync(full, sg, src);
-                    const double b_ = __shfl_sync(full, sb, src), ah = __shfl_sync(full, ahat, src);
-                    const double w = (1.0 - acc_a) * ah;
+                    const double b_ = __shfl_sync(full, sb, src);
+                    // == (1 - acc_a) * ahat: the same operations on the same
+                    // values as in the termination scan above
+                    const double w = __shfl_sync(full, wself, src);
                     acc_r += w * r_;
                     acc_g += w * g_;
                     acc_b += w * b_;
