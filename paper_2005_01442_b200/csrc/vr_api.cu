@@ -25,7 +25,7 @@ struct vr_volume {
     int ncx, ncy, ncz;
     int16_t *bricks;  // K1: the voxels in 4^3 bricks (what the ray caster reads)
     int bnx, bny, bnz;
-    short2 *win;      // per unit cube: bounds of the interpolant (vr_prep.cuh launch_interp_bounds), brick order
+    short2 *cubes;    // per unit cube: bounds of the interpolant (vr_prep.cuh launch_interp_bounds), brick order
     short2 *mcells;   // per 16^3 macro cell: union of its cells
     int nmx, nmy, nmz;
 };
@@ -34,7 +34,7 @@ static void free_volume(vr_volume *v) {
     cudaFree(v->data);
     cudaFree(v->cells);
     cudaFree(v->bricks);
-    cudaFree(v->win);
+    cudaFree(v->cubes);
     cudaFree(v->mcells);
     delete v;
 }
@@ -203,13 +203,13 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     cudaError_t e = cudaMalloc((void **)&v->cells, sizeof(short2) * (size_t)v->ncx * v->ncy * v->ncz);
     if (e == cudaSuccess) e = cudaMalloc((void **)&v->bricks, sizeof(int16_t) * 64 * (size_t)v->bnx * v->bny * v->bnz);
     if (e == cudaSuccess) e = vr::launch_brick_volume(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bricks, s);
-    if (e == cudaSuccess) e = cudaMalloc((void **)&v->win, sizeof(short2) * 64 * (size_t)v->bnx * v->bny * v->bnz);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&v->cubes, sizeof(short2) * 64 * (size_t)v->bnx * v->bny * v->bnz);
     v->nmx = (v->ncx + 3) / 4;
     v->nmy = (v->ncy + 3) / 4;
     v->nmz = (v->ncz + 3) / 4;
     if (e == cudaSuccess) e = cudaMalloc((void **)&v->mcells, sizeof(short2) * (size_t)v->nmx * v->nmy * v->nmz);
     if (e == cudaSuccess)
-        e = vr::launch_interp_bounds(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bnx, v->bny, v->win, v->ncx,
+        e = vr::launch_interp_bounds(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bnx, v->bny, v->cubes, v->ncx,
                                      v->ncy, v->ncz, v->cells, v->nmx, v->nmy, v->nmz, v->mcells, s);
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
     if (e == cudaSuccess) e = vr::launch_value_range(v->data, n, d_range, s);
@@ -342,7 +342,7 @@ int vr_volume_culling_tables(const vr_volume *v, int16_t *cubes, int16_t *cells)
     if (!v || (!cubes && !cells)) return fail(VR_EINVALID, "null pointer");
     DeviceGuard g(v->device);
     if (cubes)
-        VR_CUDA(cudaMemcpy(cubes, v->win, sizeof(short2) * 64 * (size_t)v->bnx * v->bny * v->bnz,
+        VR_CUDA(cudaMemcpy(cubes, v->cubes, sizeof(short2) * 64 * (size_t)v->bnx * v->bny * v->bnz,
                            cudaMemcpyDeviceToHost));
     if (cells)
         VR_CUDA(cudaMemcpy(cells, v->cells, sizeof(short2) * (size_t)v->ncx * v->ncy * v->ncz, cudaMemcpyDeviceToHost));
@@ -707,9 +707,9 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.ncx = vol->ncx;
         a.ncy = vol->ncy;
         a.cull = 1;
-        // per-cube bounds behind the cell bounds (development knob VR_NO_WINDOW=1 disables)
-        const char *nw = getenv("VR_NO_WINDOW");
-        a.win = (nw && atoi(nw)) ? nullptr : vol->win;
+        // per-cube bounds behind the cell bounds (development knob VR_NO_CUBES=1 disables)
+        const char *nw = getenv("VR_NO_CUBES");
+        a.cubes = (nw && atoi(nw)) ? nullptr : vol->cubes;
         const char *nm = getenv("VR_NO_MACRO");  // development knob: 1 disables the 16^3 level
         a.mcells = (nm && atoi(nm)) ? nullptr : vol->mcells;
         a.nmx = vol->nmx;

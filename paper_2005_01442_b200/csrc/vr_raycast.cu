@@ -222,8 +222,8 @@ VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z,
         return 3;
     if (bounds_transparent(__ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2)), vlo, vhi))
         return 1;
-    if (!a.win) return 0;
-    const short2 w = __ldg(a.win + (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
+    if (!a.cubes) return 0;
+    const short2 w = __ldg(a.cubes + (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
                            ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3));
     return bounds_transparent(w, vlo, vhi) ? 2 : 0;
 }

@@ -48,7 +48,7 @@ struct RenderArgs {
     // the LUT's first/last bins with nonzero opacity
     const short2 *cells;
     int ncx, ncy;
-    const short2 *win;     // optional per unit cube interpolant bounds, 4^3 brick order (index as bv)
+    const short2 *cubes;   // optional per unit cube interpolant bounds, 4^3 brick order (index as bv)
     const short2 *mcells;  // optional per 16^3 macro cell: union of its cells' bounds
     int nmx, nmy;
     const int *lut_range;
