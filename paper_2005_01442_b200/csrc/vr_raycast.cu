@@ -799,7 +799,8 @@ template <bool CUBIC, bool LIGHT, bool SKIP>
 #ifndef VR_POST_MIN_BLOCKS
 #define VR_POST_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (latency-bound; swept 1..5)
 #endif
-__global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_kernel(const __grid_constant__ RenderArgs a) {
+__global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads / kPersistThreads))
+    raycast_post_kernel(const __grid_constant__ RenderArgs a) {
 #ifdef VR_DEBUG_STATS
     // rays finished here without / with taken samples (count, trip-steps), rays handed over (count, trip-steps)
     unsigned long long dbg[6] = {};
@@ -1037,7 +1038,7 @@ __global__ void __launch_bounds__(kThreads, VR_POST_MIN_BLOCKS) raycast_post_ker
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         const unsigned long long rays = warp_sum(c_iter ? 1ull : 0ull);
         if (lane == 0) {
-            const long long w = (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+            const long long w = (long long)blockIdx.x * (kPersistThreads / 32) + (threadIdx.x >> 5);
             unsigned sm;
             asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
             a.debug_times[4 * w] = t_begin;
@@ -1100,7 +1101,8 @@ template <bool CUBIC, bool LIGHT, bool SKIP>
 #ifndef VR_HEAVY_MIN_BLOCKS
 #define VR_HEAVY_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (swept 3..8 with phase-A cap 32)
 #endif
-__global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_kernel(const __grid_constant__ RenderArgs a) {
+__global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThreads / kPersistThreads))
+    raycast_heavy_kernel(const __grid_constant__ RenderArgs a) {
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
@@ -1373,7 +1375,7 @@ __global__ void __launch_bounds__(kThreads, VR_HEAVY_MIN_BLOCKS) raycast_heavy_k
     if (a.debug_times && lane == 0) {
         unsigned long long t_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
-        const long long w = 148 * 32 + (long long)blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+        const long long w = 148 * 32 + (long long)blockIdx.x * (kPersistThreads / 32) + (threadIdx.x >> 5);
         a.debug_times[4 * w] = t_begin;
         a.debug_times[4 * w + 1] = t_end;
         a.debug_times[4 * w + 2] = count;  // rays handed over
@@ -1458,16 +1460,17 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
         int dev = 0, sms = 148, per_sm = 1;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPersistThreads, 0);
         long long ctas = (long long)sms * (per_sm > 0 ? per_sm : 1);
-        if (ctas > a.slots) ctas = a.slots;
+        const long long most = (long long)a.slots * (kThreads / kPersistThreads);  // a warp per 32 rays at most
+        if (ctas > most) ctas = most;
         // (the queue counters were zeroed by the frame's setup kernel)
-        k<<<(unsigned)ctas, kThreads, 0, stream>>>(a);
+        k<<<(unsigned)ctas, kPersistThreads, 0, stream>>>(a);
         if (a.heavy) {
             KernelFn h = pick_cooperative(a);
             int per_sm_h = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, h, kThreads, 0);
-            h<<<(unsigned)(sms * (per_sm_h > 0 ? per_sm_h : 1)), kThreads, 0, stream>>>(a);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, h, kPersistThreads, 0);
+            h<<<(unsigned)(sms * (per_sm_h > 0 ? per_sm_h : 1)), kPersistThreads, 0, stream>>>(a);
         }
         return cudaGetLastError();
     }

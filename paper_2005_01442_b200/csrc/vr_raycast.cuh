@@ -85,6 +85,10 @@ struct RenderArgs {
 constexpr int kTileW = 16;
 constexpr int kTileH = 8;
 constexpr int kThreads = 128;
+#ifndef VR_PERSIST_THREADS
+#define VR_PERSIST_THREADS 32  // one warp per CTA: resources free warp by warp (C3 +1 %)
+#endif
+constexpr int kPersistThreads = VR_PERSIST_THREADS;  // CTA size of the persistent ray casters
 constexpr size_t kHeavyRayBytes = 128;  // sizeof(HeavyRay) in vr_raycast.cu
 
 cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream);
