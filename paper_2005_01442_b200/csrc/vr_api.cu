@@ -524,7 +524,7 @@ int vr_grid_visibility(const vr_grid *gr, const double *lut_rgba, int32_t nbins,
     VR_CUDA(cudaMemcpyAsync(lut.p, lut_rgba, sizeof(double) * 4 * nbins, cudaMemcpyHostToDevice, s));
     VisScratch vs(s);
     VR_CUDA(vs.init(gr, (const double *)lut.p, nbins, lut_lo, lut_hi, 0.0, true));
-    VR_CUDA(vr::launch_visibility(gr->vol->data, gr->L, vs.v, s));
+    VR_CUDA(vr::launch_visibility(gr->vol->bricks, gr->L, vs.v, s));
     int nb = gr->nblocks;
     std::vector<long long> glob((size_t)nb * 6);
     unsigned long long cnt[2];
@@ -721,7 +721,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         vs.v.zero = zero;
         vs.v.lut_range = post ? (int *)lut_range.p : nullptr;
         vs.v.lut_inv_w = a.lut_inv_w;
-        VR_CUDA(vr::launch_visibility(vol->data, grid->L, vs.v, s));
+        VR_CUDA(vr::launch_visibility(vol->bricks, grid->L, vs.v, s));
         a.empty = vs.v.empty;
         a.box = vs.v.box;
         a.vmin = grid->vmin;

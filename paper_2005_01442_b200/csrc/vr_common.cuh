@@ -119,6 +119,81 @@ VR_D void visible_value_range(double lo, double inv_w, int nbins, int first_vis,
     vhi = a;
 }
 
+// The same thresholds with every thread of the CTA (all must call it; the
+// results are in vlo / vhi on return in every thread).  lut_bin is
+// nondecreasing in s, so each threshold is the first s of a false->true
+// predicate: a blockDim-ary search, 3 rounds over [-2^24, 2^24 + 1] instead of
+// the 2 x 25 dependent bisection steps of one thread.
+//   vlo = first s in [L, R] with lut_bin(s) >= first_vis (R when none)
+//   vhi = (first s in [L+1, R+1] with lut_bin(s) > last_vis) - 1 (R when none)
+// which is exactly what the bisections above return.
+VR_D void block_value_range(double lo, double inv_w, int nbins, int first_vis, int last_vis, int &vlo, int &vhi) {
+    __shared__ int lo_a, lo_b, hi_a, hi_b, lo_t, hi_t;
+    const int L = -(1 << 24), R = 1 << 24;
+    const int T = (int)blockDim.x, tid = (int)threadIdx.x;
+    const bool none = first_vis >= nbins || last_vis < 0;
+    if (tid == 0) {
+        lo_a = L;
+        lo_b = R;
+        hi_a = L + 1;
+        hi_b = R + 1;
+    }
+    __syncthreads();
+    for (;;) {
+        const int a0 = lo_a, b0 = lo_b, a1 = hi_a, b1 = hi_b;
+        if (none || (a0 >= b0 && a1 >= b1)) break;
+        const int st0 = (b0 - a0 + T - 1) / T, st1 = (b1 - a1 + T - 1) / T;
+        __syncthreads();  // everyone read the interval before it changes
+        if (tid == 0) {
+            lo_t = T;
+            hi_t = T;
+        }
+        __syncthreads();
+        if (a0 < b0) {
+            const long long m = (long long)a0 + (long long)tid * st0;
+            if (m < b0 && lut_bin((double)m, lo, inv_w, nbins) >= first_vis) atomicMin(&lo_t, tid);
+        }
+        if (a1 < b1) {
+            const long long m = (long long)a1 + (long long)tid * st1;
+            if (m < b1 && lut_bin((double)m, lo, inv_w, nbins) > last_vis) atomicMin(&hi_t, tid);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            // probes a + t*step (t < T, below b): the first true probe t* bounds
+            // the answer to (probe t*-1, probe t*]; none true: (last probe, b]
+            if (a0 < b0) {
+                const int t = lo_t;
+                if (t < T) {
+                    lo_b = a0 + t * st0;
+                    lo_a = t > 0 ? a0 + (t - 1) * st0 + 1 : a0;
+                } else {
+                    const int last = (b0 - 1 - a0) / st0;  // last probe below b
+                    lo_a = a0 + last * st0 + 1;
+                }
+            }
+            if (a1 < b1) {
+                const int t = hi_t;
+                if (t < T) {
+                    hi_b = a1 + t * st1;
+                    hi_a = t > 0 ? a1 + (t - 1) * st1 + 1 : a1;
+                } else {
+                    const int last = (b1 - 1 - a1) / st1;
+                    hi_a = a1 + last * st1 + 1;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (none) {
+        vlo = INT_MAX;
+        vhi = INT_MIN;
+    } else {
+        vlo = lo_a;
+        vhi = hi_a - 1;
+    }
+    __syncthreads();  // the shared state may be reused by a later call
+}
+
 // ----------------------------------------------------------- Catmull-Rom
 // _kernels.py:83-91
 VR_D void cr_weights(double t, double &w0, double &w1, double &w2, double &w3) {

@@ -294,6 +294,8 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
         ab[3] = ab[4] = ab[5] = -1;
     }
     __syncthreads();
+    int vlo = 0, vhi = 0;
+    if (v.lut_range) block_value_range(v.lut_lo, v.lut_inv_w, v.nbins, first_vis, last_vis, vlo, vhi);
     if (tid == 0) {
         v.counters[0] = n_empty;
         v.counters[1] = 0;
@@ -301,8 +303,8 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
         if (v.lut_range) {
             v.lut_range[0] = first_vis;
             v.lut_range[1] = last_vis;
-            visible_value_range(v.lut_lo, v.lut_inv_w, v.nbins, first_vis, last_vis, v.lut_range[2],
-                                v.lut_range[3]);
+            v.lut_range[2] = vlo;
+            v.lut_range[3] = vhi;
         }
     }
     if (tid < 6) v.uni[tid] = tid < 3 ? INT_MAX : INT_MIN;
@@ -340,7 +342,7 @@ VR_D int count_visible(const unsigned int *bits, const int *prefix, int lo, int 
 // that of a full scan.
 constexpr int kAabbThreads = 256;
 constexpr int kCand = 1024;  // cells examined per pass
-__global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__restrict__ vol, const Layout L,
+__global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__restrict__ bricks, const Layout L,
                                                             const VisArgs v, int zmax) {
     __shared__ unsigned int bits[2048];
     __shared__ int prefix[2049];
@@ -388,12 +390,15 @@ __global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__res
             const int nvox = ncand * 64;
             for (int e = threadIdx.x; e < nvox; e += blockDim.x) {
                 const int c = cand[e >> 6], w = e & 63;
-                const int x = (cx0 + c % ncx) * 4 + (w & 3) - ox;
-                const int y = (cy0 + c / ncx) * 4 + ((w >> 2) & 3) - oy;
+                const int gcx = cx0 + c % ncx, gcy = cy0 + c / ncx;
+                const int x = gcx * 4 + (w & 3) - ox;
+                const int y = gcy * 4 + ((w >> 2) & 3) - oy;
                 const int z = cz * 4 + (w >> 4) - oz;
                 if (x < 0 || x >= ex || y < 0 || y >= ey || z < 0 || z >= ez) continue;
-                const unsigned int u = (unsigned int)(__ldg(vol + (long long)(oz + z) * L.pz +
-                                                            (long long)(oy + y) * L.py + ox + x) + 32768);
+                // a cell is one 4^3 brick (128 contiguous bytes, w in brick
+                // order): a warp reads two whole cells, fully coalesced
+                const unsigned int u = (unsigned int)(
+                    __ldg(bricks + (((long long)cz * v.ncy + gcy) * v.ncx + gcx) * 64 + w) + 32768);
                 if ((bits[u >> 5] >> (u & 31)) & 1u) {
                     mnx = min(mnx, x); mxx = max(mxx, x);
                     mny = min(mny, y); mxy = max(mxy, y);
@@ -579,10 +584,13 @@ __global__ void lut_range_kernel(const double *lut, int nbins, double lut_lo, do
         }
     }
     __syncthreads();
+    int vlo, vhi;
+    block_value_range(lut_lo, lut_inv_w, nbins, first, last, vlo, vhi);
     if (threadIdx.x == 0) {
         range[0] = first;
         range[1] = last;
-        visible_value_range(lut_lo, lut_inv_w, nbins, first, last, range[2], range[3]);
+        range[2] = vlo;
+        range[3] = vhi;
     }
 }
 
@@ -822,7 +830,7 @@ cudaError_t launch_block_minmax(const int16_t *vol, const Layout &L, int *vmin, 
     return cudaGetLastError();
 }
 
-cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v, cudaStream_t s) {
+cudaError_t launch_visibility(const int16_t *bricks, const Layout &L, const VisArgs &v, cudaStream_t s) {
     size_t smem = (size_t)(v.nbins + 1) * sizeof(int);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(vis_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -830,7 +838,7 @@ cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs
     }
     visbits_kernel<<<2048 * 32 / kBlock, kBlock, 0, s>>>(v);
     vis_setup_kernel<<<1, kSetupThreads, smem, s>>>(v);
-    aabb_kernel<<<148 * 8, kAabbThreads, 0, s>>>(vol, L, v, zsplit_for(L));
+    aabb_kernel<<<148 * 8, kAabbThreads, 0, s>>>(bricks, L, v, zsplit_for(L));
     box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
     return cudaGetLastError();
 }

@@ -56,7 +56,7 @@ struct VisArgs {
     double lut_inv_w;        // the march's bin scale nbins / (hi - lo) (render.py:423)
     ZeroSpec zero;           // zeroed by the setup kernel (frame counters, totals, blocks_hit)
 };
-cudaError_t launch_visibility(const int16_t *vol, const Layout &L, const VisArgs &v,
+cudaError_t launch_visibility(const int16_t *bricks, const Layout &L, const VisArgs &v,
                               cudaStream_t s);
 
 // K1 brick upload: re-lay the x-fastest volume into 4x4x4 bricks of 64 voxels
