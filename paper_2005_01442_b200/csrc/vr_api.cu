@@ -507,6 +507,9 @@ struct VisScratch {
         v.ncx = gr->vol->ncx;
         v.ncy = gr->vol->ncy;
         v.ncz = gr->vol->ncz;
+        v.mcells = gr->vol->mcells;
+        v.nmx = gr->vol->nmx;
+        v.nmy = gr->vol->nmy;
         v.margin = margin;
         return cudaSuccess;
     }

@@ -119,7 +119,7 @@ VR_D void visible_value_range(double lo, double inv_w, int nbins, int first_vis,
     vhi = a;
 }
 
-// The same thresholds with every thread of the CTA (all must call it; the
+// The same thresholds with every thread of a 1024-thread CTA (all must call it; the
 // results are in vlo / vhi on return in every thread).  lut_bin is
 // nondecreasing in s, so each threshold is the first s of a false->true
 // predicate: a blockDim-ary search, 3 rounds over [-2^24, 2^24 + 1] instead of
@@ -130,7 +130,8 @@ VR_D void visible_value_range(double lo, double inv_w, int nbins, int first_vis,
 VR_D void block_value_range(double lo, double inv_w, int nbins, int first_vis, int last_vis, int &vlo, int &vhi) {
     __shared__ int lo_a, lo_b, hi_a, hi_b, lo_t, hi_t;
     const int L = -(1 << 24), R = 1 << 24;
-    const int T = (int)blockDim.x, tid = (int)threadIdx.x;
+    constexpr int T = 1024;  // callers launch 1024 threads (a constant divisor: shifts, not division)
+    const int tid = (int)threadIdx.x;
     const bool none = first_vis >= nbins || last_vis < 0;
     if (tid == 0) {
         lo_a = L;

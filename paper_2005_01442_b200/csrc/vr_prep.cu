@@ -1,4 +1,5 @@
 // vr_prep.cu -- K1/K2/K4 kernels and the point sampler (see vr_prep.cuh).
+#include <cstdlib>
 #include <cfloat>
 #include <climits>
 
@@ -366,15 +367,42 @@ __global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__res
         if (cz > (oz + ez - 1) >> 2) continue;
         const int cx0 = ox >> 2, cx1 = (ox + ex - 1) >> 2, cy0 = oy >> 2, cy1 = (oy + ey - 1) >> 2;
         const int ncx = cx1 - cx0 + 1, ncells = ncx * (cy1 - cy0 + 1);
+        if (v.mcells) {
+            // the macro cells (16^3) over this cell layer: when none can hold a
+            // visible value, neither can any of its cells.  Every warp takes the
+            // same decision, so the CTA skips the item without a barrier.
+            const int mx0 = cx0 >> 2, nmxi = (cx1 >> 2) - mx0 + 1, my0 = cy0 >> 2;
+            const int nm = nmxi * ((cy1 >> 2) - my0 + 1);
+            const short2 *mrow = v.mcells + (long long)(cz >> 2) * v.nmy * v.nmx;
+            bool vis = false;
+            for (int m = lane; m < nm && !vis; m += 32) {
+                const short2 mb = __ldg(mrow + (long long)(my0 + m / nmxi) * v.nmx + mx0 + m % nmxi);
+                vis = count_visible(bits, prefix, mb.x, mb.y) > 0;
+            }
+            if (!__any_sync(0xffffffffu, vis)) continue;
+        }
         int mnx = INT_MAX, mny = INT_MAX, mnz = INT_MAX, mxx = -1, mxy = -1, mxz = -1;
         // in chunks of kCand cells: (1) collect the cells that may hold a
         // visible voxel, (2) test their voxels, one per thread
         for (int c0 = 0; c0 < ncells; c0 += kCand) {
             if (threadIdx.x == 0) ncand = 0;
             __syncthreads();
-            for (int c = c0 + threadIdx.x; c < min(ncells, c0 + kCand); c += blockDim.x) {
+            // (loads of a pass issued before any is used: one memory round
+            // trip per pass instead of one per iteration)
+            const int cend = min(ncells, c0 + kCand);
+            short2 cbs[kCand / kAabbThreads];
+#pragma unroll
+            for (int j = 0; j < kCand / kAabbThreads; ++j) {
+                const int c = c0 + (int)threadIdx.x + j * kAabbThreads;
+                if (c < cend)
+                    cbs[j] = __ldg(v.cells + ((long long)cz * v.ncy + cy0 + c / ncx) * v.ncx + cx0 + c % ncx);
+            }
+#pragma unroll
+            for (int j = 0; j < kCand / kAabbThreads; ++j) {
+                const int c = c0 + (int)threadIdx.x + j * kAabbThreads;
+                if (c >= cend) continue;
                 const int cx = cx0 + c % ncx, cy = cy0 + c / ncx;
-                const short2 cb = __ldg(v.cells + ((long long)cz * v.ncy + cy) * v.ncx + cx);
+                const short2 cb = cbs[j];
                 const int nv = count_visible(bits, prefix, cb.x, cb.y);
                 if (nv == (int)cb.y - (int)cb.x + 1) {
                     // every value the cell can hold is visible: all its voxels
@@ -388,21 +416,35 @@ __global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__res
             }
             __syncthreads();
             const int nvox = ncand * 64;
-            for (int e = threadIdx.x; e < nvox; e += blockDim.x) {
-                const int c = cand[e >> 6], w = e & 63;
-                const int gcx = cx0 + c % ncx, gcy = cy0 + c / ncx;
-                const int x = gcx * 4 + (w & 3) - ox;
-                const int y = gcy * 4 + ((w >> 2) & 3) - oy;
-                const int z = cz * 4 + (w >> 4) - oz;
-                if (x < 0 || x >= ex || y < 0 || y >= ey || z < 0 || z >= ez) continue;
-                // a cell is one 4^3 brick (128 contiguous bytes, w in brick
-                // order): a warp reads two whole cells, fully coalesced
-                const unsigned int u = (unsigned int)(
-                    __ldg(bricks + (((long long)cz * v.ncy + gcy) * v.ncx + gcx) * 64 + w) + 32768);
-                if ((bits[u >> 5] >> (u & 31)) & 1u) {
-                    mnx = min(mnx, x); mxx = max(mxx, x);
-                    mny = min(mny, y); mxy = max(mxy, y);
-                    mnz = min(mnz, z); mxz = max(mxz, z);
+            constexpr int kU = 4;  // voxel loads in flight per thread
+            for (int e0 = threadIdx.x; e0 < nvox; e0 += kAabbThreads * kU) {
+                int16_t val[kU];
+#pragma unroll
+                for (int j = 0; j < kU; ++j) {
+                    const int e = e0 + j * kAabbThreads;
+                    if (e < nvox) {
+                        // a cell is one 4^3 brick (128 contiguous bytes, w in
+                        // brick order): a warp reads two whole cells, coalesced
+                        const int c = cand[e >> 6];
+                        val[j] = __ldg(bricks + (((long long)cz * v.ncy + cy0 + c / ncx) * v.ncx + cx0 + c % ncx) * 64 +
+                                       (e & 63));
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < kU; ++j) {
+                    const int e = e0 + j * kAabbThreads;
+                    if (e >= nvox) continue;
+                    const int c = cand[e >> 6], w = e & 63;
+                    const int x = (cx0 + c % ncx) * 4 + (w & 3) - ox;
+                    const int y = (cy0 + c / ncx) * 4 + ((w >> 2) & 3) - oy;
+                    const int z = cz * 4 + (w >> 4) - oz;
+                    if (x < 0 || x >= ex || y < 0 || y >= ey || z < 0 || z >= ez) continue;
+                    const unsigned int u = (unsigned int)((int)val[j] + 32768);
+                    if ((bits[u >> 5] >> (u & 31)) & 1u) {
+                        mnx = min(mnx, x); mxx = max(mxx, x);
+                        mny = min(mny, y); mxy = max(mxy, y);
+                        mnz = min(mnz, z); mxz = max(mxz, z);
+                    }
                 }
             }
             __syncthreads();  // cand / ncand reused
@@ -838,7 +880,11 @@ cudaError_t launch_visibility(const int16_t *bricks, const Layout &L, const VisA
     }
     visbits_kernel<<<2048 * 32 / kBlock, kBlock, 0, s>>>(v);
     vis_setup_kernel<<<1, kSetupThreads, smem, s>>>(v);
-    aabb_kernel<<<148 * 8, kAabbThreads, 0, s>>>(bricks, L, v, zsplit_for(L));
+    static int per_sm = [] {
+        const char *e = getenv("VR_AABB_CTAS");  // CTAs per SM (experiments)
+        return e && atoi(e) > 0 ? atoi(e) : 8;
+    }();
+    aabb_kernel<<<148 * per_sm, kAabbThreads, 0, s>>>(bricks, L, v, zsplit_for(L));
     box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
     return cudaGetLastError();
 }

@@ -51,6 +51,8 @@ struct VisArgs {
     int *visprefix;          // 2049: visible values in visbits words [0, w)
     const short2 *cells;     // the volume's 4^3 cell bounds (cover every voxel value of the cell)
     int ncx, ncy, ncz;
+    const short2 *mcells;    // unions over 4^3 cells (16^3 voxels): whole layers of a block skipped at once
+    int nmx, nmy;
     double margin;
     int *lut_range;          // optional out (4 ints): as launch_lut_range
     double lut_inv_w;        // the march's bin scale nbins / (hi - lo) (render.py:423)
