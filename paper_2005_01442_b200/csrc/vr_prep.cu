@@ -415,35 +415,41 @@ __global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__res
                 }
             }
             __syncthreads();
-            const int nvox = ncand * 64;
-            constexpr int kU = 4;  // voxel loads in flight per thread
-            for (int e0 = threadIdx.x; e0 < nvox; e0 += kAabbThreads * kU) {
-                int16_t val[kU];
+            // the candidate cells' voxels, 16 bytes (8 voxels: half a z-slice
+            // of the brick) per thread and load, all loads of a pass in flight
+            const int nvec = ncand * 8;
+            constexpr int kU = 4;
+            for (int e0 = threadIdx.x; e0 < nvec; e0 += kAabbThreads * kU) {
+                uint4 val[kU];
 #pragma unroll
                 for (int j = 0; j < kU; ++j) {
                     const int e = e0 + j * kAabbThreads;
-                    if (e < nvox) {
-                        // a cell is one 4^3 brick (128 contiguous bytes, w in
-                        // brick order): a warp reads two whole cells, coalesced
-                        const int c = cand[e >> 6];
-                        val[j] = __ldg(bricks + (((long long)cz * v.ncy + cy0 + c / ncx) * v.ncx + cx0 + c % ncx) * 64 +
-                                       (e & 63));
+                    if (e < nvec) {
+                        // a cell is one 4^3 brick: 128 contiguous bytes, x fastest
+                        const int c = cand[e >> 3];
+                        const long long brick = ((long long)cz * v.ncy + cy0 + c / ncx) * v.ncx + cx0 + c % ncx;
+                        val[j] = __ldg(reinterpret_cast<const uint4 *>(bricks + brick * 64) + (e & 7));
                     }
                 }
 #pragma unroll
                 for (int j = 0; j < kU; ++j) {
                     const int e = e0 + j * kAabbThreads;
-                    if (e >= nvox) continue;
-                    const int c = cand[e >> 6], w = e & 63;
-                    const int x = (cx0 + c % ncx) * 4 + (w & 3) - ox;
-                    const int y = (cy0 + c / ncx) * 4 + ((w >> 2) & 3) - oy;
-                    const int z = cz * 4 + (w >> 4) - oz;
-                    if (x < 0 || x >= ex || y < 0 || y >= ey || z < 0 || z >= ez) continue;
-                    const unsigned int u = (unsigned int)((int)val[j] + 32768);
-                    if ((bits[u >> 5] >> (u & 31)) & 1u) {
-                        mnx = min(mnx, x); mxx = max(mxx, x);
-                        mny = min(mny, y); mxy = max(mxy, y);
-                        mnz = min(mnz, z); mxz = max(mxz, z);
+                    if (e >= nvec) continue;
+                    const int c = cand[e >> 3], q = e & 7;
+                    const int z = cz * 4 + (q >> 1) - oz;
+                    const int bx = (cx0 + c % ncx) * 4 - ox, by = (cy0 + c / ncx) * 4 - oy;
+                    const unsigned words[4] = {val[j].x, val[j].y, val[j].z, val[j].w};
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        // voxel w = 8q + k of the brick: x = k & 3, y = (2q + k/4) & 3, z = q / 2
+                        const int x = bx + (k & 3), y = by + (((q << 1) + (k >> 2)) & 3);
+                        const unsigned u = (unsigned)((int)(short)(words[k >> 1] >> (16 * (k & 1))) + 32768);
+                        if (x >= 0 && x < ex && y >= 0 && y < ey && z >= 0 && z < ez &&
+                            ((bits[u >> 5] >> (u & 31)) & 1u)) {
+                            mnx = min(mnx, x); mxx = max(mxx, x);
+                            mny = min(mny, y); mxy = max(mxy, y);
+                            mnz = min(mnz, z); mxz = max(mxz, z);
+                        }
                     }
                 }
             }
