@@ -119,18 +119,18 @@ VR_D void visible_value_range(double lo, double inv_w, int nbins, int first_vis,
     vhi = a;
 }
 
-// The same thresholds with every thread of a 1024-thread CTA (all must call it; the
+// The same thresholds with every thread of a T-thread CTA (all must call it; the
 // results are in vlo / vhi on return in every thread).  lut_bin is
 // nondecreasing in s, so each threshold is the first s of a false->true
-// predicate: a blockDim-ary search, 3 rounds over [-2^24, 2^24 + 1] instead of
+// predicate: a T-ary search (T = 1024: 3 rounds over [-2^24, 2^24 + 1]) instead of
 // the 2 x 25 dependent bisection steps of one thread.
 //   vlo = first s in [L, R] with lut_bin(s) >= first_vis (R when none)
 //   vhi = (first s in [L+1, R+1] with lut_bin(s) > last_vis) - 1 (R when none)
 // which is exactly what the bisections above return.
+template <int T>
 VR_D void block_value_range(double lo, double inv_w, int nbins, int first_vis, int last_vis, int &vlo, int &vhi) {
     __shared__ int lo_a, lo_b, hi_a, hi_b, lo_t, hi_t;
     const int L = -(1 << 24), R = 1 << 24;
-    constexpr int T = 1024;  // callers launch 1024 threads (a constant divisor: shifts, not division)
     const int tid = (int)threadIdx.x;
     const bool none = first_vis >= nbins || last_vis < 0;
     if (tid == 0) {

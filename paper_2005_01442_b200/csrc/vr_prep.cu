@@ -193,14 +193,19 @@ VR_D int classified_bin_fast(double s, double lo, double bin_width, double inv_w
     return (int)f;
 }
 
-constexpr int kSetupThreads = 1024;
+#ifndef VR_SETUP_THREADS
+#define VR_SETUP_THREADS 1024
+#endif
+constexpr int kSetupThreads = VR_SETUP_THREADS;  // 64..1024 (2048 visbits words split evenly)
+constexpr int kSetupWarps = kSetupThreads / 32;
+static_assert(kSetupThreads >= 64 && kSetupThreads <= 1024 && 2048 % kSetupThreads == 0, "setup CTA size");
 
 // cull_empty (blocks.py:161-173) + the per-value visibility bitmask that
 // fit_bounding_box (blocks.py:176-199) tests per voxel, and the list of
 // non-empty blocks the AABB fit walks.  One CTA.
 __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs v) {
     extern __shared__ int prefix[];  // nbins + 1
-    __shared__ int warp_tot[kSetupThreads / 32];
+    __shared__ int warp_tot[kSetupWarps];
     __shared__ unsigned int n_empty;
     __shared__ int n_list;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -228,15 +233,15 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
         n_list = 0;
     }
     __syncthreads();
-    if (wid == 0) {
-        const int w = warp_tot[lane];
+    if (wid == 0) {  // exclusive scan of the warp totals
+        const int w = lane < kSetupWarps ? warp_tot[lane] : 0;
         int inc = w;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        warp_tot[lane] = inc - w;
+        if (lane < kSetupWarps) warp_tot[lane] = inc - w;
     }
     __syncthreads();
     int run = warp_tot[wid] + incl - s;
@@ -253,8 +258,14 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
     __syncthreads();
     // visible values before each visbits word (for the AABB fit's cell test)
     {
-        int c0 = __popc(v.visbits[2 * tid]), c1 = __popc(v.visbits[2 * tid + 1]);
-        int sum = c0 + c1, inc = sum;
+        constexpr int kWords = 2048 / kSetupThreads;  // visbits words per thread
+        int cnt[kWords], sum = 0;
+#pragma unroll
+        for (int j = 0; j < kWords; ++j) {
+            cnt[j] = __popc(v.visbits[kWords * tid + j]);
+            sum += cnt[j];
+        }
+        int inc = sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, inc, o);
@@ -264,20 +275,23 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
         if (lane == 31) warp_tot[wid] = inc;
         __syncthreads();
         if (wid == 0) {
-            const int w = warp_tot[lane];
+            const int w = lane < kSetupWarps ? warp_tot[lane] : 0;
             int x = w;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            warp_tot[lane] = x - w;
+            if (lane < kSetupWarps) warp_tot[lane] = x - w;
         }
         __syncthreads();
-        const int ex = warp_tot[wid] + inc - sum;
-        v.visprefix[2 * tid] = ex;
-        v.visprefix[2 * tid + 1] = ex + c0;
-        if (tid == kSetupThreads - 1) v.visprefix[2048] = ex + sum;
+        int ex = warp_tot[wid] + inc - sum;
+#pragma unroll
+        for (int j = 0; j < kWords; ++j) {
+            v.visprefix[kWords * tid + j] = ex;
+            ex += cnt[j];
+        }
+        if (tid == kSetupThreads - 1) v.visprefix[2048] = ex;
     }
     const double inv_w = 1.0 / v.bin_width;
     // interval test per block, sentinel AABB for the fit kernel
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
     }
     __syncthreads();
     int vlo = 0, vhi = 0;
-    if (v.lut_range) block_value_range(v.lut_lo, v.lut_inv_w, v.nbins, first_vis, last_vis, vlo, vhi);
+    if (v.lut_range) block_value_range<kSetupThreads>(v.lut_lo, v.lut_inv_w, v.nbins, first_vis, last_vis, vlo, vhi);
     if (tid == 0) {
         v.counters[0] = n_empty;
         v.counters[1] = 0;
@@ -633,7 +647,7 @@ __global__ void lut_range_kernel(const double *lut, int nbins, double lut_lo, do
     }
     __syncthreads();
     int vlo, vhi;
-    block_value_range(lut_lo, lut_inv_w, nbins, first, last, vlo, vhi);
+    block_value_range<kSetupThreads>(lut_lo, lut_inv_w, nbins, first, last, vlo, vhi);
     if (threadIdx.x == 0) {
         range[0] = first;
         range[1] = last;
@@ -937,7 +951,7 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
 
 cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double lut_inv_w, int *range,
                              const ZeroSpec &zero, cudaStream_t s) {
-    lut_range_kernel<<<1, 1024, 0, s>>>(lut, nbins, lut_lo, lut_inv_w, range, zero);
+    lut_range_kernel<<<1, kSetupThreads, 0, s>>>(lut, nbins, lut_lo, lut_inv_w, range, zero);
     return cudaGetLastError();
 }
 
