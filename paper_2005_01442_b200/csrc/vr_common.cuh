@@ -10,6 +10,8 @@
 #include <climits>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 
 #define VR_HD __host__ __device__ __forceinline__
@@ -27,6 +29,42 @@ VR_HD int clampi(int v, int lo, int hi) {
     if (v < lo) return lo;
     if (v > hi) return hi;
     return v;
+}
+
+// Programmatic dependent launch between the frame's kernels (visibility
+// setup -> ray casters -> hit count).  Each such kernel starts with
+// pdl_enter(): it waits for its predecessor grid to complete (and its writes
+// to be visible) before touching memory, then lets its own successor launch,
+// so the successor's launch and CTA rasterisation overlap this kernel instead
+// of following it.  The data dependences are those of plain stream order.
+VR_D void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Launch with the programmatic-serialisation attribute (VR_NO_PDL=1: plain
+// stream order, for A/B).  Only kernels that begin with pdl_enter() may be
+// launched this way.
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("VR_NO_PDL");
+        return !(e && atoi(e));
+    }();
+    return on;
+}
+template <typename... P, typename... A>
+cudaError_t launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
 }
 
 // Python's max(a, 0.0)

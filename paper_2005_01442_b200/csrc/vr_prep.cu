@@ -204,6 +204,7 @@ static_assert(kSetupThreads >= 64 && kSetupThreads <= 1024 && 2048 % kSetupThrea
 // fit_bounding_box (blocks.py:176-199) tests per voxel, and the list of
 // non-empty blocks the AABB fit walks.  One CTA.
 __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs v) {
+    pdl_enter();
     extern __shared__ int prefix[];  // nbins + 1
     __shared__ int warp_tot[kSetupWarps];
     __shared__ unsigned int n_empty;
@@ -329,6 +330,7 @@ __global__ void __launch_bounds__(kSetupThreads) vis_setup_kernel(const VisArgs 
 // fit_bounding_box applies per voxel): one warp per 32-value word, spread
 // over the GPU (65536 bins on a single SM were 12 us of issue time).
 __global__ void __launch_bounds__(kBlock) visbits_kernel(const VisArgs v) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (w >= 2048) return;
@@ -359,6 +361,7 @@ constexpr int kAabbThreads = 256;
 constexpr int kCand = 1024;  // cells examined per pass
 __global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__restrict__ bricks, const Layout L,
                                                             const VisArgs v, int zmax) {
+    pdl_enter();
     __shared__ unsigned int bits[2048];
     __shared__ int prefix[2049];
     __shared__ int cand[kCand];
@@ -482,6 +485,7 @@ __global__ void __launch_bounds__(kAabbThreads) aabb_kernel(const int16_t *__res
 // dilate by one, clip to the block, globalise (blocks.py:189-198) and apply
 // the render margin (render.py:388-390)
 __global__ void box_kernel(const Layout L, const VisArgs v) {
+    pdl_enter();
     int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= v.nblocks) return;
     int bi, bj, bk;
@@ -632,6 +636,7 @@ __global__ void __launch_bounds__(kBlock) cell_from_cubes_kernel(const short2 *_
 
 __global__ void lut_range_kernel(const double *lut, int nbins, double lut_lo, double lut_inv_w, int *range,
                                  const ZeroSpec zero) {
+    pdl_enter();
     __shared__ int first, last;
     zero_fill(zero);
     if (threadIdx.x == 0) {
@@ -658,6 +663,7 @@ __global__ void lut_range_kernel(const double *lut, int nbins, double lut_lo, do
 
 __global__ void count_hits_kernel(const uint8_t *hits, int n, unsigned long long *out,
                                   const unsigned long long *vis_counters) {
+    pdl_enter();
     if (vis_counters && threadIdx.x < 2) out[1 + threadIdx.x] = vis_counters[threadIdx.x];
     unsigned long long c = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) c += hits[i] ? 1 : 0;
@@ -898,14 +904,18 @@ cudaError_t launch_visibility(const int16_t *bricks, const Layout &L, const VisA
         cudaError_t e = cudaFuncSetAttribute(vis_setup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    visbits_kernel<<<2048 * 32 / kBlock, kBlock, 0, s>>>(v);
-    vis_setup_kernel<<<1, kSetupThreads, smem, s>>>(v);
+    cudaError_t e = launch_pdl(visbits_kernel, 2048 * 32 / kBlock, kBlock, 0, s, v);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(vis_setup_kernel, 1, kSetupThreads, smem, s, v);
+    if (e != cudaSuccess) return e;
     static int per_sm = [] {
         const char *e = getenv("VR_AABB_CTAS");  // CTAs per SM (experiments)
         return e && atoi(e) > 0 ? atoi(e) : 8;
     }();
-    aabb_kernel<<<148 * per_sm, kAabbThreads, 0, s>>>(bricks, L, v, zsplit_for(L));
-    box_kernel<<<(v.nblocks + 127) / 128, 128, 0, s>>>(L, v);
+    e = launch_pdl(aabb_kernel, 148 * per_sm, kAabbThreads, 0, s, bricks, L, v, zsplit_for(L));
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(box_kernel, (v.nblocks + 127) / 128, 128, 0, s, L, v);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
@@ -951,13 +961,15 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
 
 cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double lut_inv_w, int *range,
                              const ZeroSpec &zero, cudaStream_t s) {
-    lut_range_kernel<<<1, kSetupThreads, 0, s>>>(lut, nbins, lut_lo, lut_inv_w, range, zero);
+    cudaError_t e = launch_pdl(lut_range_kernel, 1, kSetupThreads, 0, s, lut, nbins, lut_lo, lut_inv_w, range, zero);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
 cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out,
                               const unsigned long long *vis_counters, cudaStream_t s) {
-    count_hits_kernel<<<1, 1024, 0, s>>>(hits, n, out, vis_counters);
+    cudaError_t e = launch_pdl(count_hits_kernel, 1, 1024, 0, s, hits, n, out, vis_counters);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

@@ -801,6 +801,7 @@ template <bool CUBIC, bool LIGHT, bool SKIP>
 #endif
 __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads / kPersistThreads))
     raycast_post_kernel(const __grid_constant__ RenderArgs a) {
+    pdl_enter();
 #ifdef VR_DEBUG_STATS
     // rays finished here without / with taken samples (count, trip-steps), rays handed over (count, trip-steps)
     unsigned long long dbg[6] = {};
@@ -1103,6 +1104,7 @@ template <bool CUBIC, bool LIGHT, bool SKIP>
 #endif
 __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThreads / kPersistThreads))
     raycast_heavy_kernel(const __grid_constant__ RenderArgs a) {
+    pdl_enter();
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
@@ -1465,12 +1467,14 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
         const long long most = (long long)a.slots * (kThreads / kPersistThreads);  // a warp per 32 rays at most
         if (ctas > most) ctas = most;
         // (the queue counters were zeroed by the frame's setup kernel)
-        k<<<(unsigned)ctas, kPersistThreads, 0, stream>>>(a);
+        cudaError_t e = launch_pdl(k, (unsigned)ctas, kPersistThreads, 0, stream, a);
+        if (e != cudaSuccess) return e;
         if (a.heavy) {
             KernelFn h = pick_cooperative(a);
             int per_sm_h = 1;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, h, kPersistThreads, 0);
-            h<<<(unsigned)(sms * (per_sm_h > 0 ? per_sm_h : 1)), kPersistThreads, 0, stream>>>(a);
+            e = launch_pdl(h, (unsigned)(sms * (per_sm_h > 0 ? per_sm_h : 1)), kPersistThreads, 0, stream, a);
+            if (e != cudaSuccess) return e;
         }
         return cudaGetLastError();
     }
