@@ -680,10 +680,12 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.heavy_count = a.work_counter + 1;
         a.heavy_head = a.work_counter + 2;
         a.heavy_count_long = a.work_counter + 3;
-        // rays with >= 256 samples left are queued apart and taken first by
-        // the cooperative kernel (sweep 128..512: C3 +5 %, C2 +5 %)
+        // rays with >= 384 samples left are queued apart and taken first by
+        // the cooperative kernel (sweep 128..512: C3 +5 %, C2 +5 % over one
+        // queue; 384 vs 256 after the first-trip hand-off rule: C3 +1.4 %,
+        // C2/C4 within noise, tools/gpu_sweep_long.sh)
         const char *hl = getenv("VR_HEAVY_LONG");
-        a.heavy_long = hl ? atoll(hl) : 256;
+        a.heavy_long = hl ? atoll(hl) : 384;
         const long long items = (long long)a.slots * vr::kTileW * vr::kTileH;
         a.heavy_cap = items < (1LL << 20) ? items : (1LL << 20);
         // development knob: VR_HEAVY_MIN_LEFT (default 64, the best of a
