@@ -22,6 +22,7 @@
 // samples stalled on no_instructions) and needed 154 registers.
 #include <cfloat>
 #include <climits>
+#include <mutex>
 
 #include "vr_raycast.cuh"
 
@@ -1448,6 +1449,41 @@ KernelFn pick_cubic(bool cubic, bool light, bool skip) {
     return cubic ? pick_light<KIND, true>(light, skip) : pick_light<KIND, false>(light, skip);
 }
 
+// Resident CTAs per SM of a persistent kernel, and the device's SM count:
+// queried once and cached (two runtime queries per frame were host time on
+// the end-to-end path).  Reentrant callers share the cache under a lock.
+int persistent_ctas_per_sm(KernelFn k) {
+    static std::mutex mu;
+    static KernelFn keys[32];
+    static int vals[32];
+    static int n = 0;
+    std::lock_guard<std::mutex> g(mu);
+    for (int i = 0; i < n; ++i)
+        if (keys[i] == k) return vals[i];
+    int per_sm = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPersistThreads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    if (n < 32) {
+        keys[n] = k;
+        vals[n] = per_sm;
+        ++n;
+    }
+    return per_sm;
+}
+
+int device_sms() {
+    static int sms[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (sms[dev] == 0) {
+        int v = 148;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        sms[dev] = v;
+    }
+    return sms[dev];
+}
+
 KernelFn pick(const RenderArgs &a) {
     const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
     if (a.mode == 1) return pick_cubic<kIso>(c, l, s);
@@ -1466,11 +1502,8 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
     if (a.mode == 0 && a.classify == 0 && a.work_counter) {
         // persistent: enough CTAs to fill every SM at the kernel's occupancy
         KernelFn k = pick_persistent(a);
-        int dev = 0, sms = 148, per_sm = 1;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPersistThreads, 0);
-        long long ctas = (long long)sms * (per_sm > 0 ? per_sm : 1);
+        const int sms = device_sms(), per_sm = persistent_ctas_per_sm(k);
+        long long ctas = (long long)sms * per_sm;
         const long long most = (long long)a.slots * (kThreads / kPersistThreads);  // a warp per 32 rays at most
         if (ctas > most) ctas = most;
         // (the queue counters were zeroed by the frame's setup kernel)
@@ -1478,9 +1511,7 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
         if (e != cudaSuccess) return e;
         if (a.heavy) {
             KernelFn h = pick_cooperative(a);
-            int per_sm_h = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_h, h, kPersistThreads, 0);
-            e = launch_pdl(h, (unsigned)(sms * (per_sm_h > 0 ? per_sm_h : 1)), kPersistThreads, 0, stream, a);
+            e = launch_pdl(h, (unsigned)(sms * persistent_ctas_per_sm(h)), kPersistThreads, 0, stream, a);
             if (e != cudaSuccess) return e;
         }
         return cudaGetLastError();
