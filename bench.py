@@ -75,8 +75,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
     p.add_argument("--transport", choices=("shared", "gather"), default=None,
-                   help="N>1 frame exchange: ranks store cells into rank 0's frame over NVLink "
-                        "(shared, default with nccl) or one NCCL/gloo gather (default with gloo)")
+                   help="N>1 frame exchange: one stream-ordered NCCL/gloo gather of the packed cells "
+                        "(gather, default) or stores into rank 0's frame over NVLink (shared; host "
+                        "barriers per frame)")
     p.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
                    help="override a RenderSettings field of the config (ablations)")
     args = p.parse_args()
@@ -189,6 +190,20 @@ def committed_traffic(config):
     return None
 
 
+def committed_ncu(config):
+    """Issue / pipe utilisation and memory traffic of the ray casters from the
+    committed ncu --set full capture (profiles/ncu_raycast_<config>.json)."""
+    p = ROOT / "profiles" / f"ncu_raycast_{config}.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+    except Exception:
+        return None
+    return {k: d[k] for k in ("source", "kernels", "dram_bytes_per_launch", "issue_active_pct",
+                              "fp64_pipe_pct", "l1_hit_pct", "l2_hit_pct", "warps_active_pct") if k in d}
+
+
 def dist_setup(n, backend):
     """One process per GPU (torchrun env); NCCL over NVLink by default.  gloo
     (CPU transport, several ranks may share one GPU) exists only to exercise
@@ -226,42 +241,66 @@ def orbit_cameras(vr, extent, size, views):
     return cams
 
 
+ORACLE_DEFAULTS = dict(step=None, interpolation="trilinear", classification="post", mode="dvr",
+                       isovalue=None, lighting=True, early_termination_alpha=0.99, use_blocks=False,
+                       block_size=64, overlap=3, background=(0.0, 0.0, 0.0, 1.0), ambient=0.1,
+                       diffuse=0.7, specular=0.2, shininess=32.0)  # RenderSettings defaults, render.py:159-181
+
+
+def oracle_scene_args(cfg, extent):
+    """Camera, TF arrays and settings of a config for the CPU oracle, built
+    without the product package (the reference arm maps no product code)."""
+    from types import SimpleNamespace
+
+    from oracle import oracle as O
+
+    cx, cy, cz = (0.5 * e for e in extent)
+    d = 2.2 * max(extent)
+    cam = SimpleNamespace(position=(cx + d, cy, cz), look_at=(cx, cy, cz), up=(0.0, 0.0, 1.0),
+                          vertical_fov_deg=30.0, width=cfg["size"], height=cfg["size"],
+                          projection=cfg["projection"],
+                          half_height_mm=0.5 * max(extent) + 1.0 if cfg["projection"] == "orthographic" else None)
+    settings = SimpleNamespace(**dict(ORACLE_DEFAULTS, **cfg["settings"]))
+    return cam, O.preset_arrays(cfg["tf"]), settings
+
+
 def cpu_oracle_frame(values, spacing, camera, tf, settings, nthreads=0):
-    """One full frame through the CPU oracle (prep + march), like reference render()."""
+    """One full frame through the CPU oracle (prep + march), like reference render().
+    tf = (values, rgba, domain) arrays."""
     from oracle import oracle as O
 
     t0 = time.perf_counter()
-    r = O.render(values, spacing, camera, tf.values, tf.rgba, tf.domain, settings,
+    r = O.render(values, spacing, camera, tf[0], tf[1], tf[2], settings,
                  projection=getattr(camera, "projection", "pinhole"),
                  ortho_half_h=getattr(camera, "half_height_mm", None), nthreads=nthreads)
     return time.perf_counter() - t0, r
 
 
+def bench_config(args, cfg):
+    """The `config` object both arms print (identical, so the driver can pair them)."""
+    return {"workload": args.config, "desc": cfg["desc"], "volume": list(cfg["dims"]),
+            "image": [cfg["size"], cfg["size"]], "views_per_step": cfg.get("views", 1), "tf": cfg["tf"],
+            "settings": {k: v for k, v in sorted(cfg["settings"].items())}}
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle port on all host threads, rank 0 only."""
+    """--impl reference: the CPU oracle port (C restatement of the reference's
+    numba march + numpy prep, pinned to the reference's goldens) on all host
+    threads, rank 0 only.  Nothing from the product package is imported: the
+    phantom is the oracle's numpy restatement of phantoms.py."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
-
-    import paper_2005_01442_b200 as vr
     from oracle import oracle as O
 
     cfg = CONFIGS[args.config]
-    values = O.phantom("torso", cfg["dims"]) if np.prod(cfg["dims"]) <= 64 ** 3 else None
-    if values is None:
-        # the product's device generator is bit-identical to the numpy phantom
-        # (pinned by tests/test_gpu_parity.py); use it when a GPU is present
-        try:
-            values = vr.device_phantom("torso", cfg["dims"]).download()
-        except Exception:
-            values = O.phantom("torso", cfg["dims"])
+    t_ph = time.perf_counter()
+    values = O.phantom("torso", cfg["dims"])
+    t_ph = time.perf_counter() - t_ph
     spacing = (1.0, 1.0, 1.0)
     nz, ny, nx = values.shape
     extent = ((nx - 1) * spacing[0], (ny - 1) * spacing[1], (nz - 1) * spacing[2])
-    camera = make_camera(vr, cfg, extent)
-    tf = vr.get_preset(cfg["tf"])
-    settings = vr.RenderSettings(**cfg["settings"])
+    camera, tf, settings = oracle_scene_args(cfg, extent)
     threads = O.num_threads()
     for _ in range(max(args.warmup, 0)):
         cpu_oracle_frame(values, spacing, camera, tf, settings)
@@ -277,12 +316,13 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "samples_per_sec": taken * fps,
-        "config": {"workload": args.config, "desc": cfg["desc"], "volume": list(cfg["dims"]),
-                   "image": [cfg["size"], cfg["size"]], "tf": cfg["tf"]},
+        "samples_per_sec": taken * fps, "samples_taken": taken,
+        "config": bench_config(args, cfg),
+        "parallelism": f"CPU, {threads} threads (rank 0 only)",
         "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
                          "sample": f"{args.steps} full {args.config} frames via oracle.render "
-                                   "(C restatement of _kernels.march, OpenMP over pixels, prep included)"},
+                                   "(C restatement of _kernels.march, OpenMP over pixels, prep included; "
+                                   f"phantom from the oracle's numpy generator, {t_ph:.1f} s, untimed)"},
         "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -322,7 +362,9 @@ def run_ours(args):
     cameras = orbit_cameras(vr, extent, cfg["size"], views) if views > 1 else [make_camera(vr, cfg, extent)]
     tf = vr.get_preset(cfg["tf"])
     settings = vr.RenderSettings(**cfg["settings"])
-    transport = args.transport or ("shared" if args.dist_backend == "nccl" else "gather")
+    # the NCCL gather is stream-ordered (no host round trip per frame); the
+    # CUDA-IPC shared frame needs host barriers per frame and is opt-in
+    transport = args.transport or "gather"
     shared = None
     if world > 1 and transport == "shared":
         from paper_2005_01442_b200.distributed import SharedFrame
@@ -356,6 +398,8 @@ def run_ours(args):
         for cam in cameras:
             if views > 1:
                 rend.set_camera(cam)
+            if shared is not None:
+                shared.acquire()  # rank 0 is done with the previous frame
             rend.render_async(stream)
             if shared is not None:
                 shared.publish()
@@ -413,9 +457,19 @@ def run_ours(args):
     cubic = settings.interpolation == "tricubic"
     b_sample = 128 if cubic else 16
     b_grad = 768 if cubic else 96
-    # bytes the ray-cast launches of one rank process: its share of the frame
-    algo_bytes = (taken * b_sample + shaded * b_grad + W * H * 4) / world
-    achieved = algo_bytes / kern_s / 1e9
+    # Bytes the ray-cast launches actually gather (one rank's share of the
+    # frame): every interpolation evaluated -- sample interpolations plus the
+    # 6 gradient taps of each shaded sample -- reads its B_s-byte tap
+    # neighbourhood; every march iteration reads its block's 32-byte skip
+    # record; every pixel writes 4 bytes.  Culled samples (provably
+    # transparent) are counted as taken but read nothing, so the survey's
+    # taken-based model overstates the work; it is kept below
+    # as `survey_model` for comparison.
+    interp = int(st.get("interpolated") or 0)
+    iters = int(st.get("march_iterations") or 0)
+    gathered = ((interp + 6 * shaded) * b_sample + iters * 32 + W * H * 4) / world
+    achieved = gathered / kern_s / 1e9
+    survey_bytes = (taken * b_sample + shaded * b_grad + W * H * 4) / world
     peak, peak_kind = measured_peak()
 
     e2e = None
@@ -476,7 +530,8 @@ def run_ours(args):
         from oracle import oracle as O
 
         values = dvol.download()
-        t, r = cpu_oracle_frame(values, spacing, cameras[0], tf, settings)
+        o_cam, o_tf, o_set = oracle_scene_args(cfg, extent)
+        t, r = cpu_oracle_frame(values, spacing, o_cam, o_tf, o_set)
         cpu = {"value": 1.0 / t, "unit": "frames/s", "cores": O.num_threads(), "kind": "port",
                "sample": f"one full {args.config} frame via oracle.render (C restatement of "
                          "_kernels.march + block prep, OpenMP over pixels)",
@@ -495,17 +550,21 @@ def run_ours(args):
         "samples_per_sec": taken * fps, "samples_taken": taken, "samples_skipped": st["samples_skipped"],
         "shaded_samples": shaded, "interpolated_samples": st.get("interpolated"),
         "march_iterations": st.get("march_iterations"),
-        "config": {"workload": args.config, "desc": cfg["desc"], "volume": list(cfg["dims"]),
-                   "image": [W, H], "views_per_step": views, "tf": cfg["tf"],
-                   "parallelism": (f"sort-first x{world} ({args.dist_backend}, {transport})" if world > 1
-                                   else "single GPU"),
-                   "l2": "flushed between steps (512 MiB write, then 512 MiB read)"},
+        "config": bench_config(args, cfg),
+        "parallelism": (f"sort-first x{world} ({args.dist_backend}, {transport})" if world > 1
+                        else "single GPU"),
+        "l2": "flushed between steps (512 MiB write, then 512 MiB read)",
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "peak_source": peak_kind,
                      "traffic": committed_traffic(args.config),
                      "kernel": "raycast_post_kernel + raycast_heavy_kernel (one vr_render launch pair)",
                      "kernel_ms": kern_s * 1e3,
-                     "bytes_model": f"taken*{b_sample} + shaded*{b_grad} + W*H*4 per launch"},
+                     "bytes_model": (f"gathered: (interpolations + 6*shaded)*{b_sample} + iterations*32 "
+                                     "+ W*H*4 per launch (taps mostly served from L1; see profiles/ "
+                                     "for DRAM bytes and issue utilisation)"),
+                     "survey_model": {"bytes": survey_bytes, "achieved": survey_bytes / kern_s / 1e9,
+                                      "formula": f"taken*{b_sample} + shaded*{b_grad} + W*H*4 (SURVEY 8(d))"},
+                     "ncu": committed_ncu(args.config)},
         "clocks": clocks.summary(),
         "gpu_launches": (launches_per_frame(settings) * views + (2 if measure else 0)) * args.steps,
         "e2e": e2e,

@@ -36,6 +36,28 @@ PREINT_BINS = 256
 PREINT_SUBSTEPS = 64
 SKIP_MARGIN = {"trilinear": 2.0, "tricubic": 3.0}  # render.py:53
 
+# transfer.py:207-228 presets as (value, r, g, b, a) control points over the
+# CT domain (-1000, 2000): the oracle's own copy, so the CPU baseline and the
+# tests never need the product package for their inputs.
+CT_DOMAIN = (-1000.0, 2000.0)
+PRESET_POINTS = {
+    "bone": [(-1000.0, 0, 0, 0, 0.0), (550.0, .40, .28, .16, 0.0), (800.0, .85, .78, .62, .70),
+             (1400.0, .98, .96, .90, .95), (2000.0, 1, 1, 1, 1.0)],
+    "soft-tissue": [(-1000.0, 0, 0, 0, 0.0), (-350.0, .55, .25, .15, 0.0), (-50.0, .70, .40, .30, .05),
+                    (100.0, .80, .45, .35, .12), (500.0, .90, .80, .70, .40),
+                    (900.0, .98, .95, .90, .85), (2000.0, 1, 1, 1, .95)],
+    "grayscale": [(-1000.0, 0, 0, 0, 0.0), (2000.0, 1, 1, 1, 1.0)],
+}
+
+
+def preset_arrays(name: str):
+    """(values, rgba, domain) of a preset TF (transfer.py:207-228)."""
+    pts = PRESET_POINTS[name]
+    v = np.array([p[0] for p in pts], dtype=np.float64)
+    c = np.array([p[1:] for p in pts], dtype=np.float64)
+    return v, c, CT_DOMAIN
+
+
 _lib = None
 
 

@@ -15,6 +15,33 @@
 #include "vr_prep.cuh"
 #include "vr_raycast.cuh"
 
+// Hand-off policy of the persistent ray casters.  Compile-time constants, so
+// no environment variable can change the production path; A/B builds pass
+// -D overrides (tools/variants.sh, _build.py defines).
+//   VR_HEAVY_LONG       rays with >= this many samples left go to the long
+//                       queue the cooperative kernel drains first (sweep
+//                       128..512: 384 best, tools/gpu_sweep_long.sh)
+//   VR_HEAVY_MIN_LEFT   rays with fewer samples left stay in the per-lane
+//                       kernel (0..512 sweep at C2/C3: 64 best; 0 = no hand-off)
+//   VR_HEAVY_AFTER      hand off after this many trips even before the queue drains
+//   VR_HEAVY_VIS        hand off dense lit rays after this many composited samples
+//   VR_HEAVY_VIS_ALPHA  ... while their opacity is still below this
+#ifndef VR_HEAVY_LONG
+#define VR_HEAVY_LONG 384
+#endif
+#ifndef VR_HEAVY_MIN_LEFT
+#define VR_HEAVY_MIN_LEFT 64
+#endif
+#ifndef VR_HEAVY_AFTER
+#define VR_HEAVY_AFTER (1 << 30)
+#endif
+#ifndef VR_HEAVY_VIS
+#define VR_HEAVY_VIS 4
+#endif
+#ifndef VR_HEAVY_VIS_ALPHA
+#define VR_HEAVY_VIS_ALPHA 0.5
+#endif
+
 struct vr_volume {
     int device;
     int64_t nx, ny, nz;
@@ -684,26 +711,19 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         // the cooperative kernel (sweep 128..512: C3 +5 %, C2 +5 % over one
         // queue; 384 vs 256 after the first-trip hand-off rule: C3 +1.4 %,
         // C2/C4 within noise, tools/gpu_sweep_long.sh)
-        const char *hl = getenv("VR_HEAVY_LONG");
-        a.heavy_long = hl ? atoll(hl) : 384;
+        a.heavy_long = VR_HEAVY_LONG;
         const long long items = (long long)a.slots * vr::kTileW * vr::kTileH;
         a.heavy_cap = items < (1LL << 20) ? items : (1LL << 20);
-        // development knob: VR_HEAVY_MIN_LEFT (default 64, the best of a
-        // 0..512 sweep at C2/C3; 0 disables the hand-off)
-        const char *hm = getenv("VR_HEAVY_MIN_LEFT");
-        a.heavy_min_left = hm ? atoll(hm) : 64;
-        const char *ha = getenv("VR_HEAVY_AFTER");
-        a.heavy_after = ha ? atoi(ha) : 1 << 30;
+        a.heavy_min_left = VR_HEAVY_MIN_LEFT;
+        a.heavy_after = VR_HEAVY_AFTER;
         // Dense rays (4 composited samples) go to the cooperative kernel at
         // once when it can save work on them: with lighting and early
         // termination it computes gradients only up to the terminating
         // sample (C3-soft 94 -> 145 fps; C1/C2/C3 unchanged, sweep 2..32).
         // Without, its in-order composite of a fully visible chunk is serial
         // and the per-lane kernel is faster (C3-stress 21 vs 12 fps).
-        const char *hva = getenv("VR_HEAVY_VIS_ALPHA");
-        a.heavy_vis_alpha = hva ? atof(hva) : 0.5;
-        const char *hv = getenv("VR_HEAVY_VIS");
-        a.heavy_vis = hv ? atoi(hv) : (prm->lighting && prm->term_alpha < 1.0 ? 4 : 1 << 30);
+        a.heavy_vis_alpha = VR_HEAVY_VIS_ALPHA;
+        a.heavy_vis = prm->lighting && prm->term_alpha < 1.0 ? VR_HEAVY_VIS : 1 << 30;
         if (a.heavy_min_left > 0) {
             VR_CUDA(heavy.alloc(2 * (size_t)a.heavy_cap * vr::kHeavyRayBytes));  // short + long queue
             a.heavy = heavy.p;
@@ -712,11 +732,18 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.ncx = vol->ncx;
         a.ncy = vol->ncy;
         a.cull = 1;
-        // per-cube bounds behind the cell bounds (development knob VR_NO_CUBES=1 disables)
-        const char *nw = getenv("VR_NO_CUBES");
-        a.cubes = (nw && atoi(nw)) ? nullptr : vol->cubes;
-        const char *nm = getenv("VR_NO_MACRO");  // development knob: 1 disables the 16^3 level
-        a.mcells = (nm && atoi(nm)) ? nullptr : vol->mcells;
+        // per-cube bounds and the 16^3 macro level behind the cell bounds
+        // (compile with -DVR_NO_CUBES / -DVR_NO_MACRO for A/B builds)
+#ifdef VR_NO_CUBES
+        a.cubes = nullptr;
+#else
+        a.cubes = vol->cubes;
+#endif
+#ifdef VR_NO_MACRO
+        a.mcells = nullptr;
+#else
+        a.mcells = vol->mcells;
+#endif
         a.nmx = vol->nmx;
         a.nmy = vol->nmy;
     }

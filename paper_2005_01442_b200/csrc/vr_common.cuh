@@ -42,16 +42,14 @@ VR_D void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Launch with the programmatic-serialisation attribute (VR_NO_PDL=1: plain
-// stream order, for A/B).  Only kernels that begin with pdl_enter() may be
-// launched this way.
-inline bool pdl_enabled() {
-    static const bool on = [] {
-        const char *e = getenv("VR_NO_PDL");
-        return !(e && atoi(e));
-    }();
-    return on;
-}
+// Launch with the programmatic-serialisation attribute (build with
+// -DVR_NO_PDL for plain stream order, A/B).  Only kernels that begin with
+// pdl_enter() may be launched this way.
+#ifdef VR_NO_PDL
+constexpr int kPdl = 0;
+#else
+constexpr int kPdl = 1;
+#endif
 template <typename... P, typename... A>
 cudaError_t launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A &&...args) {
     cudaLaunchConfig_t cfg = {};
@@ -61,11 +59,15 @@ cudaError_t launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cuda
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = kPdl;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
 }
+
+// SM count of the current device, queried once per device (grids of the
+// persistent and grid-stride kernels are sized from it).
+int device_sms();
 
 // Python's max(a, 0.0)
 VR_HD double pymax0(double a) { return (0.0 > a) ? 0.0 : a; }

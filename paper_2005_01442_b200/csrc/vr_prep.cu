@@ -26,7 +26,9 @@ VR_D unsigned long long warp_sum(unsigned long long v) {
     return v;
 }
 
-int grid_for(long long n, int block, int cap = 148 * 16) {
+// grid of a grid-stride kernel: one thread per item, at most `per_sm` CTAs per SM
+int grid_for(long long n, int block, int per_sm = 16) {
+    const long long cap = (long long)device_sms() * per_sm;
     long long g = (n + block - 1) / block;
     if (g < 1) g = 1;
     return (int)(g < cap ? g : cap);
@@ -880,7 +882,7 @@ cudaError_t launch_phantom(int kind, int nx, int ny, int nz, int16_t *out, cudaS
         p.r_out = 0.80 * p.radius;
     }
     long long n = (long long)nx * ny * nz;
-    phantom_kernel<<<grid_for(n, kBlock, 148 * 64), kBlock, 0, s>>>(p, out);
+    phantom_kernel<<<grid_for(n, kBlock, 64), kBlock, 0, s>>>(p, out);
     return cudaGetLastError();
 }
 
@@ -908,11 +910,10 @@ cudaError_t launch_visibility(const int16_t *bricks, const Layout &L, const VisA
     if (e != cudaSuccess) return e;
     e = launch_pdl(vis_setup_kernel, 1, kSetupThreads, smem, s, v);
     if (e != cudaSuccess) return e;
-    static int per_sm = [] {
-        const char *e = getenv("VR_AABB_CTAS");  // CTAs per SM (experiments)
-        return e && atoi(e) > 0 ? atoi(e) : 8;
-    }();
-    e = launch_pdl(aabb_kernel, 148 * per_sm, kAabbThreads, 0, s, bricks, L, v, zsplit_for(L));
+#ifndef VR_AABB_CTAS
+#define VR_AABB_CTAS 8  // CTAs per SM (swept 2..16)
+#endif
+    e = launch_pdl(aabb_kernel, device_sms() * VR_AABB_CTAS, kAabbThreads, 0, s, bricks, L, v, zsplit_for(L));
     if (e != cudaSuccess) return e;
     e = launch_pdl(box_kernel, (v.nblocks + 127) / 128, 128, 0, s, L, v);
     if (e != cudaSuccess) return e;
@@ -922,7 +923,7 @@ cudaError_t launch_visibility(const int16_t *bricks, const Layout &L, const VisA
 cudaError_t launch_brick_volume(const int16_t *vol, int nx, int ny, int nz, int16_t *bricks, cudaStream_t s) {
     int bnx = (nx + 3) / 4, bny = (ny + 3) / 4, bnz = (nz + 3) / 4;
     long long total = (long long)bnx * bny * bnz * 64;
-    brick_kernel<<<grid_for(total, kBlock, 148 * 64), kBlock, 0, s>>>(vol, nx, ny, nz, bnx, bny, total, bricks);
+    brick_kernel<<<grid_for(total, kBlock, 64), kBlock, 0, s>>>(vol, nx, ny, nz, bnx, bny, total, bricks);
     return cudaGetLastError();
 }
 
@@ -952,9 +953,9 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
     dim3 grid((nx + kCubeTile - 1) / kCubeTile, (ny + kCubeTile - 1) / kCubeTile, (nz + kCubeTile - 1) / kCubeTile);
     cube_bound_kernel<<<grid, 512, 0, s>>>(vol, nx, ny, nz, bnx, bny, cubes);
     const long long nc = (long long)ncx * ncy * ncz;
-    cell_from_cubes_kernel<<<grid_for(nc, kBlock, 148 * 32), kBlock, 0, s>>>(cubes, nx, ny, nz, ncx, ncy, ncz, cells);
+    cell_from_cubes_kernel<<<grid_for(nc, kBlock, 32), kBlock, 0, s>>>(cubes, nx, ny, nz, ncx, ncy, ncz, cells);
     const long long nm = (long long)nmx * nmy * nmz;
-    macro_from_cells_kernel<<<grid_for(nm, kBlock, 148 * 32), kBlock, 0, s>>>(cells, ncx, ncy, ncz, nmx, nmy, nmz,
+    macro_from_cells_kernel<<<grid_for(nm, kBlock, 32), kBlock, 0, s>>>(cells, ncx, ncy, ncz, nmx, nmy, nmz,
                                                                              mcells);
     return cudaGetLastError();
 }
@@ -975,7 +976,7 @@ cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *ou
 
 cudaError_t launch_preclassify(const int16_t *vol, long long n, const double *lut, int nbins, double lut_lo,
                                double bin_width, uint8_t *rgba, cudaStream_t s) {
-    preclassify_kernel<<<grid_for(n, kBlock, 148 * 64), kBlock, 0, s>>>(vol, n, lut, nbins, lut_lo, bin_width, rgba);
+    preclassify_kernel<<<grid_for(n, kBlock, 64), kBlock, 0, s>>>(vol, n, lut, nbins, lut_lo, bin_width, rgba);
     return cudaGetLastError();
 }
 
@@ -990,14 +991,14 @@ cudaError_t launch_sample_points(const int16_t *vol, int nx, int ny, int nz, con
 
 cudaError_t launch_threshold_count(const int16_t *vol, long long n, int thr, unsigned long long *count,
                                    cudaStream_t s) {
-    threshold_kernel<<<grid_for(n / 8 + 1, kBlock, 148 * 8), kBlock, 0, s>>>(vol, n, thr, count);
+    threshold_kernel<<<grid_for(n / 8 + 1, kBlock, 8), kBlock, 0, s>>>(vol, n, thr, count);
     return cudaGetLastError();
 }
 
 cudaError_t launch_ingest(const void *src, int format, long long nxy, int nz, const double *calib,
                           int16_t *out, unsigned long long *clamped, cudaStream_t s) {
     const long long n = nxy * nz;
-    const int grid = grid_for(n, kBlock, 148 * 16);
+    const int grid = grid_for(n, kBlock, 16);
     if (format == kFormatU8)
         ingest_kernel<<<grid, kBlock, 0, s>>>(static_cast<const uint8_t *>(src), nxy, n, calib, out, clamped);
     else if (format == kFormatI16)

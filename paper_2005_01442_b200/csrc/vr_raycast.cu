@@ -859,8 +859,8 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
         // ---- once the ray queue has drained, hand long rays to the
         // warp-cooperative kernel (at a clean point, nothing pending): the
         // frame would otherwise end with a few warps finishing grazing rays
-        // of ~700 samples while every other SM idles
-                // A ray fetched as the queue drains first gets one trip here: most
+        // of ~700 samples while every other SM idles.
+        // A ray fetched as the queue drains first gets one trip here: most
         // rays end (or pass their long empty stretch) within it, cheaper than
         // a hand-off record and a warp's fetch (C3 +3 %, C2 +4 %).  A frame
         // with fewer rays than this kernel has lanes hands them over at once:
@@ -971,7 +971,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
                 }
             }
             const double v = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
-            ++c_eval;
+            c_eval += R.stage == 0;  // sample interpolations (gradient taps: 6 per shaded sample)
             bool composite = false;
             if (R.stage == 0) {
                 const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
@@ -1449,39 +1449,32 @@ KernelFn pick_cubic(bool cubic, bool light, bool skip) {
     return cubic ? pick_light<KIND, true>(light, skip) : pick_light<KIND, false>(light, skip);
 }
 
-// Resident CTAs per SM of a persistent kernel, and the device's SM count:
-// queried once and cached (two runtime queries per frame were host time on
-// the end-to-end path).  Reentrant callers share the cache under a lock.
+// Resident CTAs per SM of a persistent kernel on the current device, queried
+// once per (device, kernel) and cached (two runtime queries per frame were
+// host time on the end-to-end path).  Reentrant callers share the cache
+// under a lock.
+std::mutex g_occ_mu;
+
 int persistent_ctas_per_sm(KernelFn k) {
-    static std::mutex mu;
-    static KernelFn keys[32];
-    static int vals[32];
+    static int keys_dev[64];
+    static KernelFn keys[64];
+    static int vals[64];
     static int n = 0;
-    std::lock_guard<std::mutex> g(mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(g_occ_mu);
     for (int i = 0; i < n; ++i)
-        if (keys[i] == k) return vals[i];
+        if (keys[i] == k && keys_dev[i] == dev) return vals[i];
     int per_sm = 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kPersistThreads, 0) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    if (n < 32) {
+    if (n < 64) {
+        keys_dev[n] = dev;
         keys[n] = k;
         vals[n] = per_sm;
         ++n;
     }
     return per_sm;
-}
-
-int device_sms() {
-    static int sms[64] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) dev = 0;
-    if (sms[dev] == 0) {
-        int v = 148;
-        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        sms[dev] = v;
-    }
-    return sms[dev];
 }
 
 KernelFn pick(const RenderArgs &a) {
@@ -1495,6 +1488,23 @@ KernelFn pick(const RenderArgs &a) {
 }
 
 }  // namespace
+
+int device_sms() {
+    static int sms[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    std::lock_guard<std::mutex> g(g_occ_mu);
+    if (sms[dev] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1) {
+            cudaGetLastError();
+            v = 148;  // B200
+        }
+        sms[dev] = v;
+    }
+    return sms[dev];
+}
 
 cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
     if (a.tw <= 0 || a.th <= 0) return cudaSuccess;

@@ -129,6 +129,15 @@ class SharedFrame:
             if owner != dev:
                 _lib.check(_lib.load().vr_enable_peer_access(dev, owner))
 
+    def acquire(self):
+        """Collective, before a frame's stores: rank 0 has finished reading the
+        previous frame (its ``frame.cpu()`` returned before it entered this
+        barrier), so no rank's next-frame stores can overwrite cells rank 0 is
+        still copying (write-after-read across frames)."""
+        import torch.distributed as dist
+
+        dist.barrier(group=self.group)
+
     def publish(self):
         """Every rank's stores into the frame are complete and visible to rank 0."""
         import torch
@@ -138,37 +147,92 @@ class SharedFrame:
         dist.barrier(group=self.group)
 
 
+class ShardedRenderer:
+    """One rank's share of sort-first multi-GPU rendering, kept across frames:
+    the volume, block grid, LUT and output buffers stay resident (one
+    ``Renderer`` per rank), so a frame is one camera update plus one
+    ``vr_render`` call -- no allocation and no table upload per frame.
+
+    ``render_async(camera)`` enqueues the frame on the current stream.  With
+    the NCCL gather (``shared=None``) the exchange is stream-ordered as well:
+    ``gather_async()`` enqueues ``dist.gather`` of the packed cells and the
+    unpack on rank 0, and nothing in the frame waits on the host.  With a
+    ``SharedFrame`` the cells land in rank 0's frame directly; ``gather_async()`` then
+    publishes it and ``render_async`` first waits until rank 0 has read the
+    previous frame (host barriers: the CUDA-IPC transport's only ordering).
+    """
+
+    def __init__(self, volume, camera, tf, settings, *, group=None, device=None,
+                 shared: SharedFrame | None = None):
+        import torch
+        import torch.distributed as dist
+
+        from .render import Renderer
+
+        self.group = group
+        self.n = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.k = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = torch.cuda.current_device() if device is None else device
+        self.shared = shared if self.n > 1 else None
+        self.width, self.height = camera.width, camera.height
+        self.renderer = Renderer(volume, camera, tf, settings, device=self.device,
+                                 interleave=(self.n, self.k) if self.n > 1 else None,
+                                 frame_out=self.shared.frame if self.shared is not None else None)
+
+    def render_async(self, camera=None):
+        if camera is not None:
+            if (camera.width, camera.height) != (self.width, self.height):
+                raise ValueError("ShardedRenderer: camera size differs from the one it was built for")
+            self.renderer.set_camera(camera)
+        if self.shared is not None:
+            self.shared.acquire()
+        self.renderer.render_async()
+
+    def gather_async(self):
+        """Stream-ordered exchange: rank 0 gets the (H, W, 4) device frame."""
+        if self.shared is not None:
+            self.shared.publish()
+            return self.shared.frame if self.k == 0 else None
+        if self.n == 1:
+            return self.renderer.pixels
+        return gather_frame(self.renderer.pixels.reshape(-1, 4), self.width, self.height, self.group)
+
+    def stats(self):
+        """[samples_taken, samples_skipped] summed over ranks (synchronising)."""
+        import torch.distributed as dist
+
+        totals = self.renderer.totals[:2].clone()
+        if self.n > 1:
+            if dist.get_backend(self.group) == "gloo":
+                totals = totals.cpu()
+            dist.all_reduce(totals, group=self.group)
+        return totals.cpu().tolist()
+
+
+_SHARDED: dict = {}
+
+
 def render_sharded(volume, camera, tf, settings, *, group=None, device=None, shared: SharedFrame | None = None):
     """Multi-GPU render of one frame: every rank calls this with the same
     arguments; rank 0 returns the (H, W, 4) uint8 frame as a host array and
     the summed stats, other ranks return (None, stats).  With ``shared`` (a
     SharedFrame of the frame's size) the cells are stored straight into rank
-    0's frame instead of gathered."""
+    0's frame instead of gathered.  The per-rank renderer is cached across
+    calls for the same volume, TF, settings, frame size and transport."""
     import torch
-    import torch.distributed as dist
 
-    from .render import Renderer
-
-    n = dist.get_world_size(group) if dist.is_initialized() else 1
-    k = dist.get_rank(group) if dist.is_initialized() else 0
     dev = torch.cuda.current_device() if device is None else device
-    frame_out = shared.frame if (shared is not None and n > 1) else None
-    r = Renderer(volume, camera, tf, settings, device=dev, interleave=(n, k) if n > 1 else None,
-                 frame_out=frame_out)
-    r.render_async()
-    totals = r.totals[:2].clone()
-    if n > 1:
-        if dist.get_backend(group) == "gloo":
-            totals = totals.cpu()
-        dist.all_reduce(totals, group=group)
-        if shared is not None:
-            shared.publish()
-            frame = shared.frame if k == 0 else None
-        else:
-            frame = gather_frame(r.pixels.reshape(-1, 4), camera.width, camera.height, group)
-    else:
-        frame = r.pixels
-    stats = totals.cpu().tolist()
+    key = (id(volume), id(tf), settings, camera.width, camera.height, id(group), dev, id(shared))
+    sr = _SHARDED.get(key)
+    if sr is None or sr[0] is not volume or sr[1] is not tf:
+        if len(_SHARDED) > 8:
+            _SHARDED.clear()
+        sr = (volume, tf, ShardedRenderer(volume, camera, tf, settings, group=group, device=dev, shared=shared))
+        _SHARDED[key] = sr
+    r = sr[2]
+    r.render_async(camera)
+    frame = r.gather_async()
+    stats = r.stats()
     if frame is None:
         return None, stats
     return frame.cpu().numpy(), stats

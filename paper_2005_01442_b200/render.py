@@ -352,6 +352,91 @@ def _resolve(volume_spacing, value_range, tf: TransferFunction, settings: Render
     return _Resolved(p, lut, table)
 
 
+# ---------------------------------------------------- reference-typed inputs
+# render() is a drop-in for voxelray.render.render: its callers (service.py:68-88
+# prepare_render, store.py:131-143, quality.py:98-101) hand it the REFERENCE's
+# own objects -- voxelray.volume.ScalarVolume, voxelray.blocks.BlockGrid,
+# voxelray.render.Camera / RenderSettings, voxelray.transfer.TransferFunction.
+# These adapters accept anything carrying the reference's attributes.
+
+_foreign_volumes: dict = {}
+
+
+def as_volume(obj) -> ScalarVolume:
+    """A ScalarVolume for any object with the reference's ``values`` (int16
+    (nz, ny, nx)), ``spacing`` and optional ``value_range`` / ``clamp_count``
+    (volume.py:23-71).  The wrapper -- and with it the device upload and block
+    grids -- is cached per source object for as long as that object lives, as
+    the reference's store caches volumes by id (store.py:62-67)."""
+    if isinstance(obj, ScalarVolume):
+        return obj
+    if not (hasattr(obj, "values") and hasattr(obj, "spacing")):
+        raise TypeError(f"render target must be a volume or a block grid, got {type(obj).__name__}")
+    hit = _foreign_volumes.get(id(obj))
+    if hit is not None and hit[0]() is obj:
+        return hit[1]
+    vals = np.ascontiguousarray(obj.values, dtype=np.int16)
+    vr_ = getattr(obj, "value_range", None)
+    value_range = (int(vr_[0]), int(vr_[1])) if vr_ is not None else (int(vals.min()), int(vals.max()))
+    sv = ScalarVolume(vals, tuple(float(x) for x in obj.spacing), value_range,
+                      int(getattr(obj, "clamp_count", 0) or 0))
+    try:
+        ref = weakref.ref(obj, lambda _r, k=id(obj): _foreign_volumes.pop(k, None))
+    except TypeError:  # not weak-referenceable: no caching
+        return sv
+    _foreign_volumes[id(obj)] = (ref, sv)
+    return sv
+
+
+def as_camera(cam):
+    """The camera itself when it is one of ours; otherwise a Camera (pinhole,
+    render.py:56-95) or OrthographicCamera built from the reference's
+    attributes (position, look_at, up, vertical_fov_deg, width, height)."""
+    if isinstance(cam, (Camera, OrthographicCamera)):
+        return cam
+    up = tuple(getattr(cam, "up", (0.0, 0.0, 1.0)))
+    if getattr(cam, "projection", "pinhole") == "orthographic":
+        return OrthographicCamera(position=tuple(cam.position), look_at=tuple(cam.look_at), up=up,
+                                  half_height_mm=float(cam.half_height_mm), width=int(cam.width),
+                                  height=int(cam.height))
+    return Camera(position=tuple(cam.position), look_at=tuple(cam.look_at), up=up,
+                  vertical_fov_deg=float(getattr(cam, "vertical_fov_deg", 30.0)), width=int(cam.width),
+                  height=int(cam.height))
+
+
+def as_settings(settings) -> "RenderSettings":
+    """RenderSettings from any object with the reference's fields (render.py:159-181)."""
+    if isinstance(settings, RenderSettings):
+        return settings
+    kw = {}
+    for f in RenderSettings.__dataclass_fields__:
+        if hasattr(settings, f):
+            kw[f] = getattr(settings, f)
+    if kw.get("background") is not None:
+        kw["background"] = tuple(kw["background"])
+    return RenderSettings(**kw)
+
+
+def as_transfer(tf) -> TransferFunction:
+    """TransferFunction from any object with ``values``, ``rgba`` and ``domain``
+    (transfer.py:28-62); ours pass through."""
+    if isinstance(tf, TransferFunction):
+        return tf
+    hit = _foreign_tfs.get(id(tf))
+    if hit is not None and hit[0]() is tf:
+        return hit[1]
+    ours = TransferFunction(np.array(tf.values, dtype=np.float64), np.array(tf.rgba, dtype=np.float64),
+                            (float(tf.domain[0]), float(tf.domain[1])))
+    try:
+        _foreign_tfs[id(tf)] = (weakref.ref(tf, lambda _r, k=id(tf): _foreign_tfs.pop(k, None)), ours)
+    except TypeError:
+        pass
+    return ours
+
+
+_foreign_tfs: dict = {}
+
+
 def camera_struct(camera, tile=None, interleave=None) -> _lib.Camera:
     """C camera for the frame or the sub-rectangle tile=(x0, y0, w, h);
     interleave=(n, k) renders the k-th of n sort-first cell sets."""
@@ -388,13 +473,18 @@ def render(target, camera, tf: TransferFunction, settings: RenderSettings = Rend
     crop of the full render).  return_premultiplied attaches the
     float64 premultiplied buffer as ``image.premultiplied`` (parity checks).
     """
-    settings.validate()
     t_start = time.perf_counter()
-    if isinstance(target, BlockGrid):
-        grid, volume, use_blocks = target, target.volume, True
-        block_size, overlap = target.block_size, target.overlap
+    settings = as_settings(settings)
+    settings.validate()
+    camera = as_camera(camera)
+    tf = as_transfer(tf)
+    if isinstance(target, BlockGrid) or (not hasattr(target, "values") and hasattr(target, "block_size")):
+        # ours, or the reference's BlockGrid (blocks.py:73-97): only its volume
+        # and layout are used -- visibility is recomputed from the LUT per frame
+        grid, volume, use_blocks = target, as_volume(target.volume), True
+        block_size, overlap = int(target.block_size), int(target.overlap)
     else:
-        volume, grid, use_blocks = target, None, settings.use_blocks
+        volume, grid, use_blocks = as_volume(target), None, settings.use_blocks
         block_size, overlap = settings.block_size, settings.overlap
         if use_blocks:
             from .blocks import _check_spec
@@ -438,7 +528,11 @@ class Renderer:
                  per_pixel_counts: bool = False, time_kernel: bool = False, frame_out=None):
         import torch
 
+        settings = as_settings(settings)
         settings.validate()
+        tf = as_transfer(tf)
+        if not isinstance(volume, DeviceVolume):
+            volume = as_volume(volume)
         self.torch = torch
         self.device = torch.device("cuda", device)
         if isinstance(volume, DeviceVolume):
@@ -513,6 +607,7 @@ class Renderer:
 
     def set_camera(self, camera, tile=None):
         """Point at a new view (same rectangle size); buffers are reused."""
+        camera = as_camera(camera)
         self.camera = camera
         self.cam = camera_struct(camera, tile, self.interleave)
         if getattr(self, "frame_out", None) is not None:

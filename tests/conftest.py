@@ -48,14 +48,7 @@ def golden_sampling():
     return dict(np.load(GOLDEN / "sampling.npz"))
 
 
-PRESET_POINTS = {
-    "bone": [(-1000.0, 0, 0, 0, 0.0), (550.0, .40, .28, .16, 0.0), (800.0, .85, .78, .62, .70),
-             (1400.0, .98, .96, .90, .95), (2000.0, 1, 1, 1, 1.0)],
-    "soft-tissue": [(-1000.0, 0, 0, 0, 0.0), (-350.0, .55, .25, .15, 0.0), (-50.0, .70, .40, .30, .05),
-                    (100.0, .80, .45, .35, .12), (500.0, .90, .80, .70, .40),
-                    (900.0, .98, .95, .90, .85), (2000.0, 1, 1, 1, .95)],
-    "grayscale": [(-1000.0, 0, 0, 0, 0.0), (2000.0, 1, 1, 1, 1.0)],
-}
+from oracle.oracle import PRESET_POINTS  # noqa: E402  (transfer.py:207-228)
 
 
 def tf_arrays(spec):

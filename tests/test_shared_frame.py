@@ -45,6 +45,13 @@ def test_interleaved_cells_at_frame_positions(n):
     assert taken == vr.render(vol, cam, tf, st).stats.samples_taken
 
 
+def _other_view(vr, vol, cam):
+    ext = vol.extent_mm
+    c = tuple(0.5 * e for e in ext)
+    return vr.Camera(position=(c[0], c[1] - 2.2 * max(ext), c[2] + 9.0), look_at=c, width=cam.width,
+                     height=cam.height)
+
+
 def _worker(rank, world, port, out):
     import torch
     import torch.distributed as dist
@@ -59,9 +66,12 @@ def _worker(rank, world, port, out):
     vol, cam, tf, st = _scene(vr)
     shared = SharedFrame(cam.height, cam.width)
     frame, stats = render_sharded(vol, cam, tf, st, shared=shared)
-    frame2, _ = render_sharded(vol, cam, tf, st, shared=shared)  # reuse across frames
+    # a different view straight after: the peers' stores of frame 2 must not
+    # land in rank 0's frame before rank 0 has read frame 1 (write-after-read)
+    frame2, _ = render_sharded(vol, _other_view(vr, vol, cam), tf, st, shared=shared)
+    frame3, _ = render_sharded(vol, cam, tf, st, shared=shared)
     if rank == 0:
-        np.save(out, np.stack([frame, frame2]))
+        np.save(out, np.stack([frame, frame2, frame3]))
         np.save(out + ".stats.npy", np.array(stats, dtype=np.int64))
     dist.barrier()
     dist.destroy_process_group()
@@ -82,6 +92,7 @@ def test_two_processes_store_into_rank0_frame(tmp_path):
     ref = vr.render(vol, cam, tf, st)
     frames = np.load(out)
     np.testing.assert_array_equal(frames[0], ref.pixels)
-    np.testing.assert_array_equal(frames[1], ref.pixels)
+    np.testing.assert_array_equal(frames[1], vr.render(vol, _other_view(vr, vol, cam), tf, st).pixels)
+    np.testing.assert_array_equal(frames[2], ref.pixels)
     stats = np.load(out + ".stats.npy")
     assert int(stats[0]) == ref.stats.samples_taken and int(stats[1]) == ref.stats.samples_skipped
