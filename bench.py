@@ -392,7 +392,7 @@ def run_ours(args):
         rng = np.random.default_rng(0)
         centres = torch.from_numpy(rng.uniform(0.2, 0.8, size=(measure["balls"], 3)) * np.array(extent)).to(dev)
         radii = torch.full((measure["balls"],), float(measure["radius"]), dtype=torch.float64, device=dev)
-        k4 = torch.zeros(1 + 4 * measure["balls"], dtype=torch.int64, device=dev)
+        k4 = torch.zeros(2 + 2 * measure["balls"], dtype=torch.int64, device=dev)
 
     def frame():
         for cam in cameras:
@@ -407,13 +407,12 @@ def run_ours(args):
                 packed = rend.pixels.reshape(-1, 4)
                 gather_frame(packed if args.dist_backend == "nccl" else packed.cpu(), W, H)
         if measure:
-            k4[:1].zero_()
             s = _lib.ptr_stream(stream)
-            _lib.check(L.vr_threshold_count(dvol.handle, int(measure["threshold"]), _lib.ptr(k4), s))
+            _lib.check(L.vr_threshold_measure(dvol.handle, int(measure["threshold"]), _lib.ptr(k4), s))
             nb = measure["balls"]
-            _lib.check(L.vr_ball_counts(dvol.handle, int(measure["threshold"]), _lib.ptr(centres), _lib.ptr(radii),
-                                        nb, ctypes.c_void_p(k4.data_ptr() + 8),
-                                        ctypes.c_void_p(k4.data_ptr() + 8 + 8 * nb), s))
+            _lib.check(L.vr_ball_measure(dvol.handle, int(measure["threshold"]), _lib.ptr(centres), _lib.ptr(radii),
+                                         nb, ctypes.c_void_p(k4.data_ptr() + 16),
+                                         ctypes.c_void_p(k4.data_ptr() + 16 + 8 * nb), s))
 
     for _ in range(max(args.warmup, 3)):
         frame()

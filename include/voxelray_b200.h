@@ -240,18 +240,26 @@ int vr_gradient_points(const vr_volume *vol, const double *pts, int64_t n, int c
 /* Number of voxels with value >= thr (builder-defined, no
  * reference function).  count: device uint64 (accumulated; zero it first). */
 int vr_threshold_count(const vr_volume *vol, int32_t thr, uint64_t *count, void *stream);
-/* Method-of-spheres voxel form: for each ball q (centre
- * mm, radius mm), the member voxels -- value >= thr and centre
- * (i*sx, j*sy, k*sz) with ((dx^2 + dy^2) + dz^2) <= r^2 -- are counted, and
- * their exposed faces (6-neighbour below thr or outside the volume) per
- * axis: faces[3q+0] x-faces (area sy*sz each), [3q+1] y-faces (sx*sz),
- * [3q+2] z-faces (sx*sy).  V = count * sx*sy*sz, S = sum of face areas,
- * SVR = S / V.  centres (nballs,3), radii (nballs) device float64;
- * counts (nballs) and faces (nballs*3) device uint64, overwritten; faces may
- * be NULL. */
-int vr_ball_counts(const vr_volume *vol, int32_t thr, const double *centres,
-                   const double *radii, int64_t nballs, uint64_t *counts, uint64_t *faces,
-                   void *stream);
+/* The method of spheres on the voxel grid.  Replaces the
+ * reference's mesh estimators morphology.py:70-143 clipped_area (S),
+ * :238-267 clipped_volume (V) and :270-306 svr_at_point (SVR = S/V) for a CT
+ * volume thresholded at thr:
+ *   V = (voxels with value >= thr [and centre (i*sx, j*sy, k*sz) in the closed
+ *       ball, ((dx^2 + dy^2) + dz^2) <= r^2]) * sx*sy*sz;
+ *   S = area (mm^2) of the isosurface at level thr - 0.5 of the piecewise-
+ *       linear interpolant over the 6 Kuhn tetrahedra of every cell (cells
+ *       between voxel centres, the volume padded with -32768 so the surface
+ *       closes at its border) [polygons with vertex centroid in the ball],
+ *       each polygon rounded to a multiple of 2^-24 mm^2: area_fx = S * 2^24
+ *       as an exact integer sum.
+ * vr_threshold_measure: out[0] = count, out[1] = area_fx for the whole volume
+ * (device uint64[2], overwritten).  vr_ball_measure: per ball q (centres
+ * (nballs,3) mm, radii (nballs) mm, device float64) counts[q] and, unless
+ * area_fx is NULL, area_fx[q] (device uint64, overwritten).  Asynchronous. */
+#define VR_AREA_SCALE 16777216.0 /* 2^24 */
+int vr_threshold_measure(const vr_volume *vol, int32_t thr, uint64_t *out, void *stream);
+int vr_ball_measure(const vr_volume *vol, int32_t thr, const double *centres, const double *radii,
+                    int64_t nballs, uint64_t *counts, uint64_t *area_fx, void *stream);
 
 /* Let kernels running on `device` read and write `peer`'s memory (NVLink P2P),
  * e.g. a frame of rank 0 mapped into another rank with interleave_frame = 1.

@@ -95,7 +95,9 @@ def lib():
         L.vro_build_atlas.argtypes = [P, i64, i64, i64, P, P, i64, P, P, i64, P, P, i64, P, P]
         L.vro_threshold_count.argtypes = [P, i64, ctypes.c_int32]
         L.vro_threshold_count.restype = ctypes.c_uint64
-        L.vro_ball_counts.argtypes = [P, i64, i64, i64, f64, f64, f64, ctypes.c_int32, P, P, i64, P, P]
+        L.vro_ball_counts.argtypes = [P, i64, i64, i64, f64, f64, f64, ctypes.c_int32, P, P, i64, P]
+        L.vro_threshold_measure.argtypes = [P, i64, i64, i64, f64, f64, f64, ctypes.c_int32, P]
+        L.vro_ball_measure.argtypes = [P, i64, i64, i64, f64, f64, f64, ctypes.c_int32, P, P, i64, P, P]
         L.vro_sample_points.argtypes = [P, i64, i64, i64, P, i64, i32, P]
         L.vro_gradient_points.argtypes = [P, i64, i64, i64, P, i64, i32, f64, f64, f64, P]
         L.vro_num_threads.restype = i32
@@ -544,16 +546,43 @@ def threshold_count(values_zyx, thr: int) -> int:
     return int(lib().vro_threshold_count(_p(vals), vals.size, int(thr)))
 
 
-def ball_counts(values_zyx, spacing, thr: int, centres, radii, with_faces: bool = False):
-    """K4 ball form (parity unpinned): voxels >= thr inside each closed ball,
-    and (with_faces) their exposed faces per axis, shape (nballs, 3)."""
+AREA_SCALE = float(1 << 24)  # vr_oracle.c VRO_AREA_SCALE
+
+
+def ball_counts(values_zyx, spacing, thr: int, centres, radii):
+    """K4 ball form (parity unpinned): voxels >= thr with centre in each closed ball."""
     vals = np.ascontiguousarray(values_zyx, dtype=np.int16)
     nz, ny, nx = vals.shape
     centres = np.ascontiguousarray(centres, dtype=np.float64).reshape(-1, 3)
     radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
     counts = np.empty(centres.shape[0], dtype=np.uint64)
-    faces = np.empty((centres.shape[0], 3), dtype=np.uint64)
     sx, sy, sz = spacing
     lib().vro_ball_counts(_p(vals), nx, ny, nz, float(sx), float(sy), float(sz), int(thr),
-                          _p(centres), _p(radii), centres.shape[0], _p(counts), _p(faces))
-    return (counts, faces) if with_faces else counts
+                          _p(centres), _p(radii), centres.shape[0], _p(counts))
+    return counts
+
+
+def threshold_measure(values_zyx, spacing, thr: int):
+    """K4 whole volume: (voxels >= thr, isosurface area * 2^24) as ints
+    (marching tetrahedra at thr - 0.5, vr_oracle.c)."""
+    vals = np.ascontiguousarray(values_zyx, dtype=np.int16)
+    nz, ny, nx = vals.shape
+    out = np.zeros(2, dtype=np.uint64)
+    sx, sy, sz = spacing
+    lib().vro_threshold_measure(_p(vals), nx, ny, nz, float(sx), float(sy), float(sz), int(thr), _p(out))
+    return int(out[0]), int(out[1])
+
+
+def ball_measure(values_zyx, spacing, thr: int, centres, radii):
+    """K4 per ball: (counts, area * 2^24) uint64 arrays -- V = count * voxel
+    volume, S = area / 2^24 mm^2 of the isosurface with centroid in the ball."""
+    vals = np.ascontiguousarray(values_zyx, dtype=np.int16)
+    nz, ny, nx = vals.shape
+    centres = np.ascontiguousarray(centres, dtype=np.float64).reshape(-1, 3)
+    radii = np.ascontiguousarray(radii, dtype=np.float64).reshape(-1)
+    counts = np.empty(centres.shape[0], dtype=np.uint64)
+    area = np.empty(centres.shape[0], dtype=np.uint64)
+    sx, sy, sz = spacing
+    lib().vro_ball_measure(_p(vals), nx, ny, nz, float(sx), float(sy), float(sz), int(thr),
+                           _p(centres), _p(radii), centres.shape[0], _p(counts), _p(area))
+    return counts, area

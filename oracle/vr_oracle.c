@@ -28,8 +28,11 @@
  *   blocks.py:161-220   cull_empty/fit_bounding_box/with_visibility -> vro_visibility
  *   blocks.py:269-294   build_atlas         -> vro_build_atlas
  *   phantoms.py:76-111  torso phantom       (numpy restatement lives in oracle.py)
- *   K4 (no reference function): vro_threshold_count / vro_ball_counts,
- *   semantics from SPEC.md:457-465 and morphology.py:238-267 -- parity unpinned.
+ *   K4 (no voxel function in the reference): vro_threshold_count,
+ *   vro_ball_counts, vro_threshold_measure, vro_ball_measure -- S and V of the
+ *   method of spheres (morphology.py:70-306)
+ *   restated on the voxel grid; parity unpinned (no reference function), the
+ *   semantics pinned by the analytic oracles of SPEC.md:472-473 instead.
  */
 #include <math.h>
 #include <stdint.h>
@@ -227,6 +230,38 @@ static inline int64_t lut_bin(double s, double lo, double inv_w, int64_t nbins) 
     return clampi((int64_t)((s - lo) * inv_w), 0, nbins - 1);
 }
 
+#ifdef VRO_CR_POW
+/* Diagnostics build only (never the oracle proper): x^n for integer n as a
+ * double-double ladder rounded once, i.e. a correctly rounded power, to tell
+ * glibc pow's <= 0.52-ulp rounding apart from other differences. */
+static double vro_pow(double x, double y) {
+    if (y != floor(y) || y < 0 || y > 4096) return pow(x, y);
+    int n = (int)y;
+    double rh = 1.0, rl = 0.0, bh = x, bl = 0.0;
+    while (n > 0) {
+        if (n & 1) {
+            double p = rh * bh, e = fma(rh, bh, -p);
+            e += rh * bl + rl * bh;
+            double s = p + e, bb = s - p;
+            rl = (p - (s - bb)) + (e - bb);
+            rh = s;
+        }
+        n >>= 1;
+        if (n) {
+            double p = bh * bh, e = fma(bh, bh, -p);
+            e += 2.0 * bh * bl;
+            double s = p + e, bb = s - p;
+            bl = (p - (s - bb)) + (e - bb);
+            bh = s;
+        }
+    }
+    return rh + rl;
+}
+#define SHADE_POW vro_pow
+#else
+#define SHADE_POW pow
+#endif
+
 /* _kernels.py:195-208 */
 static inline void shade(double *r, double *g, double *b, double nx, double ny, double nz,
                          double lx, double ly, double lz, double ka, double kd, double ks,
@@ -234,7 +269,7 @@ static inline void shade(double *r, double *g, double *b, double nx, double ny, 
     double ndl = (nx * lx + ny * ly) + nz * lz;
     double diff = kd * pymax0(ndl);
     double rv = 2.0 * ndl * ndl - 1.0;
-    double spec = ks * pow(pymax0(rv), shininess);
+    double spec = ks * SHADE_POW(pymax0(rv), shininess);
     *r = clampf(*r * (ka + diff) + spec, 0.0, 1.0);
     *g = clampf(*g * (ka + diff) + spec, 0.0, 1.0);
     *b = clampf(*b * (ka + diff) + spec, 0.0, 1.0);
@@ -749,12 +784,11 @@ uint64_t vro_threshold_count(const int16_t *vals, int64_t n, int32_t thr) {
  * ((dx^2 + dy^2) + dz^2) in float64. */
 void vro_ball_counts(const int16_t *vals, int64_t nx, int64_t ny, int64_t nz, double sx,
                      double sy, double sz, int32_t thr, const double *centres,
-                     const double *radii, int64_t nballs, uint64_t *counts, uint64_t *faces) {
-    const int64_t py = nx, pz = nx * ny;
+                     const double *radii, int64_t nballs, uint64_t *counts) {
     for (int64_t q = 0; q < nballs; ++q) {
         double cx = centres[3 * q], cy = centres[3 * q + 1], cz = centres[3 * q + 2];
         double r2 = radii[q] * radii[q];
-        uint64_t c = 0, f[3] = {0, 0, 0};
+        uint64_t c = 0;
         for (int64_t k = 0; k < nz; ++k) {
             double dz = (double)k * sz - cz;
             for (int64_t j = 0; j < ny; ++j) {
@@ -762,21 +796,162 @@ void vro_ball_counts(const int16_t *vals, int64_t nx, int64_t ny, int64_t nz, do
                 const int16_t *row = vals + (k * ny + j) * nx;
                 for (int64_t i = 0; i < nx; ++i) {
                     double dx = (double)i * sx - cx;
-                    if (!(row[i] >= thr && (dx * dx + dy * dy) + dz * dz <= r2)) continue;
-                    c++;
-                    const int16_t *p = row + i;
-                    /* exposed faces: neighbour below thr or outside the volume */
-                    f[0] += (i == 0 || p[-1] < thr) + (i == nx - 1 || p[1] < thr);
-                    f[1] += (j == 0 || p[-py] < thr) + (j == ny - 1 || p[py] < thr);
-                    f[2] += (k == 0 || p[-pz] < thr) + (k == nz - 1 || p[pz] < thr);
+                    c += (row[i] >= thr && (dx * dx + dy * dy) + dz * dz <= r2);
                 }
             }
         }
         counts[q] = c;
-        if (faces) {
-            faces[3 * q] = f[0];
-            faces[3 * q + 1] = f[1];
-            faces[3 * q + 2] = f[2];
+    }
+}
+
+/* K4 surface S of the method of spheres (the reference
+ * measures it on triangle meshes, morphology.py:70-143 clipped_area).  On the
+ * voxel grid the object {v >= thr} is bounded by the isosurface of the
+ * trilinear-by-tetrahedra interpolant at level L = thr - 0.5 (integer voxels:
+ * v >= thr <=> v > L, so the surface separates exactly the voxels V counts):
+ *  - cells are the unit cubes between voxel centres, padded by one cell on
+ *    every side with the outside value -32768 (the surface closes at the
+ *    volume border);
+ *  - each cell is split into the 6 Kuhn tetrahedra 000 -> e_a -> e_a+e_b -> 111
+ *    (a, b, c a permutation of x, y, z; face-consistent between cells);
+ *  - in a tetrahedron the linear interpolant's level set is a triangle (one
+ *    corner inside or outside) or a planar quad (two and two), its vertices
+ *    at t = f_in / (f_in - f_out) from the inside corner (f = v - L);
+ *  - S sums the polygon areas (mm^2; corners at index * spacing), each rounded
+ *    to a multiple of 2^-24 mm^2 so the sum is exact and order-free; the ball
+ *    form keeps the polygons whose vertex centroid lies in the closed ball.
+ * Bit-exactness with the CUDA kernel: same operations, same order, no FMA. */
+#define VRO_AREA_SCALE 16777216.0 /* 2^24 */
+
+static const int KUHN[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+
+static inline double field_at(const int16_t *vals, int64_t nx, int64_t ny, int64_t nz, int64_t i, int64_t j,
+                              int64_t k, double level) {
+    if (i < 0 || j < 0 || k < 0 || i >= nx || j >= ny || k >= nz) return -32768.0 - level;
+    return (double)vals[(k * ny + j) * nx + i] - level;
+}
+
+static inline void edge_point(const double *P, const double *Q, double fp, double fq, double *out) {
+    double t = fp / (fp - fq);
+    out[0] = P[0] + t * (Q[0] - P[0]);
+    out[1] = P[1] + t * (Q[1] - P[1]);
+    out[2] = P[2] + t * (Q[2] - P[2]);
+}
+
+static inline double cross_half_norm(double ux, double uy, double uz, double wx, double wy, double wz) {
+    double cx = uy * wz - uz * wy;
+    double cy = uz * wx - ux * wz;
+    double cz = ux * wy - uy * wx;
+    return 0.5 * sqrt((cx * cx + cy * cy) + cz * cz);
+}
+
+/* area (fixed point) of the cell's surface polygons; ball == NULL keeps all */
+static uint64_t cell_area_fx(const double f[8], const double P[8][3], const double *ball, double r2) {
+    uint64_t acc = 0;
+    for (int t = 0; t < 6; ++t) {
+        int v[4];
+        v[0] = 0;
+        v[1] = 1 << KUHN[t][0];
+        v[2] = v[1] | (1 << KUHN[t][1]);
+        v[3] = 7;
+        int in[4], out[4], ni = 0, no = 0;
+        for (int c = 0; c < 4; ++c) {
+            if (f[v[c]] > 0.0) in[ni++] = v[c];
+            else out[no++] = v[c];
         }
+        if (ni == 0 || no == 0) continue;
+        double a[3], b[3], c3[3], d[3], area, gx, gy, gz;
+        if (ni == 1 || no == 1) {
+            if (ni == 1) {
+                edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
+                edge_point(P[in[0]], P[out[1]], f[in[0]], f[out[1]], b);
+                edge_point(P[in[0]], P[out[2]], f[in[0]], f[out[2]], c3);
+            } else {
+                edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
+                edge_point(P[in[1]], P[out[0]], f[in[1]], f[out[0]], b);
+                edge_point(P[in[2]], P[out[0]], f[in[2]], f[out[0]], c3);
+            }
+            area = cross_half_norm(b[0] - a[0], b[1] - a[1], b[2] - a[2], c3[0] - a[0], c3[1] - a[1], c3[2] - a[2]);
+            gx = ((a[0] + b[0]) + c3[0]) / 3.0;
+            gy = ((a[1] + b[1]) + c3[1]) / 3.0;
+            gz = ((a[2] + b[2]) + c3[2]) / 3.0;
+        } else {
+            /* quad a=(i0,o0) b=(i0,o1) c=(i1,o1) d=(i1,o0): a cycle, planar */
+            edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
+            edge_point(P[in[0]], P[out[1]], f[in[0]], f[out[1]], b);
+            edge_point(P[in[1]], P[out[1]], f[in[1]], f[out[1]], c3);
+            edge_point(P[in[1]], P[out[0]], f[in[1]], f[out[0]], d);
+            area = cross_half_norm(c3[0] - a[0], c3[1] - a[1], c3[2] - a[2], d[0] - b[0], d[1] - b[1], d[2] - b[2]);
+            gx = (((a[0] + b[0]) + c3[0]) + d[0]) * 0.25;
+            gy = (((a[1] + b[1]) + c3[1]) + d[1]) * 0.25;
+            gz = (((a[2] + b[2]) + c3[2]) + d[2]) * 0.25;
+        }
+        if (ball) {
+            double dx = gx - ball[0], dy = gy - ball[1], dz = gz - ball[2];
+            if (!((dx * dx + dy * dy) + dz * dz <= r2)) continue;
+        }
+        acc += (uint64_t)llrint(area * VRO_AREA_SCALE);
+    }
+    return acc;
+}
+
+static uint64_t cell_at(const int16_t *vals, int64_t nx, int64_t ny, int64_t nz, double sx, double sy,
+                        double sz, double level, int64_t i, int64_t j, int64_t k, const double *ball,
+                        double r2) {
+    double f[8], P[8][3];
+    int any_in = 0, any_out = 0;
+    for (int c = 0; c < 8; ++c) {
+        int64_t a = i + (c & 1), b = j + ((c >> 1) & 1), e = k + ((c >> 2) & 1);
+        f[c] = field_at(vals, nx, ny, nz, a, b, e, level);
+        P[c][0] = (double)a * sx;
+        P[c][1] = (double)b * sy;
+        P[c][2] = (double)e * sz;
+        if (f[c] > 0.0) any_in = 1; else any_out = 1;
+    }
+    if (!any_in || !any_out) return 0;
+    return cell_area_fx(f, P, ball, r2);
+}
+
+/* whole volume: out[0] = voxels >= thr, out[1] = surface area * 2^24 */
+void vro_threshold_measure(const int16_t *vals, int64_t nx, int64_t ny, int64_t nz, double sx, double sy,
+                           double sz, int32_t thr, uint64_t *out) {
+    const double level = (double)thr - 0.5;
+    uint64_t area = 0;
+#pragma omp parallel for reduction(+ : area) schedule(dynamic, 1)
+    for (int64_t k = -1; k < nz; ++k)
+        for (int64_t j = -1; j < ny; ++j)
+            for (int64_t i = -1; i < nx; ++i) area += cell_at(vals, nx, ny, nz, sx, sy, sz, level, i, j, k, NULL, 0.0);
+    uint64_t c = 0;
+    for (int64_t i = 0; i < nx * ny * nz; ++i) c += (vals[i] >= thr);
+    out[0] = c;
+    out[1] = area;
+}
+
+/* per ball: counts[q] = voxels >= thr with centre in the ball (vro_ball_counts),
+ * area[q] = surface inside the ball * 2^24 (cells of the ball's bounding box
+ * widened by one cell; the centroid test decides) */
+void vro_ball_measure(const int16_t *vals, int64_t nx, int64_t ny, int64_t nz, double sx, double sy, double sz,
+                      int32_t thr, const double *centres, const double *radii, int64_t nballs, uint64_t *counts,
+                      uint64_t *area) {
+    const double level = (double)thr - 0.5;
+    vro_ball_counts(vals, nx, ny, nz, sx, sy, sz, thr, centres, radii, nballs, counts);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t q = 0; q < nballs; ++q) {
+        const double *c = centres + 3 * q;
+        double rad = radii[q], r2 = rad * rad;
+        int64_t i0 = (int64_t)floor((c[0] - rad) / sx) - 1, i1 = (int64_t)ceil((c[0] + rad) / sx) + 1;
+        int64_t j0 = (int64_t)floor((c[1] - rad) / sy) - 1, j1 = (int64_t)ceil((c[1] + rad) / sy) + 1;
+        int64_t k0 = (int64_t)floor((c[2] - rad) / sz) - 1, k1 = (int64_t)ceil((c[2] + rad) / sz) + 1;
+        if (i0 < -1) i0 = -1;
+        if (j0 < -1) j0 = -1;
+        if (k0 < -1) k0 = -1;
+        if (i1 > nx - 1) i1 = nx - 1;
+        if (j1 > ny - 1) j1 = ny - 1;
+        if (k1 > nz - 1) k1 = nz - 1;
+        uint64_t a = 0;
+        for (int64_t k = k0; k <= k1; ++k)
+            for (int64_t j = j0; j <= j1; ++j)
+                for (int64_t i = i0; i <= i1; ++i) a += cell_at(vals, nx, ny, nz, sx, sy, sz, level, i, j, k, c, r2);
+        area[q] = a;
     }
 }

@@ -22,7 +22,7 @@ from .errors import (
     VoxelrayError,
 )
 from .ingest import DeviceVolumeCache, assemble_volume_device, ingest_raw, volume_id
-from .measure import ball_counts, ball_measure, threshold_count, threshold_volume_mm3
+from .measure import ball_counts, ball_measure, threshold_count, threshold_measure, threshold_volume_mm3
 from .phantoms import PHANTOM_NAMES, device_phantom, generate_phantom
 from .quality import convergence_study, psnr, ssim
 from .render import (

@@ -30,7 +30,8 @@ EXPORTS = (
     "vr_volume_destroy", "vr_volume_culling_tables", "vr_volume_info", "vr_volume_data", "vr_volume_download",
     "vr_grid_create", "vr_grid_destroy", "vr_grid_shape", "vr_grid_minmax",
     "vr_grid_visibility", "vr_render", "vr_render_to_host", "vr_preclassify",
-    "vr_sample_points", "vr_gradient_points", "vr_threshold_count", "vr_ball_counts",
+    "vr_sample_points", "vr_gradient_points", "vr_threshold_count", "vr_threshold_measure",
+    "vr_ball_measure",
     "vr_event_create", "vr_event_destroy", "vr_event_elapsed_ms", "vr_interleave_size",
     "vr_image_sse", "vr_image_ssim", "vr_enable_peer_access",
 )
@@ -111,7 +112,8 @@ def load() -> ctypes.CDLL:
         "vr_sample_points": ([P, P, i64, ctypes.c_int, P, P], ctypes.c_int),
         "vr_gradient_points": ([P, P, i64, ctypes.c_int, P, P], ctypes.c_int),
         "vr_threshold_count": ([P, i32, P, P], ctypes.c_int),
-        "vr_ball_counts": ([P, i32, P, P, i64, P, P, P], ctypes.c_int),
+        "vr_threshold_measure": ([P, i32, P, P], ctypes.c_int),
+        "vr_ball_measure": ([P, i32, P, P, i64, P, P, P], ctypes.c_int),
         "vr_event_create": ([VP], ctypes.c_int),
         "vr_event_destroy": ([P], ctypes.c_int),
         "vr_event_elapsed_ms": ([P, P, ctypes.POINTER(ctypes.c_float)], ctypes.c_int),

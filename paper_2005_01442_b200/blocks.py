@@ -29,6 +29,10 @@ DEFAULT_BLOCK_SIZE = 64
 DEFAULT_OVERLAP = 3
 
 
+def _destroy_grid(L, h, _volume):
+    L.vr_grid_destroy(h)
+
+
 class DeviceGrid:
     """``vr_grid`` handle: layout + per-block int32 min/max in HBM."""
 
@@ -41,7 +45,9 @@ class DeviceGrid:
         shape = (ctypes.c_int64 * 3)()
         _lib.check(L.vr_grid_shape(h, shape))
         self.shape = tuple(int(s) for s in shape)
-        self._finalizer = weakref.finalize(self, L.vr_grid_destroy, h)
+        # the finalizer holds the volume: its handle outlives the grid's even
+        # when both are collected in one cycle
+        self._finalizer = weakref.finalize(self, _destroy_grid, L, h, dvol)
 
     @property
     def handle(self):

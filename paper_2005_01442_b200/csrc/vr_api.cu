@@ -68,6 +68,7 @@ static void free_volume(vr_volume *v) {
 
 struct vr_grid {
     vr_volume *vol;
+    int device;  // the volume's device, kept here: destroy must not dereference vol
     int64_t block_size, overlap;
     vr::Layout L;
     int nblocks;
@@ -97,6 +98,9 @@ int cuda_fail(cudaError_t e, const char *where) {
 struct DeviceGuard {
     int prev = -1;
     explicit DeviceGuard(int dev) {
+        // every entry point reports only its own CUDA errors: drop a stale,
+        // non-sticky error some earlier call left in this thread's state
+        cudaGetLastError();
         cudaGetDevice(&prev);
         if (prev != dev) cudaSetDevice(dev);
     }
@@ -428,6 +432,7 @@ int vr_grid_create(vr_volume *vol, int64_t block_size, int64_t overlap, void *st
     int64_t stride = block_size - overlap;
     vr_grid *gr = new vr_grid();
     gr->vol = vol;
+    gr->device = vol->device;
     gr->block_size = block_size;
     gr->overlap = overlap;
     vr::Layout &L = gr->L;
@@ -460,7 +465,7 @@ int vr_grid_create(vr_volume *vol, int64_t block_size, int64_t overlap, void *st
 
 int vr_grid_destroy(vr_grid *gr) {
     if (!gr) return VR_OK;
-    DeviceGuard g(gr->vol->device);
+    DeviceGuard g(gr->device);
     cudaFree(gr->vmin);
     cudaFree(gr->vmax);
     delete gr;
@@ -889,14 +894,22 @@ int vr_threshold_count(const vr_volume *vol, int32_t thr, uint64_t *count, void 
     return VR_OK;
 }
 
-int vr_ball_counts(const vr_volume *vol, int32_t thr, const double *centres, const double *radii, int64_t nballs,
-                   uint64_t *counts, uint64_t *faces, void *stream) {
-    if (!vol || (nballs > 0 && (!centres || !radii || !counts))) return fail(VR_EINVALID, "null pointer");
-    if (nballs > (1 << 30)) return fail(VR_EINVALID, "too many balls");
+int vr_threshold_measure(const vr_volume *vol, int32_t thr, uint64_t *out, void *stream) {
+    if (!vol || !out) return fail(VR_EINVALID, "null pointer");
     DeviceGuard g(vol->device);
-    VR_CUDA(vr::launch_ball_counts(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, vol->sx, vol->sy, vol->sz,
-                                   thr, centres, radii, (int)nballs, (unsigned long long *)counts,
-                                   (unsigned long long *)faces, (cudaStream_t)stream));
+    VR_CUDA(vr::launch_threshold_measure(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, vol->sx, vol->sy,
+                                         vol->sz, thr, (unsigned long long *)out, (cudaStream_t)stream));
+    return VR_OK;
+}
+
+int vr_ball_measure(const vr_volume *vol, int32_t thr, const double *centres, const double *radii, int64_t nballs,
+                    uint64_t *counts, uint64_t *area_fx, void *stream) {
+    if (!vol || (nballs > 0 && (!centres || !radii || !counts))) return fail(VR_EINVALID, "null pointer");
+    if (nballs < 0 || nballs > (1 << 30)) return fail(VR_EINVALID, "ball count out of range");
+    DeviceGuard g(vol->device);
+    VR_CUDA(vr::launch_ball_measure(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, vol->sx, vol->sy, vol->sz,
+                                    thr, centres, radii, (int)nballs, (unsigned long long *)counts,
+                                    (unsigned long long *)area_fx, (cudaStream_t)stream));
     return VR_OK;
 }
 

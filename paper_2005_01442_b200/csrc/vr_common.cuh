@@ -14,6 +14,8 @@
 #include <utility>
 #include <cuda_runtime.h>
 
+#include "vr_glibc_pow.h"
+
 #define VR_HD __host__ __device__ __forceinline__
 #define VR_D __device__ __forceinline__
 
@@ -101,7 +103,6 @@ inline Divisor make_divisor(double s) {
 // path, and the kernels call these from many sites).
 static __device__ __noinline__ double div_rn(double x, double s) { return x / s; }
 static __device__ __noinline__ double floor_div(double a, double s) { return floor(a / s); }
-static __device__ __noinline__ double pow_general(double x, double y) { return pow(x, y); }
 
 VR_D double divide(double x, const Divisor &d) { return d.pow2 ? x * d.inv : div_rn(x, d.s); }
 
@@ -550,80 +551,29 @@ VR_HD int block_extent(const Layout &L, int a, int b) {
     return e < L.bsize ? e : L.bsize;
 }
 
-// ---------------------------------------------------------- exact powers
-// Error-free double-double product (fma is exact; the explicit call is not
-// affected by -fmad=false).
-VR_D void two_prod(double a, double b, double &p, double &e) {
-    p = a * b;
-    e = fma(a, b, -p);
-}
-
-VR_D void two_sum(double a, double b, double &s, double &e) {
-    s = a + b;
-    double bb = s - a;
-    e = (a - (s - bb)) + (b - bb);
-}
-
-// x^n for a non-negative integer n in double-double (about 100 significant
-// bits), rounded once: agrees with a correctly rounded pow (glibc's pow, used
-// by the reference's `**`) except in cases closer to a rounding midpoint
-// than ~2^-95 relative.
-VR_D double pow_int_dd(double x, int n) {
-    double rh = 1.0, rl = 0.0;
-    double bh = x, bl = 0.0;
-    while (n > 0) {
-        if (n & 1) {
-            double p, e;
-            two_prod(rh, bh, p, e);
-            e += rh * bl + rl * bh;
-            two_sum(p, e, rh, rl);
-        }
-        n >>= 1;
-        if (n) {
-            double p, e;
-            two_prod(bh, bh, p, e);
-            e += 2.0 * bh * bl;
-            two_sum(p, e, bh, bl);
-        }
-    }
-    return rh + rl;
-}
-
-// pow(x, y) for the two exponents the reference raises at run time:
-// the opacity correction (1 - a)^(step/ref_step) (_kernels.py:489,519) and
-// the Phong exponent (_kernels.py:204,569).  Integer exponents use the
-// double-double ladder, y == 0.5 is sqrt (correctly rounded, as is a
-// correctly rounded pow), anything else the CUDA pow (<= 2 ulp).
+// ---------------------------------------------------------------- powers
+// pow(x, y) for the exponents the reference raises at run time: the
+// opacity correction (1 - a)^(step/ref_step) (_kernels.py:489,519) and the
+// Phong exponent (_kernels.py:204,569).  The reference's `**` is libm's pow
+// (glibc 2.39), accurate to <= 0.52 ulp but not correctly rounded, so the
+// kernels run glibc's own algorithm on its own tables (vr_glibc_pow.h,
+// checked bit for bit against libm by tools/gen_pow_tables.py).  y == 1 (the
+// default step) is the identity, exactly as libm's pow(x, 1) == x.
 struct PowSpec {
-    int kind;  // 0 identity (y == 1), 1 integer, 2 sqrt, 3 general
-    int n;
+    int kind;  // 0 identity (y == 1), 1 glibc pow
     double y;
 };
 
 inline PowSpec make_pow(double y) {
     PowSpec p;
     p.y = y;
-    p.n = 0;
-    if (y == 1.0) {
-        p.kind = 0;
-    } else if (y >= 0.0 && y <= 4096.0 && y == (double)(int)y) {
-        p.kind = 1;
-        p.n = (int)y;
-    } else if (y == 0.5) {
-        p.kind = 2;
-    } else {
-        p.kind = 3;
-    }
+    p.kind = (y == 1.0) ? 0 : 1;
     return p;
 }
 
-VR_D double vr_pow(double x, const PowSpec &p) {
-    switch (p.kind) {
-        case 0: return x;
-        case 1: return (x == 0.0 && p.n == 0) ? 1.0 : pow_int_dd(x, p.n);
-        case 2: return sqrt(x);
-        default: return pow_general(x, p.y);
-    }
-}
+// out of line: one copy of the ~80-instruction pow serves every call site
+static __device__ __noinline__ double pow_glibc(double x, double y) { return vr_glibc_pow(x, y); }
+
+VR_D double vr_pow(double x, const PowSpec &p) { return p.kind == 0 ? x : pow_glibc(x, p.y); }
 
 }  // namespace vr

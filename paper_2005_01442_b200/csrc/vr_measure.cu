@@ -1,0 +1,349 @@
+// vr_measure.cu -- K4: the paper's "method of spheres" on
+// the voxel grid.  The reference measures S (surface area inside a probe ball)
+// and V (object volume inside it) on triangle meshes by Monte Carlo
+// (/root/reference/pkg/src/voxelray/morphology.py:70-143 clipped_area,
+// :238-267 clipped_volume, :270-306 svr_at_point); it has no voxel form
+// (SURVEY G2).  Here, on the CT volume itself, exactly:
+//
+//  * V: voxels with value >= thr (centre inside the closed ball for the ball
+//    form) -- an integer count, V = count * sx*sy*sz;
+//  * S: area of the isosurface at level L = thr - 0.5 of the piecewise-linear
+//    (Kuhn-tetrahedra) interpolant -- for integer voxels v >= thr <=> v > L, so
+//    the surface separates exactly the voxels V counts.  Cells are the unit
+//    cubes between voxel centres, padded by one cell on every side with the
+//    outside value -32768 (the surface closes at the volume border); each cell
+//    splits into the 6 tetrahedra 000 -> e_a -> e_a+e_b -> 111, in each of
+//    which the level set is a triangle or a planar quad.  Every polygon's area
+//    is rounded to a multiple of 2^-24 mm^2 and summed in 64-bit integers, so
+//    the sum is independent of summation order and bit-exact against the C
+//    restatement (oracle/vr_oracle.c vro_threshold_measure / vro_ball_measure:
+//    same float64 operations, same order, no FMA).  The ball form keeps the
+//    polygons whose vertex centroid lies in the closed ball.
+//
+// Parity of the definition cannot be pinned to a reference function (there is
+// none); tests/test_measure.py pins it to the analytic oracles of
+// SPEC.md:472-473 (flat face SVR -> 3/(2R), enclosed sphere SVR -> 3/a).
+//
+// The whole-volume pass is HBM-bound: each thread owns a run of 8 cells along
+// x, loads its four voxel rows as 16-byte vectors (every voxel row is read by
+// 4 neighbouring cell rows of the same CTA: one DRAM read, three L1/L2 hits),
+// classifies the 32 corner voxels with bit masks and runs the tetrahedra only
+// for cells that straddle the level (a few per cent of the volume).
+#include <cstdint>
+
+#include "vr_common.cuh"
+#include "vr_prep.cuh"
+
+namespace vr {
+namespace {
+
+constexpr int kMeasureThreads = 256;
+constexpr double kAreaScale = 16777216.0;  // 2^24
+
+VR_D void edge_point(const double *P, const double *Q, double fp, double fq, double *out) {
+    const double t = fp / (fp - fq);
+    out[0] = P[0] + t * (Q[0] - P[0]);
+    out[1] = P[1] + t * (Q[1] - P[1]);
+    out[2] = P[2] + t * (Q[2] - P[2]);
+}
+
+VR_D double cross_half_norm(double ux, double uy, double uz, double wx, double wy, double wz) {
+    const double cx = uy * wz - uz * wy;
+    const double cy = uz * wx - ux * wz;
+    const double cz = ux * wy - uy * wx;
+    return 0.5 * sqrt((cx * cx + cy * cy) + cz * cz);
+}
+
+// Fixed-point area of one cell's level-set polygons (corner c = x | y<<1 | z<<2
+// with field f[c] = v - L and position P[c] in mm); BALL keeps only polygons
+// whose centroid lies in the closed ball (bx, by, bz, r2).
+template <bool BALL>
+VR_D unsigned long long cell_area_fx(const double f[8], const double P[8][3], double bx, double by, double bz,
+                                     double r2) {
+    unsigned long long acc = 0;
+#pragma unroll 1
+    for (int t = 0; t < 6; ++t) {
+        // Kuhn permutations (0,1,2),(0,2,1),(1,0,2),(1,2,0),(2,0,1),(2,1,0)
+        const int p0 = t >> 1;
+        const int p1 = (t == 0 || t == 5) ? 1 : ((t == 1 || t == 3) ? 2 : 0);
+        const int v1 = 1 << p0, v2 = v1 | (1 << p1);
+        const int v[4] = {0, v1, v2, 7};
+        int in[4], out[4], ni = 0, no = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (f[v[c]] > 0.0)
+                in[ni++] = v[c];
+            else
+                out[no++] = v[c];
+        }
+        if (ni == 0 || no == 0) continue;
+        double a[3], b[3], c3[3], d[3], area, gx, gy, gz;
+        if (ni == 1 || no == 1) {
+            if (ni == 1) {
+                edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
+                edge_point(P[in[0]], P[out[1]], f[in[0]], f[out[1]], b);
+                edge_point(P[in[0]], P[out[2]], f[in[0]], f[out[2]], c3);
+            } else {
+                edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
+                edge_point(P[in[1]], P[out[0]], f[in[1]], f[out[0]], b);
+                edge_point(P[in[2]], P[out[0]], f[in[2]], f[out[0]], c3);
+            }
+            area = cross_half_norm(b[0] - a[0], b[1] - a[1], b[2] - a[2], c3[0] - a[0], c3[1] - a[1], c3[2] - a[2]);
+            if (BALL) {
+                gx = ((a[0] + b[0]) + c3[0]) / 3.0;
+                gy = ((a[1] + b[1]) + c3[1]) / 3.0;
+                gz = ((a[2] + b[2]) + c3[2]) / 3.0;
+            }
+        } else {
+            // planar quad (in0,out0) (in0,out1) (in1,out1) (in1,out0)
+            edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
+            edge_point(P[in[0]], P[out[1]], f[in[0]], f[out[1]], b);
+            edge_point(P[in[1]], P[out[1]], f[in[1]], f[out[1]], c3);
+            edge_point(P[in[1]], P[out[0]], f[in[1]], f[out[0]], d);
+            area = cross_half_norm(c3[0] - a[0], c3[1] - a[1], c3[2] - a[2], d[0] - b[0], d[1] - b[1], d[2] - b[2]);
+            if (BALL) {
+                gx = (((a[0] + b[0]) + c3[0]) + d[0]) * 0.25;
+                gy = (((a[1] + b[1]) + c3[1]) + d[1]) * 0.25;
+                gz = (((a[2] + b[2]) + c3[2]) + d[2]) * 0.25;
+            }
+        }
+        if (BALL) {
+            const double dx = gx - bx, dy = gy - by, dz = gz - bz;
+            if (!((dx * dx + dy * dy) + dz * dz <= r2)) continue;
+        }
+        acc += (unsigned long long)llrint(area * kAreaScale);
+    }
+    return acc;
+}
+
+VR_D unsigned long long warp_sum64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One CTA-wide sum of (count, area) into out[0..1].
+VR_D void cta_accumulate(unsigned long long c, unsigned long long area, unsigned long long *out_c,
+                         unsigned long long *out_a, bool store) {
+    __shared__ unsigned long long part[2][kMeasureThreads / 32];
+    c = warp_sum64(c);
+    area = warp_sum64(area);
+    if ((threadIdx.x & 31) == 0) {
+        part[0][threadIdx.x >> 5] = c;
+        part[1][threadIdx.x >> 5] = area;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        unsigned long long s = 0;
+        for (int w = 0; w < kMeasureThreads / 32; ++w) s += part[threadIdx.x][w];
+        unsigned long long *dst = threadIdx.x == 0 ? out_c : out_a;
+        if (dst) {
+            if (store)
+                *dst = s;
+            else if (s)
+                atomicAdd(dst, s);
+        }
+    }
+}
+
+// Voxel (x) of a row held as prev (voxel x0-1) + chunk lo/hi (voxels x0..x0+7);
+// position p in 0..8.
+VR_D int row_voxel(int prev, unsigned long long lo, unsigned long long hi, int p) {
+    if (p == 0) return prev;
+    const int s = p - 1;
+    const unsigned long long w = s < 4 ? (lo >> (16 * s)) : (hi >> (16 * (s - 4)));
+    return (int)(short)(w & 0xffffull);
+}
+
+struct MeasureVol {
+    const int16_t *v;
+    int nx, ny, nz;
+    double sx, sy, sz;
+};
+
+// Row (j, k) voxels x0-1 .. x0+7 (out of range: -32768).
+template <bool VEC>
+VR_D void load_row(const MeasureVol &m, int x0, int j, int k, int &prev, unsigned long long &lo,
+                   unsigned long long &hi) {
+    const unsigned long long pad = 0x8000800080008000ull;
+    prev = -32768;
+    lo = hi = pad;
+    if (j < 0 || k < 0 || j >= m.ny || k >= m.nz) return;
+    const int16_t *row = m.v + ((long long)k * m.ny + j) * m.nx;
+    if (x0 > 0) prev = __ldg(row + x0 - 1);
+    if (VEC && x0 + 8 <= m.nx) {
+        const int4 q = __ldg(reinterpret_cast<const int4 *>(row + x0));
+        lo = ((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x;
+        hi = ((unsigned long long)(unsigned)q.w << 32) | (unsigned)q.z;
+        return;
+    }
+    lo = hi = 0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+        const unsigned long long u = (x0 + s < m.nx) ? (unsigned short)__ldg(row + x0 + s) : 0x8000u;
+        if (s < 4)
+            lo |= u << (16 * s);
+        else
+            hi |= u << (16 * (s - 4));
+    }
+}
+
+// inside bits (v >= thr) of the 9 voxels x0-1 .. x0+7 (bit p = voxel x0-1+p)
+VR_D unsigned row_mask(int prev, unsigned long long lo, unsigned long long hi, int thr) {
+    unsigned m = prev >= thr ? 1u : 0u;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        m |= ((int)(short)((lo >> (16 * s)) & 0xffff) >= thr ? 1u : 0u) << (1 + s);
+        m |= ((int)(short)((hi >> (16 * s)) & 0xffff) >= thr ? 1u : 0u) << (5 + s);
+    }
+    return m;
+}
+
+// Whole volume: cells (cx, cy, cz) in [-1, n-1]^3; thread t -> run q of cells
+// x0-1 .. x0+6 (x0 = 8q) of cell row (cy, cz), q fastest so a CTA covers a
+// few neighbouring cell rows of one slab.
+template <bool VEC>
+__global__ void __launch_bounds__(kMeasureThreads) threshold_measure_kernel(MeasureVol m, int thr, int runs,
+                                                                            unsigned long long *out) {
+    const double level = (double)thr - 0.5;
+    const long long total = (long long)runs * (m.ny + 1) * (m.nz + 1);
+    unsigned long long count = 0, area = 0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int q = (int)(t % runs);
+        const long long r = t / runs;
+        const int cy = (int)(r % (m.ny + 1)) - 1, cz = (int)(r / (m.ny + 1)) - 1;
+        const int x0 = 8 * q;
+        int pv[4];
+        unsigned long long lo[4], hi[4];
+        unsigned mk[4];
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+            load_row<VEC>(m, x0, cy + (rr & 1), cz + (rr >> 1), pv[rr], lo[rr], hi[rr]);
+            mk[rr] = row_mask(pv[rr], lo[rr], hi[rr], thr);
+        }
+        // V: the row (cy, cz) of voxels x0 .. x0+7, counted once (as the lower
+        // row of its cell row); padding voxels are never inside
+        if (cy >= 0 && cz >= 0 && x0 < m.nx) {
+            const int nvalid = m.nx - x0 < 8 ? m.nx - x0 : 8;
+            count += (unsigned long long)__popc((mk[0] >> 1) & ((1u << nvalid) - 1u));
+        }
+        const unsigned all = mk[0] & mk[1] & mk[2] & mk[3];
+        const unsigned any = mk[0] | mk[1] | mk[2] | mk[3];
+        unsigned straddle = ((any | (any >> 1)) & ~(all & (all >> 1))) & 0xffu;
+        while (straddle) {
+            const int b = __ffs(straddle) - 1;  // cell x0-1+b, corners at row positions b, b+1
+            straddle &= straddle - 1;
+            const int cx = x0 - 1 + b;
+            double f[8], P[8][3];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int rr = (c >> 1);  // (y, z) bits -> row index y | z<<1
+                const int p = b + (c & 1);
+                f[c] = (double)row_voxel(pv[rr], lo[rr], hi[rr], p) - level;
+                P[c][0] = (double)(cx + (c & 1)) * m.sx;
+                P[c][1] = (double)(cy + ((c >> 1) & 1)) * m.sy;
+                P[c][2] = (double)(cz + ((c >> 2) & 1)) * m.sz;
+            }
+            area += cell_area_fx<false>(f, P, 0.0, 0.0, 0.0, 0.0);
+        }
+    }
+    cta_accumulate(count, area, out, out + 1, false);
+}
+
+VR_D int voxel_or_pad(const MeasureVol &m, int i, int j, int k) {
+    if (i < 0 || j < 0 || k < 0 || i >= m.nx || j >= m.ny || k >= m.nz) return -32768;
+    return __ldg(m.v + ((long long)k * m.ny + j) * m.nx + i);
+}
+
+// first / last cell index of a ball's bounding box, clamped to [-1, n-1] in
+// floating point first (no overflow for balls far outside the volume)
+VR_D int box_lo(double lo_mm, double s) {
+    const double v = floor(lo_mm / s) - 1.0;
+    return v < -1.0 ? -1 : (v > 2.0e9 ? 2000000000 : (int)v);
+}
+VR_D int box_hi(double hi_mm, double s, int n) {
+    const double v = ceil(hi_mm / s) + 1.0;
+    return v > (double)(n - 1) ? n - 1 : (v < -2.0e9 ? -2000000000 : (int)v);
+}
+
+// One CTA per ball: the cells of the ball's bounding box (one cell of slack),
+// each contributing its polygons with centroid in the ball and -- for cells
+// at non-negative indices -- its base voxel when that voxel's centre is in
+// the ball and its value >= thr.
+__global__ void __launch_bounds__(kMeasureThreads) ball_measure_kernel(MeasureVol m, int thr, const double *centres,
+                                                                       const double *radii,
+                                                                       unsigned long long *counts,
+                                                                       unsigned long long *areas) {
+    const int q = blockIdx.x;
+    const double cx = centres[3 * q], cy = centres[3 * q + 1], cz = centres[3 * q + 2];
+    const double rad = radii[q];
+    const double r2 = rad * rad;
+    const double level = (double)thr - 0.5;
+    // bounding box as vro_ball_measure computes it (floor/ceil of a true division)
+    // (any superset of the contributing cells gives the same sums: the
+    // centroid and voxel-centre tests decide)
+    const int i0 = box_lo(cx - rad, m.sx), i1 = box_hi(cx + rad, m.sx, m.nx);
+    const int j0 = box_lo(cy - rad, m.sy), j1 = box_hi(cy + rad, m.sy, m.ny);
+    const int k0 = box_lo(cz - rad, m.sz), k1 = box_hi(cz + rad, m.sz, m.nz);
+    unsigned long long count = 0, area = 0;
+    if (i0 <= i1 && j0 <= j1 && k0 <= k1) {
+        const int wx = i1 - i0 + 1, wy = j1 - j0 + 1;
+        const long long n = (long long)wx * wy * (k1 - k0 + 1);
+        for (long long t = threadIdx.x; t < n; t += blockDim.x) {
+            const int i = i0 + (int)(t % wx);
+            const long long r = t / wx;
+            const int j = j0 + (int)(r % wy), k = k0 + (int)(r / wy);
+            double f[8], P[8][3];
+            bool any_in = false, any_out = false;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int a = i + (c & 1), b = j + ((c >> 1) & 1), e = k + ((c >> 2) & 1);
+                f[c] = (double)voxel_or_pad(m, a, b, e) - level;
+                P[c][0] = (double)a * m.sx;
+                P[c][1] = (double)b * m.sy;
+                P[c][2] = (double)e * m.sz;
+                if (f[c] > 0.0) any_in = true; else any_out = true;
+            }
+            if (i >= 0 && j >= 0 && k >= 0 && f[0] > 0.0) {
+                // the cell's base voxel (i, j, k): centre in the closed ball (vro_ball_counts)
+                const double dx = (double)i * m.sx - cx, dy = (double)j * m.sy - cy, dz = (double)k * m.sz - cz;
+                count += ((dx * dx + dy * dy) + dz * dz <= r2) ? 1 : 0;
+            }
+            if (any_in && any_out) area += cell_area_fx<true>(f, P, cx, cy, cz, r2);
+        }
+    }
+    cta_accumulate(count, area, counts + q, areas ? areas + q : nullptr, true);
+}
+
+}  // namespace
+
+cudaError_t launch_threshold_measure(const int16_t *vol, int nx, int ny, int nz, double sx, double sy, double sz,
+                                     int thr, unsigned long long *out, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    MeasureVol m{vol, nx, ny, nz, sx, sy, sz};
+    const int runs = (nx + 1 + 7) / 8;  // cells -1 .. nx-1 in runs of 8
+    const long long total = (long long)runs * (ny + 1) * (nz + 1);
+    long long grid = (total + kMeasureThreads - 1) / kMeasureThreads;
+    const long long cap = (long long)device_sms() * 8;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    const bool vec = (nx % 8) == 0 && (reinterpret_cast<uintptr_t>(vol) & 15) == 0;
+    if (vec)
+        threshold_measure_kernel<true><<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, thr, runs, out);
+    else
+        threshold_measure_kernel<false><<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, thr, runs, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ball_measure(const int16_t *vol, int nx, int ny, int nz, double sx, double sy, double sz, int thr,
+                                const double *centres, const double *radii, int nballs, unsigned long long *counts,
+                                unsigned long long *areas, cudaStream_t s) {
+    if (nballs <= 0) return cudaSuccess;
+    MeasureVol m{vol, nx, ny, nz, sx, sy, sz};
+    ball_measure_kernel<<<nballs, kMeasureThreads, 0, s>>>(m, thr, centres, radii, counts, areas);
+    return cudaGetLastError();
+}
+
+}  // namespace vr

@@ -773,64 +773,6 @@ __global__ void __launch_bounds__(kBlock) ingest_kernel(const T *__restrict__ sr
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(clamped, c);
 }
 
-// one CTA per ball; voxels of the ball's bounding box, exact membership test
-__global__ void __launch_bounds__(kBlock) ball_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
-                                                      double sx, double sy, double sz, int thr,
-                                                      const double *centres, const double *radii,
-                                                      unsigned long long *counts, unsigned long long *faces) {
-    int q = blockIdx.x;
-    double cx = centres[3 * q], cy = centres[3 * q + 1], cz = centres[3 * q + 2];
-    double rad = radii[q];
-    double r2 = rad * rad;
-    // conservative index bounds (one voxel of slack each side)
-    int i0 = max(0, (int)floor((cx - rad) / sx) - 1), i1 = min(nx - 1, (int)ceil((cx + rad) / sx) + 1);
-    int j0 = max(0, (int)floor((cy - rad) / sy) - 1), j1 = min(ny - 1, (int)ceil((cy + rad) / sy) + 1);
-    int k0 = max(0, (int)floor((cz - rad) / sz) - 1), k1 = min(nz - 1, (int)ceil((cz + rad) / sz) + 1);
-    unsigned long long c = 0, fx = 0, fy = 0, fz = 0;
-    if (i0 <= i1 && j0 <= j1 && k0 <= k1) {
-        int wx = i1 - i0 + 1, wy = j1 - j0 + 1;
-        long long cnt = (long long)wx * wy * (k1 - k0 + 1);
-        long long py = nx, pz = (long long)nx * ny;
-        for (long long t = threadIdx.x; t < cnt; t += blockDim.x) {
-            int i = i0 + (int)(t % wx);
-            long long r = t / wx;
-            int j = j0 + (int)(r % wy);
-            int k = k0 + (int)(r / wy);
-            double dx = (double)i * sx - cx, dy = (double)j * sy - cy, dz = (double)k * sz - cz;
-            if ((dx * dx + dy * dy) + dz * dz > r2) continue;
-            const int16_t *p = vol + k * pz + j * py + i;
-            if (__ldg(p) < thr) continue;
-            c += 1;
-            if (faces) {
-                // exposed faces: 6-neighbour below thr or outside the volume
-                fx += ((i == 0 || __ldg(p - 1) < thr) ? 1 : 0) + ((i == nx - 1 || __ldg(p + 1) < thr) ? 1 : 0);
-                fy += ((j == 0 || __ldg(p - py) < thr) ? 1 : 0) + ((j == ny - 1 || __ldg(p + py) < thr) ? 1 : 0);
-                fz += ((k == 0 || __ldg(p - pz) < thr) ? 1 : 0) + ((k == nz - 1 || __ldg(p + pz) < thr) ? 1 : 0);
-            }
-        }
-    }
-    c = warp_sum(c);
-    fx = warp_sum(fx);
-    fy = warp_sum(fy);
-    fz = warp_sum(fz);
-    __shared__ unsigned long long part[4][kBlock / 32];
-    if ((threadIdx.x & 31) == 0) {
-        part[0][threadIdx.x >> 5] = c;
-        part[1][threadIdx.x >> 5] = fx;
-        part[2][threadIdx.x >> 5] = fy;
-        part[3][threadIdx.x >> 5] = fz;
-    }
-    __syncthreads();
-    if (threadIdx.x < 4) {
-        unsigned long long s = 0;
-        for (int w = 0; w < kBlock / 32; ++w) s += part[threadIdx.x][w];
-        if (threadIdx.x == 0)
-            counts[q] = s;
-        else if (faces)
-            faces[3 * q + threadIdx.x - 1] = s;
-    }
-}
-
 }  // namespace
 
 cudaError_t launch_value_range(const int16_t *vol, long long n, int *out, cudaStream_t s) {
@@ -1010,12 +952,5 @@ cudaError_t launch_ingest(const void *src, int format, long long nxy, int nz, co
     return cudaGetLastError();
 }
 
-cudaError_t launch_ball_counts(const int16_t *vol, int nx, int ny, int nz, double sx, double sy, double sz,
-                               int thr, const double *centres, const double *radii, int nballs,
-                               unsigned long long *counts, unsigned long long *faces, cudaStream_t s) {
-    if (nballs <= 0) return cudaSuccess;
-    ball_kernel<<<nballs, kBlock, 0, s>>>(vol, nx, ny, nz, sx, sy, sz, thr, centres, radii, counts, faces);
-    return cudaGetLastError();
-}
 
 }  // namespace vr

@@ -116,10 +116,13 @@ cudaError_t launch_ingest(const void *src, int format, long long nxy, int nz, co
 cudaError_t launch_threshold_count(const int16_t *vol, long long n, int thr,
                                    unsigned long long *count, cudaStream_t s);
 // K4 ball form
-cudaError_t launch_ball_counts(const int16_t *vol, int nx, int ny, int nz, double sx, double sy,
-                               double sz, int thr, const double *centres, const double *radii,
-                               int nballs, unsigned long long *counts, unsigned long long *faces,
-                               cudaStream_t s);
+// K4 method of spheres (vr_measure.cu): whole-volume count + isosurface area
+// (out[0..1], zeroed by the call), and per ball count + area (areas may be null)
+cudaError_t launch_threshold_measure(const int16_t *vol, int nx, int ny, int nz, double sx, double sy,
+                                     double sz, int thr, unsigned long long *out, cudaStream_t s);
+cudaError_t launch_ball_measure(const int16_t *vol, int nx, int ny, int nz, double sx, double sy, double sz,
+                                int thr, const double *centres, const double *radii, int nballs,
+                                unsigned long long *counts, unsigned long long *areas, cudaStream_t s);
 
 // image metrics (vr_quality.cu; quality.py:37-79): exact sum of squared RGB
 // differences, and the sum of the SSIM map over the valid region

@@ -1,19 +1,21 @@
 """Voxel volume measure (K4) -- the paper's "method of spheres" on voxels.
 
-The reference measures S and V of a probe ball on triangle meshes by Monte
-Carlo (morphology.py:238-306); it has no voxel form.  Here, on the
-CT volume itself and exactly:
+The reference measures S (surface inside a probe ball) and V (object volume
+inside it) on triangle meshes by Monte Carlo (morphology.py:70-143
+clipped_area, :238-267 clipped_volume, :270-306 svr_at_point: SVR = S/V,
+undefined where V == 0); it has no voxel form.  Here, on the CT
+volume thresholded at ``thr`` (csrc/vr_measure.cu):
 
-* ``threshold_count(volume, thr)``: number of voxels with value >= thr; the
-  object volume is that count times the voxel volume sx*sy*sz.
-* ``ball_measure(volume, thr, centres, radii)``: per probe ball B(X, R), the
-  member voxels (value >= thr, centre (i*sx, j*sy, k*sz) inside the closed
-  ball) -> V = count * voxel volume, and their exposed faces (6-neighbour
-  below thr or outside the volume) -> S = sum of face areas; SVR = S / V
-  (PAPER.md:150-172), undefined (None/NaN) where V == 0.
+* V = number of voxels with value >= thr (centre in the closed ball for the
+  ball form) times the voxel volume sx*sy*sz -- an exact integer count;
+* S = area of the isosurface at thr - 0.5 of the piecewise-linear
+  (Kuhn-tetrahedra) interpolant, which separates exactly the voxels V counts
+  (polygons with centroid in the ball for the ball form), summed exactly in
+  units of 2^-24 mm^2.
 
-Integer results; the CPU restatement in oracle/ checks them bit-exactly
-(parity unpinned: there is no reference function to pin against).
+Both are bit-exact against the C restatement in oracle/ (parity unpinned:
+there is no reference function); the definitions are pinned by the analytic
+oracles of SPEC.md:472-473 in tests/test_measure.py.
 """
 
 from __future__ import annotations
@@ -22,12 +24,23 @@ import numpy as np
 
 from . import _lib
 
+AREA_SCALE = float(1 << 24)  # include/voxelray_b200.h VR_AREA_SCALE
+
 
 def _dev(volume, device):
     import torch
 
+    if not hasattr(volume, "handle"):
+        from .render import as_volume
+
+        volume = as_volume(volume)
     dvol = volume.device(device) if hasattr(volume, "device") and callable(volume.device) else volume
     return torch, dvol, torch.device("cuda", dvol.device)
+
+
+def _svr(V, S):
+    with np.errstate(divide="ignore", invalid="ignore"):
+        return np.where(V > 0, S / np.where(V > 0, V, 1.0), np.nan)
 
 
 def threshold_count(volume, thr: int, device: int = 0) -> int:
@@ -43,8 +56,20 @@ def threshold_volume_mm3(volume, thr: int, device: int = 0) -> float:
     return threshold_count(volume, thr, device) * (sx * sy * sz)
 
 
-def ball_counts(volume, thr: int, centres, radii, device: int = 0):
-    """(counts (nballs,), faces (nballs, 3) exposed faces per axis) as uint64."""
+def threshold_measure(volume, thr: int, device: int = 0) -> dict:
+    """Whole volume: count, area_fx (exact), V (mm^3), S (mm^2), SVR = S/V."""
+    torch, dvol, dev = _dev(volume, device)
+    out = torch.empty(2, dtype=torch.int64, device=dev)
+    _lib.check(_lib.load().vr_threshold_measure(dvol.handle, int(thr), _lib.ptr(out),
+                                                _lib.ptr_stream(torch.cuda.current_stream(dev))))
+    count, area_fx = (int(x) for x in out.cpu().tolist())
+    sx, sy, sz = volume.spacing
+    V = count * (sx * sy * sz)
+    S = area_fx / AREA_SCALE
+    return {"count": count, "area_fx": area_fx, "V_mm3": V, "S_mm2": S, "svr": S / V if V > 0 else float("nan")}
+
+
+def _balls(volume, thr, centres, radii, device, with_area):
     torch, dvol, dev = _dev(volume, device)
     c = np.ascontiguousarray(centres, dtype=np.float64).reshape(-1, 3)
     r = np.array(np.broadcast_to(np.asarray(radii, dtype=np.float64), (c.shape[0],)))
@@ -52,20 +77,24 @@ def ball_counts(volume, thr: int, centres, radii, device: int = 0):
     ct = torch.from_numpy(c).to(dev)
     rt = torch.from_numpy(r).to(dev)
     counts = torch.empty(n, dtype=torch.int64, device=dev)
-    faces = torch.empty((n, 3), dtype=torch.int64, device=dev)
-    _lib.check(_lib.load().vr_ball_counts(dvol.handle, int(thr), _lib.ptr(ct), _lib.ptr(rt), n,
-                                          _lib.ptr(counts), _lib.ptr(faces),
-                                          _lib.ptr_stream(torch.cuda.current_stream(dev))))
-    return counts.cpu().numpy().astype(np.uint64), faces.cpu().numpy().astype(np.uint64)
+    area = torch.empty(n, dtype=torch.int64, device=dev) if with_area else None
+    _lib.check(_lib.load().vr_ball_measure(dvol.handle, int(thr), _lib.ptr(ct), _lib.ptr(rt), n,
+                                           _lib.ptr(counts), _lib.ptr(area),
+                                           _lib.ptr_stream(torch.cuda.current_stream(dev))))
+    counts = counts.cpu().numpy().astype(np.uint64)
+    return (counts, area.cpu().numpy().astype(np.uint64)) if with_area else counts
+
+
+def ball_counts(volume, thr: int, centres, radii, device: int = 0) -> np.ndarray:
+    """Voxels >= thr with centre in each closed ball B(X, R), uint64 (nballs,)."""
+    return _balls(volume, thr, centres, radii, device, False)
 
 
 def ball_measure(volume, thr: int, centres, radii, device: int = 0) -> dict:
-    """V (mm^3), S (mm^2) and SVR = S/V per ball (NaN where V == 0)."""
-    counts, faces = ball_counts(volume, thr, centres, radii, device)
+    """Per ball: count, area_fx (exact), V (mm^3), S (mm^2) and SVR = S/V
+    (NaN where V == 0: the reference's Undefined, morphology.py:296-306)."""
+    counts, area = _balls(volume, thr, centres, radii, device, True)
     sx, sy, sz = volume.spacing
     V = counts.astype(np.float64) * (sx * sy * sz)
-    f = faces.astype(np.float64)
-    S = (f[:, 0] * (sy * sz) + f[:, 1] * (sx * sz)) + f[:, 2] * (sx * sy)
-    with np.errstate(divide="ignore", invalid="ignore"):
-        svr = np.where(V > 0, S / V, np.nan)
-    return {"count": counts, "faces": faces, "V_mm3": V, "S_mm2": S, "svr": svr}
+    S = area.astype(np.float64) / AREA_SCALE
+    return {"count": counts, "area_fx": area, "V_mm3": V, "S_mm2": S, "svr": _svr(V, S)}

@@ -123,17 +123,8 @@ def test_threshold_restatement_matches_numpy():
     radii = np.array([6.0, 10.0, 3.3])
     got = O.ball_counts(vals, sp, 550, centres, radii)
     k, j, i = np.meshgrid(np.arange(32), np.arange(36), np.arange(40), indexing="ij")
-    _, faces = O.ball_counts(vals, sp, 550, centres, radii, with_faces=True)
-    solid = np.pad(vals >= 550, 1, constant_values=False)  # outside the volume counts as exposed
     for q in range(3):
         d2 = ((i * sp[0] - centres[q, 0]) ** 2 + (j * sp[1] - centres[q, 1]) ** 2) + (k * sp[2] - centres[q, 2]) ** 2
         member = (d2 <= radii[q] ** 2) & (vals >= 550)
         assert got[q] == np.count_nonzero(member)
-        core = solid[1:-1, 1:-1, 1:-1]
-        for axis, (lo, hi) in enumerate((((1, 1, 0), (1, 1, 2)), ((1, 0, 1), (1, 2, 1)), ((0, 1, 1), (2, 1, 1)))):
-            # neighbour along x is the last array axis, z the first
-            nb_lo = solid[lo[0]:lo[0] + 32, lo[1]:lo[1] + 36, lo[2]:lo[2] + 40]
-            nb_hi = solid[hi[0]:hi[0] + 32, hi[1]:hi[1] + 36, hi[2]:hi[2] + 40]
-            want = np.count_nonzero(member & ~nb_lo) + np.count_nonzero(member & ~nb_hi)
-            assert faces[q, axis] == want, (q, axis)
-        assert core.shape == vals.shape
+
