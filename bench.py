@@ -26,6 +26,7 @@ from __future__ import annotations
 import argparse
 import gc
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -55,11 +56,17 @@ CONFIGS = {
     "c4": dict(dims=(512, 512, 2048), size=2048, tf="bone", projection="pinhole",
                settings=dict(interpolation="tricubic", use_blocks=True),
                desc="512x512x2048 -> 2048^2, tricubic, bricks 64/3"),
-    "c5": dict(dims=(512, 512, 512), size=1024, tf="bone", projection="pinhole", views=36,
+    "c5": dict(dims=(512, 512, 512), size=1024, tf="bone", projection="pinhole", views=360,
                settings=dict(interpolation="tricubic", use_blocks=True),
-               measure=dict(threshold=550, balls=64, radius=16.0),
-               desc="turntable: 36 views/step (10 deg apart) of C3 + threshold count and 64 ball measures"),
+               measure=dict(threshold=550, balls=360, radius=16.0),
+               desc="turntable: 360 views/step (1 deg apart) of C3 in one batched submission + the method "
+                    "of spheres (threshold 550: whole-volume V and S, 360 probe balls R=16 mm)"),
 }
+
+# standalone K4 line (`--config k4`): the method of spheres on the C3 volume
+K4_CONFIG = dict(dims=(512, 512, 512), threshold=550, balls=360, radius=16.0,
+                 desc="method of spheres on the 512^3 torso: whole-volume V (voxel count) and S (isosurface "
+                      "area) at 550 HU + 360 probe balls R=16 mm")
 
 L2_FLUSH_BYTES = 512 << 20
 
@@ -70,7 +77,7 @@ def parse():
     p.add_argument("--steps", type=int, default=100)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    p.add_argument("--config", choices=sorted(CONFIGS) + ["k4"], default="c3")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--dist-backend", choices=("nccl", "gloo"), default="nccl")
@@ -81,7 +88,7 @@ def parse():
     p.add_argument("--set", action="append", default=[], metavar="KEY=VALUE",
                    help="override a RenderSettings field of the config (ablations)")
     args = p.parse_args()
-    for kv in args.set:
+    for kv in args.set if args.config != "k4" else []:
         key, val = kv.split("=", 1)
         try:
             CONFIGS[args.config]["settings"][key] = json.loads(val)
@@ -283,6 +290,48 @@ def bench_config(args, cfg):
             "settings": {k: v for k, v in sorted(cfg["settings"].items())}}
 
 
+def ball_centres(extent, n):
+    """K4 probe-ball centres (seeded: default_rng(0))."""
+    import numpy as np
+
+    rng = np.random.default_rng(0)
+    return rng.uniform(0.2, 0.8, size=(n, 3)) * np.array(extent)
+
+
+def cpu_sweep_sample(cfg, values, spacing, extent, sample_views):
+    """C5 on the CPU oracle, bounded: `sample_views` of the 360 views (evenly
+    spaced) plus the full method-of-spheres measure; the sweep time is
+    estimated as 360/sample_views x the views' time + the measure's."""
+    from types import SimpleNamespace
+
+    from oracle import oracle as O
+
+    views = cfg["views"]
+    cam0, tf, settings = oracle_scene_args(cfg, extent)
+    cx, cy, cz = (0.5 * e for e in extent)
+    d = 2.2 * max(extent)
+    t_views = 0.0
+    taken = 0
+    for i in range(sample_views):
+        k = i * views // sample_views
+        ang = 2.0 * math.pi * k / views
+        cam = SimpleNamespace(**{**cam0.__dict__, "position": (cx + d * math.cos(ang), cy + d * math.sin(ang), cz)})
+        t, r = cpu_oracle_frame(values, spacing, cam, tf, settings)
+        t_views += t
+        taken += r.samples_taken
+    m = cfg["measure"]
+    t0 = time.perf_counter()
+    O.threshold_measure(values, spacing, m["threshold"])
+    O.ball_measure(values, spacing, m["threshold"], ball_centres(extent, m["balls"]), [m["radius"]] * m["balls"])
+    t_k4 = time.perf_counter() - t0
+    sweep = t_views * views / sample_views + t_k4
+    return {"value": views / sweep, "unit": "frames/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"{sample_views} of the {views} views via oracle.render ({t_views:.2f} s) + the full "
+                      f"method-of-spheres measure via the oracle ({t_k4:.2f} s); sweep time estimated as "
+                      f"{views}/{sample_views} x views + measure",
+            "samples_taken_sampled_views": taken}
+
+
 def run_reference(args):
     """--impl reference: the CPU oracle port (C restatement of the reference's
     numba march + numpy prep, pinned to the reference's goldens) on all host
@@ -302,6 +351,25 @@ def run_reference(args):
     extent = ((nx - 1) * spacing[0], (ny - 1) * spacing[1], (nz - 1) * spacing[2])
     camera, tf, settings = oracle_scene_args(cfg, extent)
     threads = O.num_threads()
+    if cfg.get("views", 1) > 1:
+        # the sweep, sampled: each step renders 2 of the views + the full measure
+        for _ in range(max(args.warmup, 0)):
+            cpu_sweep_sample(cfg, values, spacing, extent, sample_views=2)
+        est = [cpu_sweep_sample(cfg, values, spacing, extent, sample_views=2) for _ in range(args.steps)]
+        sweep_s = [cfg["views"] / e["value"] for e in est]
+        fps = args.steps * cfg["views"] / sum(sweep_s)
+        line = {
+            "impl": "reference", "metric": "frames/sec", "value": fps, "unit": "frames/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sum(sweep_s) / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": bench_config(args, cfg),
+            "parallelism": f"CPU, {threads} threads (rank 0 only)",
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": threads, "kind": "port",
+                             "sample": "per step: " + est[-1]["sample"]},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
     for _ in range(max(args.warmup, 0)):
         cpu_oracle_frame(values, spacing, camera, tf, settings)
     times, taken = [], 0
@@ -360,13 +428,14 @@ def run_ours(args):
     extent = ((nx - 1) * spacing[0], (ny - 1) * spacing[1], (nz - 1) * spacing[2])
     views = cfg.get("views", 1)
     cameras = orbit_cameras(vr, extent, cfg["size"], views) if views > 1 else [make_camera(vr, cfg, extent)]
+    my_views = list(range(rank, views, world)) if views > 1 else [0]  # view-parallel sweep: view v -> rank v % N
     tf = vr.get_preset(cfg["tf"])
     settings = vr.RenderSettings(**cfg["settings"])
     # the NCCL gather is stream-ordered (no host round trip per frame); the
     # CUDA-IPC shared frame needs host barriers per frame and is opt-in
     transport = args.transport or "gather"
     shared = None
-    if world > 1 and transport == "shared":
+    if world > 1 and views == 1 and transport == "shared":
         from paper_2005_01442_b200.distributed import SharedFrame
 
         try:
@@ -374,9 +443,15 @@ def run_ours(args):
         except Exception as exc:  # no peer access between these GPUs: fall back to the gather
             print(f"shared frame unavailable ({exc}); using the gather", file=sys.stderr)
             transport = "gather"
-    rend = vr.Renderer(dvol, cameras[0], tf, settings, device=dev.index,
-                       interleave=(world, rank) if world > 1 else None, time_kernel=True,
-                       frame_out=shared.frame if shared is not None else None)
+    if views > 1:
+        # the sweep: one vr_render_views submission for all of this rank's views
+        rend = vr.Renderer(dvol, cameras[my_views[0]], tf, settings, device=dev.index, time_kernel=True,
+                           views=len(my_views))
+        rend.set_views([cameras[v] for v in my_views])
+    else:
+        rend = vr.Renderer(dvol, cameras[0], tf, settings, device=dev.index,
+                           interleave=(world, rank) if world > 1 else None, time_kernel=True,
+                           frame_out=shared.frame if shared is not None else None)
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     # read after the write flush so L2 holds clean lines: the timed frame then
@@ -389,15 +464,14 @@ def run_ours(args):
         # K4 batched with the sweep: whole-volume threshold count + ball counts
         import numpy as np
 
-        rng = np.random.default_rng(0)
-        centres = torch.from_numpy(rng.uniform(0.2, 0.8, size=(measure["balls"], 3)) * np.array(extent)).to(dev)
+        centres = torch.from_numpy(ball_centres(extent, measure["balls"])).to(dev)
         radii = torch.full((measure["balls"],), float(measure["radius"]), dtype=torch.float64, device=dev)
         k4 = torch.zeros(2 + 2 * measure["balls"], dtype=torch.int64, device=dev)
 
     def frame():
-        for cam in cameras:
-            if views > 1:
-                rend.set_camera(cam)
+        if views > 1:
+            rend.render_async(stream)
+        else:
             if shared is not None:
                 shared.acquire()  # rank 0 is done with the previous frame
             rend.render_async(stream)
@@ -406,7 +480,7 @@ def run_ours(args):
             elif world > 1:
                 packed = rend.pixels.reshape(-1, 4)
                 gather_frame(packed if args.dist_backend == "nccl" else packed.cpu(), W, H)
-        if measure:
+        if measure and rank == 0:  # K4 on the sweep's stream (rank 0: it is whole-volume)
             s = _lib.ptr_stream(stream)
             _lib.check(L.vr_threshold_measure(dvol.handle, int(measure["threshold"]), _lib.ptr(k4), s))
             nb = measure["balls"]
@@ -417,7 +491,8 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         frame()
     torch.cuda.synchronize()
-    st = rend.stats()  # the last view of the sweep
+    st = rend.stats()  # this rank's frame share, or its whole batch of views
+    st_local = dict(st)
     if world > 1:
         import torch.distributed as dist
 
@@ -439,7 +514,7 @@ def run_ours(args):
             ev1.record(stream)
             ev1.synchronize()
             step_ms.append(ev0.elapsed_time(ev1))
-            kern_ms.append(rend.kernel_ms())  # last view's ray-cast launches
+            kern_ms.append(rend.kernel_ms())  # the ray-cast launch pair (all of a batch's views)
         torch.cuda.synchronize()
     total_ms = sum(step_ms)
     kern_total = sum(kern_ms)
@@ -464,14 +539,59 @@ def run_ours(args):
     # transparent) are counted as taken but read nothing, so the survey's
     # taken-based model overstates the work; it is kept below
     # as `survey_model` for comparison.
-    interp = int(st.get("interpolated") or 0)
-    iters = int(st.get("march_iterations") or 0)
-    gathered = ((interp + 6 * shaded) * b_sample + iters * 32 + W * H * 4) / world
+    interp = int(st_local.get("interpolated") or 0)
+    iters = int(st_local.get("march_iterations") or 0)
+    pix_bytes = (W * H * len(my_views) if views > 1 else rend.npix) * 4
+    gathered = (interp + 6 * st_local["shaded"]) * b_sample + iters * 32 + pix_bytes
     achieved = gathered / kern_s / 1e9
-    survey_bytes = (taken * b_sample + shaded * b_grad + W * H * 4) / world
+    survey_bytes = st_local["samples_taken"] * b_sample + st_local["shaded"] * b_grad + pix_bytes
     peak, peak_kind = measured_peak()
 
     e2e = None
+    if not args.no_e2e and views > 1:
+        # the sweep through the public host API: render_views (one submission,
+        # frames copied to host memory) + the method of spheres on rank 0
+        import numpy as np
+
+        host_vol = vr.ScalarVolume(dvol.download(), spacing, dvol.value_range)
+        host_vol._attach_device(dvol)
+        mine = [cameras[v] for v in my_views]
+        c_host = centres.cpu().numpy() if measure else None
+
+        def call():
+            imgs = vr.render_views(host_vol, mine, tf, settings)
+            if measure and rank == 0:
+                vr.threshold_measure(host_vol, measure["threshold"])
+                vr.ball_measure(host_vol, measure["threshold"], c_host, measure["radius"])
+            return imgs
+        for _ in range(max(1, min(args.warmup, 2))):
+            call()
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        gc.collect()
+        gc.disable()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            imgs = call()
+        e2e_s = time.perf_counter() - t0
+        gc.enable()
+        del imgs
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64)
+            t = t if args.dist_backend == "gloo" else t.to(dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        nb = measure["balls"] if measure else 0
+        e2e = {"value": args.steps * views / e2e_s, "unit": "frames/s",
+               "h2d_bytes_per_step": 4096 * 4 * 8 + 14 * 8 * len(my_views) + (32 * nb if measure else 0),
+               "d2h_bytes_per_step": W * H * 4 * len(my_views) + 8 * (5 * len(my_views) + 3)
+               + (16 + 16 * nb if measure else 0),
+               "api": ("paper_2005_01442_b200.render_views(volume, cameras, TF, settings) -> [ImageRGBA] "
+                       "(vr_render_views: one submission for the sweep; frames copied to host) + "
+                       "threshold_measure / ball_measure (vr_threshold_measure / vr_ball_measure)")}
     if not args.no_e2e and views == 1:
         host_vol = vr.ScalarVolume(dvol.download(), spacing, dvol.value_range)
         host_vol._attach_device(dvol)
@@ -525,6 +645,8 @@ def run_ours(args):
                "api": api}
 
     cpu = None
+    if rank == 0 and world == 1 and views > 1 and not args.no_cpu_baseline:
+        cpu = cpu_sweep_sample(cfg, dvol.download(), spacing, extent, sample_views=2)
     if rank == 0 and world == 1 and views == 1 and not args.no_cpu_baseline:
         from oracle import oracle as O
 
@@ -546,7 +668,8 @@ def run_ours(args):
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (torso phantom generated on the device, bit-identical to the reference's)",
-        "samples_per_sec": taken * fps, "samples_taken": taken, "samples_skipped": st["samples_skipped"],
+        "samples_per_sec": taken / (total_ms / args.steps / 1e3), "samples_taken": taken,
+        "samples_skipped": st["samples_skipped"],
         "shaded_samples": shaded, "interpolated_samples": st.get("interpolated"),
         "march_iterations": st.get("march_iterations"),
         "config": bench_config(args, cfg),
@@ -565,7 +688,7 @@ def run_ours(args):
                                       "formula": f"taken*{b_sample} + shaded*{b_grad} + W*H*4 (SURVEY 8(d))"},
                      "ncu": committed_ncu(args.config)},
         "clocks": clocks.summary(),
-        "gpu_launches": (launches_per_frame(settings) * views + (2 if measure else 0)) * args.steps,
+        "gpu_launches": (launches_per_frame(settings) + (2 if measure else 0)) * args.steps,
         "e2e": e2e,
         "cpu_baseline": cpu,
     }
@@ -576,9 +699,126 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_k4(args):
+    """--config k4: K4 alone.  One step = whole-volume threshold measure (V
+    count + isosurface S) + 360 probe balls, L2 flushed before each step.  The
+    roofline is the whole-volume pass (HBM-bound: 2 bytes per voxel), timed
+    per kernel with CUDA events on the launching stream; the count-only pass
+    (vr_threshold_count) is reported beside it."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import paper_2005_01442_b200 as vr
+    from paper_2005_01442_b200 import _lib
+
+    rank, world, _ = dist_setup(args.gpus, args.dist_backend)
+    if world == 1:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    c = K4_CONFIG
+    spacing = (1.0, 1.0, 1.0)
+    dvol = vr.device_phantom("torso", c["dims"], spacing, device=dev.index)
+    nx, ny, nz = dvol.dims
+    extent = ((nx - 1) * spacing[0], (ny - 1) * spacing[1], (nz - 1) * spacing[2])
+    nb = c["balls"]
+    centres = torch.from_numpy(ball_centres(extent, nb)).to(dev)
+    radii = torch.full((nb,), float(c["radius"]), dtype=torch.float64, device=dev)
+    out = torch.zeros(2 + 2 * nb, dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    L = _lib.load()
+    stream = torch.cuda.current_stream(dev)
+    s = _lib.ptr_stream(stream)
+    thr = int(c["threshold"])
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+
+    def step(timed):
+        if timed:
+            ev[0].record(stream)
+        _lib.check(L.vr_threshold_measure(dvol.handle, thr, _lib.ptr(out), s))
+        if timed:
+            ev[1].record(stream)
+        _lib.check(L.vr_ball_measure(dvol.handle, thr, _lib.ptr(centres), _lib.ptr(radii), nb,
+                                     ctypes.c_void_p(out.data_ptr() + 16),
+                                     ctypes.c_void_p(out.data_ptr() + 16 + 8 * nb), s))
+        if timed:
+            ev[2].record(stream)
+
+    for _ in range(max(args.warmup, 3)):
+        step(False)
+    torch.cuda.synchronize()
+    t_step, t_whole, t_balls, t_count = [], [], [], []
+    with ClockSampler(dev.index) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            step(True)
+            flush.fill_(2)
+            cnt.zero_()
+            ev[3].record(stream)
+            _lib.check(L.vr_threshold_count(dvol.handle, thr, _lib.ptr(cnt), s))
+            ev[4].record(stream)
+            ev[4].synchronize()
+            t_whole.append(ev[0].elapsed_time(ev[1]))
+            t_balls.append(ev[1].elapsed_time(ev[2]))
+            t_step.append(ev[0].elapsed_time(ev[2]))
+            t_count.append(ev[3].elapsed_time(ev[4]))
+    res = out.cpu().numpy()
+    count, area_fx = int(res[0]), int(res[1])
+    nvox = nx * ny * nz
+    peak, peak_kind = measured_peak()
+    whole_ms = float(np.mean(t_whole))
+    count_ms = float(np.mean(t_count))
+    achieved = 2 * nvox / (whole_ms / 1e3) / 1e9
+    count_gbs = 2 * nvox / (count_ms / 1e3) / 1e9
+    total_ms = sum(t_step)
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O
+
+        values = dvol.download()
+        t0 = time.perf_counter()
+        want = O.threshold_measure(values, spacing, thr)
+        t_cpu = time.perf_counter() - t0
+        assert want == (count, area_fx), (want, count, area_fx)
+        cpu = {"value": 1.0 / t_cpu, "unit": "whole-volume measures/s", "cores": O.num_threads(), "kind": "port",
+               "sample": "one whole-volume measure (V count + marching-tetrahedra S) via oracle.threshold_measure "
+                         "(equal to the GPU's, checked)"}
+    line = {
+        "metric": "method-of-spheres measures/sec", "value": args.steps / (total_ms / 1e3),
+        "unit": "measures/s", "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "replicas",
+        "vs_baseline": None, "dtype": "i16 -> u64 (S in f64, fixed-point sum)", "data": "synthetic",
+        "config": {"workload": "k4", "desc": c["desc"], "volume": list(c["dims"]), "balls": nb,
+                   "radius_mm": c["radius"], "threshold": thr},
+        "l2": "flushed before every timed kernel (512 MiB write)",
+        "result": {"count": count, "V_mm3": count * 1.0, "S_mm2": area_fx / 2.0 ** 24,
+                   "svr_per_mm": (area_fx / 2.0 ** 24) / count if count else None},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": peak_kind, "traffic": None,
+                     "kernel": "threshold_measure_kernel (whole volume: V count + isosurface S)",
+                     "kernel_ms": whole_ms, "bytes_model": "2 B per voxel (int16 read once)",
+                     "count_only": {"kernel": "threshold_kernel (vr_threshold_count)", "kernel_ms": count_ms,
+                                    "achieved": count_gbs, "frac": count_gbs / peak},
+                     "balls_ms": float(np.mean(t_balls))},
+        "clocks": clocks.summary(),
+        "gpu_launches": 3 * args.steps,
+        "e2e": None,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.config == "k4":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "k4 is an auxiliary line; the reference arm "
+                              "times the headline configs"}))
+            return
+        run_k4(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

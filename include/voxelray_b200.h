@@ -211,6 +211,22 @@ int vr_render(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_rend
               const double *lut, const double *table, const uint8_t *rgba,
               const vr_render_outputs *out, void *stream);
 
+/* A batch of views in one submission -- the turntable sweep of BASELINE
+ * configs[4] (the reference's viewer orbits the camera, frontend/src/camera.ts
+ * :35-44, and renders each view with its own render() call, render.py:327).
+ * Every view is the frame `frame` describes (size, tile, projection,
+ * interleave) seen from views[14 v .. 14 v + 13] = position[3], fwd[3],
+ * right[3], up[3], half_w, half_h (device float64, v < nviews).  The TF
+ * visibility (K2b) runs once for the batch, then one persistent ray-cast pass
+ * takes the rays of all views from one queue.  Outputs are laid out view after
+ * view: pixels / premult / depth / taken / skipped at v * (pixels per view),
+ * blocks_hit at v * nblocks, totals at 5 v (work: the whole batch).  Each
+ * view's outputs equal vr_render's for that camera.  Asynchronous. */
+int vr_render_views(vr_volume *vol, vr_grid *grid, const vr_camera *frame, const double *views,
+                    int32_t nviews, const vr_render_params *prm, const double *lut,
+                    const double *table, const uint8_t *rgba, const vr_render_outputs *out,
+                    void *stream);
+
 /* Reference-facing host entry: same as vr_render with HOST tables and HOST
  * outputs (pixels required, others optional; totals_host[5] required).  The
  * library stages tables/outputs through stream-ordered device memory; the

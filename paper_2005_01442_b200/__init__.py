@@ -36,6 +36,7 @@ from .render import (
     composite_step,
     generate_ray,
     render,
+    render_views,
     settings_from_dict,
     shade_headlight,
 )

@@ -29,7 +29,7 @@ EXPORTS = (
     "vr_last_error", "vr_abi_version", "vr_volume_create", "vr_volume_ingest", "vr_phantom_create",
     "vr_volume_destroy", "vr_volume_culling_tables", "vr_volume_info", "vr_volume_data", "vr_volume_download",
     "vr_grid_create", "vr_grid_destroy", "vr_grid_shape", "vr_grid_minmax",
-    "vr_grid_visibility", "vr_render", "vr_render_to_host", "vr_preclassify",
+    "vr_grid_visibility", "vr_render", "vr_render_views", "vr_render_to_host", "vr_preclassify",
     "vr_sample_points", "vr_gradient_points", "vr_threshold_count", "vr_threshold_measure",
     "vr_ball_measure",
     "vr_event_create", "vr_event_destroy", "vr_event_elapsed_ms", "vr_interleave_size",
@@ -106,6 +106,8 @@ def load() -> ctypes.CDLL:
         "vr_grid_visibility": ([P, P, i32, f64, f64, P, P, P, P], ctypes.c_int),
         "vr_render": ([P, P, ctypes.POINTER(Camera), ctypes.POINTER(RenderParams), P, P, P,
                        ctypes.POINTER(RenderOutputs), P], ctypes.c_int),
+        "vr_render_views": ([P, P, ctypes.POINTER(Camera), P, i32, ctypes.POINTER(RenderParams), P, P, P,
+                             ctypes.POINTER(RenderOutputs), P], ctypes.c_int),
         "vr_render_to_host": ([P, P, ctypes.POINTER(Camera), ctypes.POINTER(RenderParams), P, P,
                                P, P, P, P, P], ctypes.c_int),
         "vr_preclassify": ([P, P, i32, f64, f64, P, P], ctypes.c_int),

@@ -633,8 +633,14 @@ static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
     }
     a.half_w = cam->half_w;
     a.half_h = cam->half_h;
-    long long npix_unused;
-    cell_counts(cam, a.cells_x, a.ncells, a.slots, npix_unused);
+    long long npix;
+    cell_counts(cam, a.cells_x, a.ncells, a.slots, npix);
+    a.nviews = 1;
+    a.view0 = 0;
+    a.views = nullptr;
+    a.items_per_view = (long long)a.slots * vr::kTileW * vr::kTileH;
+    a.view_pix = npix;
+    a.nblocks = grid ? grid->nblocks : 1;
     a.il_n = cam->interleave_n > 1 ? cam->interleave_n : 1;
     a.il_k = cam->interleave_n > 1 ? cam->interleave_k : 0;
     a.il_packed = cam->interleave_n > 1 && !cam->interleave_frame;
@@ -671,11 +677,15 @@ static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
 
 static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_render_params *prm,
                        const double *lut, const double *table, const uint8_t *rgba, const vr_render_outputs *out,
-                       cudaStream_t s) {
+                       cudaStream_t s, const double *views = nullptr, int nviews = 1) {
     vr::RenderArgs a;
     int rc = build_args(vol, grid, cam, prm, lut, table, rgba, a);
     if (rc) return rc;
     if (!out) return fail(VR_EINVALID, "null outputs");
+    if (nviews < 1 || (nviews > 1 && !views)) return fail(VR_EINVALID, "views: need nviews >= 1 and a view table");
+    if ((long long)nviews * a.items_per_view >= (1LL << 40)) return fail(VR_EINVALID, "too many views");
+    a.nviews = nviews;
+    a.views = views;
     a.pixels = out->pixels;
     a.premult = out->premult;
     a.depth = out->depth;
@@ -690,7 +700,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     vr::ZeroSpec zero{};
     if (a.totals) {
         zero.p[1] = a.totals;
-        zero.n[1] = 5;
+        zero.n[1] = 5 * nviews;
     }
     if (a.work) {
         zero.p[2] = a.work;
@@ -698,7 +708,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     }
     if (a.blocks_hit) {
         zero.b = a.blocks_hit;
-        zero.nb = nblocks;
+        zero.nb = nblocks * nviews;
     }
     const bool post = a.mode == VR_MODE_DVR && a.classify == VR_CLS_POST && vol->cells;
     Scratch lut_range(s), heavy(s);
@@ -717,8 +727,11 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         // queue; 384 vs 256 after the first-trip hand-off rule: C3 +1.4 %,
         // C2/C4 within noise, tools/gpu_sweep_long.sh)
         a.heavy_long = VR_HEAVY_LONG;
-        const long long items = (long long)a.slots * vr::kTileW * vr::kTileH;
-        a.heavy_cap = items < (1LL << 20) ? items : (1LL << 20);
+        // queue capacity: every ray of one frame (up to 2^20); a batched sweep
+        // hands over rays all along (dense lit rays), so up to 2^22 there
+        const long long items = a.items_per_view * (nviews < vr::kViewChunk ? nviews : vr::kViewChunk);
+        const long long cap = nviews > 1 ? (1LL << 22) : (1LL << 20);
+        a.heavy_cap = items < cap ? items : cap;
         a.heavy_min_left = VR_HEAVY_MIN_LEFT;
         a.heavy_after = VR_HEAVY_AFTER;
         // Dense rays (4 composited samples) go to the cooperative kernel at
@@ -777,13 +790,10 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     if (out->ev_start) VR_CUDA(cudaEventRecord((cudaEvent_t)out->ev_start, s));
     VR_CUDA(vr::launch_raycast(a, s));
     if (out->ev_stop) VR_CUDA(cudaEventRecord((cudaEvent_t)out->ev_stop, s));
-    if (out->totals) {
-        // totals[2] = blocks_visited; totals[3..4] = the visibility counters (zero without a grid)
-        if (a.blocks_hit)
-            VR_CUDA(vr::launch_count_hits(a.blocks_hit, nblocks, a.totals + 2, grid ? vs.v.counters : nullptr, s));
-        else if (grid)
-            VR_CUDA(cudaMemcpyAsync(a.totals + 3, vs.v.counters, 2 * sizeof(unsigned long long),
-                                    cudaMemcpyDeviceToDevice, s));
+    if (out->totals && (a.blocks_hit || grid)) {
+        // per view: totals[5 v + 2] = blocks_visited (with blocks_hit);
+        // [5 v + 3 .. 4] = the visibility counters (zero without a grid)
+        VR_CUDA(vr::launch_count_hits(a.blocks_hit, nblocks, nviews, a.totals, grid ? vs.v.counters : nullptr, s));
     }
     return VR_OK;
 }
@@ -793,6 +803,17 @@ int vr_render(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_rend
     if (!vol) return fail(VR_EINVALID, "null volume");
     DeviceGuard g(vol->device);
     return render_impl(vol, grid, cam, prm, lut, table, rgba, out, (cudaStream_t)stream);
+}
+
+int vr_render_views(vr_volume *vol, vr_grid *grid, const vr_camera *frame, const double *views, int32_t nviews,
+                    const vr_render_params *prm, const double *lut, const double *table, const uint8_t *rgba,
+                    const vr_render_outputs *out, void *stream) {
+    if (!vol) return fail(VR_EINVALID, "null volume");
+    if (nviews < 1 || !views) return fail(VR_EINVALID, "views: need nviews >= 1 and a device view table");
+    if (frame && frame->interleave_n > 1 && frame->interleave_frame)
+        return fail(VR_EINVALID, "views: interleave_frame is not supported for batched views");
+    DeviceGuard g(vol->device);
+    return render_impl(vol, grid, frame, prm, lut, table, rgba, out, (cudaStream_t)stream, views, nviews);
 }
 
 int vr_render_to_host(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_render_params *prm,

@@ -574,6 +574,12 @@ inline PowSpec make_pow(double y) {
 // out of line: one copy of the ~80-instruction pow serves every call site
 static __device__ __noinline__ double pow_glibc(double x, double y) { return vr_glibc_pow(x, y); }
 
-VR_D double vr_pow(double x, const PowSpec &p) { return p.kind == 0 ? x : pow_glibc(x, p.y); }
+// (+0)^y = +0 for y > 0 without the call: the Phong base max(2 (n.l)^2 - 1, 0)
+// is zero for most shaded samples
+VR_D double vr_pow(double x, const PowSpec &p) {
+    if (p.kind == 0) return x;
+    if (x == 0.0 && p.y > 0.0) return 0.0;
+    return pow_glibc(x, p.y);
+}
 
 }  // namespace vr

@@ -316,24 +316,280 @@ __global__ void __launch_bounds__(kMeasureThreads) ball_measure_kernel(MeasureVo
     cta_accumulate(count, area, counts + q, areas ? areas + q : nullptr, true);
 }
 
+// ------------------------------------------------ two-pass fast path
+// Pass 1 (HBM-bound, the only pass over the int16 voxels): every voxel's
+// inside bit (v >= thr) into a flat bit array -- bit i of word i/32 is voxel
+// i in (z, y, x) order, 1/16 of the volume (16 MiB at 512^3, L2-resident) --
+// and the voxel count V.  A lane reads 16 bytes (8 voxels), four lanes merge
+// their bytes into one 32-bit word: every load and store is coalesced.
+// Pass 2 (L2-bound): per cell row (cy, cz) and 32-cell chunk, the 33-bit
+// windows of its four voxel rows locate the cells whose corners are not all
+// equal; only those (a few per mille at CT thresholds) read their 8 voxels
+// and run the tetrahedra.
+__global__ void __launch_bounds__(kMeasureThreads) inside_bits_kernel(const int16_t *__restrict__ v, long long n,
+                                                                      int thr, unsigned *__restrict__ bits,
+                                                                      unsigned long long *count) {
+    const long long n8 = n >> 3;  // whole 8-voxel groups
+    const int lane = threadIdx.x & 31;
+    unsigned long long c = 0;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    // the loop bound is warp-uniform (whole warps of groups), so the shuffles
+    // below always run converged
+    for (long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) & ~31ll; g0 < n8; g0 += stride) {
+        const long long g = g0 + lane;
+        unsigned b = 0;
+        if (g < n8) {
+            const int4 q = __ldg(reinterpret_cast<const int4 *>(v) + g);
+            const unsigned w[4] = {(unsigned)q.x, (unsigned)q.y, (unsigned)q.z, (unsigned)q.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                b |= ((int)(short)(w[k] & 0xffffu) >= thr ? 1u : 0u) << (2 * k);
+                b |= ((int)(short)(w[k] >> 16) >= thr ? 1u : 0u) << (2 * k + 1);
+            }
+            c += (unsigned long long)__popc(b);
+        }
+        // lanes 4m .. 4m+3 hold voxels 32m' .. 32m'+31 of one word
+        unsigned word = b << (8 * (lane & 3));
+        word |= __shfl_xor_sync(0xffffffffu, word, 1);
+        word |= __shfl_xor_sync(0xffffffffu, word, 2);
+        // (the word holding the last n % 32 voxels belongs to the tail thread)
+        if ((lane & 3) == 0 && g < n8 && !((n & 31) && (g >> 2) == (n >> 5))) bits[g >> 2] = word;
+    }
+    // tail voxels (n % 8) and the tail word's missing lanes: one thread
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 31)) {
+        const long long w0 = n >> 5;
+        unsigned word = 0;
+        for (long long i = w0 << 5; i < n; ++i) {
+            const bool in = v[i] >= thr;
+            word |= (in ? 1u : 0u) << (i & 31);
+            if (i >= (n8 << 3)) c += in ? 1 : 0;
+        }
+        bits[w0] = word;
+    }
+    const unsigned long long cs = warp_sum64(c);
+    if (lane == 0 && cs) atomicAdd(count, cs);
+}
+
+// bits of voxels x0 .. x0+32 of row (j, k) (bit b = voxel x0+b; outside the
+// volume: 0), from the flat bit array
+VR_D unsigned long long row_bits33(const MeasureVol &m, const unsigned *bits, int x0, int j, int k) {
+    if (j < 0 || k < 0 || j >= m.ny || k >= m.nz) return 0ull;
+    const int lo = x0 < 0 ? 0 : x0;
+    const int hi = x0 + 32 < m.nx - 1 ? x0 + 32 : m.nx - 1;  // last voxel wanted
+    if (lo > hi) return 0ull;
+    const long long b0 = ((long long)k * m.ny + j) * m.nx + lo;
+    const long long w = b0 >> 5;
+    const int sh = (int)(b0 & 31);
+    const long long nwords = ((long long)m.nx * m.ny * m.nz + 31) >> 5;
+    const unsigned long long win =
+        (unsigned long long)__ldg(bits + w) | ((w + 1 < nwords ? (unsigned long long)__ldg(bits + w + 1) : 0ull) << 32);
+    unsigned long long r = win >> sh;  // >= 33 valid bits (sh <= 31)
+    const int len = hi - lo + 1;
+    r &= len >= 64 ? ~0ull : ((1ull << len) - 1ull);
+    return r << (lo - x0);
+}
+
+// position of the k-th (0-based) set bit of m
+VR_D int nth_set_bit(unsigned m, int k) {
+    int pos = 0;
+#pragma unroll
+    for (int w = 16; w >= 1; w >>= 1) {
+        const int c = __popc(m & ((1u << w) - 1u));
+        if (k >= c) {
+            k -= c;
+            m >>= w;
+            pos += w;
+        }
+    }
+    return pos;
+}
+
+// The straddling cells of all 32 lanes (lane l: cells x0_l + b for the set
+// bits b of st_l, row (cy_l, cz_l)) spread evenly over the lanes -- 32 cells
+// per round -- so the tetrahedra run at full SIMT width however unevenly the
+// surface crosses the lanes' chunks.  Every lane of the warp must call this;
+// returns this lane's share of the fixed-point area.
+template <bool BALL>
+VR_D unsigned long long warp_cells_area(const MeasureVol &m, unsigned st, int x0, int cy, int cz, double level,
+                                        double bx, double by, double bz, double r2) {
+    const unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int cnt = __popc(st);
+    int incl = cnt;  // inclusive prefix of the counts over the lanes
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(full, incl, 31);
+    const int base = incl - cnt;
+    unsigned long long area = 0;
+    for (int start = 0; start < total; start += 32) {
+        const int id = start + lane;
+        int src = 0;  // the last lane whose base <= id
+#pragma unroll
+        for (int step = 16; step >= 1; step >>= 1) {
+            const int cand = src + step;
+            const int b = __shfl_sync(full, base, cand & 31);
+            if (cand < 32 && b <= id) src = cand;
+        }
+        const int k = id - __shfl_sync(full, base, src);
+        const unsigned ms = __shfl_sync(full, st, src);
+        const int sx0 = __shfl_sync(full, x0, src), scy = __shfl_sync(full, cy, src), scz = __shfl_sync(full, cz, src);
+        if (id < total) {
+            const int cx = sx0 + nth_set_bit(ms, k);
+            double f[8], P[8][3];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int a = cx + (c & 1), jj = scy + ((c >> 1) & 1), kk = scz + ((c >> 2) & 1);
+                f[c] = (double)voxel_or_pad(m, a, jj, kk) - level;
+                P[c][0] = (double)a * m.sx;
+                P[c][1] = (double)jj * m.sy;
+                P[c][2] = (double)kk * m.sz;
+            }
+            area += cell_area_fx<BALL>(f, P, bx, by, bz, r2);
+        }
+    }
+    return area;
+}
+
+// cells x0 .. x0+31 of cell row (cy, cz) whose 8 corner bits are not all equal
+VR_D unsigned long long chunk_straddle(const MeasureVol &m, const unsigned *bits, int x0, int cy, int cz) {
+    const unsigned long long r0 = row_bits33(m, bits, x0, cy, cz), r1 = row_bits33(m, bits, x0, cy + 1, cz);
+    const unsigned long long r2 = row_bits33(m, bits, x0, cy, cz + 1), r3 = row_bits33(m, bits, x0, cy + 1, cz + 1);
+    const unsigned long long all = r0 & r1 & r2 & r3, any = r0 | r1 | r2 | r3;
+    unsigned long long st = ((any | (any >> 1)) & ~(all & (all >> 1))) & 0xffffffffull;
+    const int ncells = m.nx - x0;  // cells x0 .. nx-1 exist (cx <= nx-1)
+    if (ncells < 32) st &= ncells <= 0 ? 0ull : ((1ull << ncells) - 1ull);
+    return st;
+}
+
+// Pass 2, whole volume: thread = (32-cell chunk, cell row cy), CTA row =
+// chunks of one cell row; blockIdx.y = cell row, blockIdx.z = slab chunk.
+__global__ void __launch_bounds__(kMeasureThreads) surface_kernel(MeasureVol m, const unsigned *__restrict__ bits,
+                                                                  int thr, int nchunks, unsigned long long *out) {
+    const double level = (double)thr - 0.5;
+    unsigned long long area = 0;
+    const long long total = (long long)nchunks * (m.ny + 1) * (m.nz + 1);
+    // warp-uniform trip count: the tetrahedra are shared out warp-wide
+    for (long long t0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) & ~31ll; t0 < total;
+         t0 += (long long)gridDim.x * blockDim.x) {
+        const long long t = t0 + (threadIdx.x & 31);
+        unsigned st = 0;
+        int x0 = 0, cy = 0, cz = 0;
+        if (t < total) {
+            const int c = (int)(t % nchunks);
+            const long long r = t / nchunks;
+            cy = (int)(r % (m.ny + 1)) - 1;
+            cz = (int)(r / (m.ny + 1)) - 1;
+            x0 = 32 * c - 1;
+            st = (unsigned)chunk_straddle(m, bits, x0, cy, cz);
+        }
+        if (__any_sync(0xffffffffu, st != 0u))
+            area += warp_cells_area<false>(m, st, x0, cy, cz, level, 0.0, 0.0, 0.0, 0.0);
+    }
+    cta_accumulate(0, area, nullptr, out + 1, false);
+}
+
+// Pass 2 per ball: one CTA per ball; thread = (32-cell chunk, cell row, cell
+// slab) of the ball's bounding box.  V: the inside voxels of row
+// (cy, cz) whose centres lie in the ball; S: the straddling cells' polygons
+// with centroid in the ball.
+__global__ void __launch_bounds__(kMeasureThreads) ball_surface_kernel(MeasureVol m, const unsigned *__restrict__ bits,
+                                                                       int thr, const double *centres,
+                                                                       const double *radii, unsigned long long *counts,
+                                                                       unsigned long long *areas) {
+    const int ball = blockIdx.x;
+    const double bx = centres[3 * ball], by = centres[3 * ball + 1], bz = centres[3 * ball + 2];
+    const double rad = radii[ball];
+    const double r2 = rad * rad;
+    const double level = (double)thr - 0.5;
+    const int i0 = box_lo(bx - rad, m.sx), i1 = box_hi(bx + rad, m.sx, m.nx);
+    const int j0 = box_lo(by - rad, m.sy), j1 = box_hi(by + rad, m.sy, m.ny);
+    const int k0 = box_lo(bz - rad, m.sz), k1 = box_hi(bz + rad, m.sz, m.nz);
+    unsigned long long count = 0, area = 0;
+    if (i0 <= i1 && j0 <= j1 && k0 <= k1) {
+        const int nc = (i1 - i0) / 32 + 1, nj = j1 - j0 + 1;
+        const int items = nc * nj * (k1 - k0 + 1);  // (32-cell chunk, cell row, cell slab)
+        // warp-uniform trip counts: tetrahedra shared out warp-wide
+        for (int t0 = threadIdx.x & ~31; t0 < items; t0 += blockDim.x) {
+            const int t = t0 + (threadIdx.x & 31);
+            const bool valid = t < items;
+            const int tc = valid ? t : 0;
+            const int x0 = i0 + 32 * (tc % nc), cy = j0 + (tc / nc) % nj, cz = k0 + tc / (nc * nj);
+            const int xe = min(x0 + 31, i1);  // this chunk's last cell
+            const unsigned long long keep = valid ? (2ull << (xe - x0)) - 1ull : 0ull;
+            const unsigned st = (unsigned)(valid ? chunk_straddle(m, bits, x0, cy, cz) & keep : 0ull);
+            if (areas && __any_sync(0xffffffffu, st != 0u))
+                area += warp_cells_area<true>(m, st, x0, cy, cz, level, bx, by, bz, r2);
+            // voxels x0 .. xe of row (cy, cz) (cells at negative indices have no base voxel)
+            unsigned long long in = valid ? row_bits33(m, bits, x0, cy, cz) & keep : 0ull;
+            while (in) {
+                const int b = __ffsll((long long)in) - 1;
+                in &= in - 1;
+                const double dx = (double)(x0 + b) * m.sx - bx, dy = (double)cy * m.sy - by;
+                const double dz = (double)cz * m.sz - bz;
+                count += ((dx * dx + dy * dy) + dz * dz <= r2) ? 1 : 0;
+            }
+        }
+    }
+    cta_accumulate(count, area, counts + ball, areas ? areas + ball : nullptr, false);
+}
+
 }  // namespace
+
+// stream-ordered scratch for the inside-bit array (freed on the stream)
+struct BitsScratch {
+    cudaStream_t s;
+    unsigned *p = nullptr;
+    unsigned long long *count = nullptr;  // a spare counter after the bits
+    explicit BitsScratch(cudaStream_t st) : s(st) {}
+    cudaError_t alloc(long long nvox) {
+        const size_t words = (size_t)((nvox + 31) / 32 + 1) & ~(size_t)1;  // even: the counter is 8-byte aligned
+        cudaError_t e = cudaMallocAsync((void **)&p, words * 4 + 8, s);
+        if (e == cudaSuccess) count = reinterpret_cast<unsigned long long *>(p + words);
+        return e;
+    }
+    ~BitsScratch() {
+        if (p) cudaFreeAsync(p, s);
+    }
+};
+
+cudaError_t launch_inside_bits(const int16_t *vol, long long n, int thr, unsigned *bits, unsigned long long *count,
+                               cudaStream_t s) {
+    long long grid = (n / 8 + kMeasureThreads - 1) / kMeasureThreads;
+    const long long cap = (long long)device_sms() * 16;
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    inside_bits_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(vol, n, thr, bits, count);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_threshold_measure(const int16_t *vol, int nx, int ny, int nz, double sx, double sy, double sz,
                                      int thr, unsigned long long *out, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(out, 0, 2 * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return e;
     MeasureVol m{vol, nx, ny, nz, sx, sy, sz};
+    const long long n = (long long)nx * ny * nz;
+    if ((reinterpret_cast<uintptr_t>(vol) & 15) == 0) {
+        BitsScratch bits(s);
+        if ((e = bits.alloc(n)) != cudaSuccess) return e;
+        if ((e = launch_inside_bits(vol, n, thr, bits.p, out, s)) != cudaSuccess) return e;
+        const int nchunks = (nx + 1 + 31) / 32;  // cells -1 .. nx-1 in chunks of 32
+        const long long total = (long long)nchunks * (ny + 1) * (nz + 1);
+        long long grid = (total + kMeasureThreads - 1) / kMeasureThreads;
+        const long long cap = (long long)device_sms() * 16;
+        if (grid > cap) grid = cap;
+        surface_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, thr, nchunks, out);
+        return cudaGetLastError();
+    }
     const int runs = (nx + 1 + 7) / 8;  // cells -1 .. nx-1 in runs of 8
     const long long total = (long long)runs * (ny + 1) * (nz + 1);
     long long grid = (total + kMeasureThreads - 1) / kMeasureThreads;
     const long long cap = (long long)device_sms() * 8;
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    const bool vec = (nx % 8) == 0 && (reinterpret_cast<uintptr_t>(vol) & 15) == 0;
-    if (vec)
-        threshold_measure_kernel<true><<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, thr, runs, out);
-    else
-        threshold_measure_kernel<false><<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, thr, runs, out);
+    threshold_measure_kernel<false><<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, thr, runs, out);
     return cudaGetLastError();
 }
 
@@ -342,6 +598,19 @@ cudaError_t launch_ball_measure(const int16_t *vol, int nx, int ny, int nz, doub
                                 unsigned long long *areas, cudaStream_t s) {
     if (nballs <= 0) return cudaSuccess;
     MeasureVol m{vol, nx, ny, nz, sx, sy, sz};
+    if ((reinterpret_cast<uintptr_t>(vol) & 15) == 0) {
+        const long long n = (long long)nx * ny * nz;
+        cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * nballs, s);
+        if (e == cudaSuccess && areas) e = cudaMemsetAsync(areas, 0, sizeof(unsigned long long) * nballs, s);
+        if (e != cudaSuccess) return e;
+        BitsScratch bits(s);
+        if ((e = bits.alloc(n)) != cudaSuccess) return e;
+        // (pass 1's whole-volume count is not needed here: the spare counter)
+        if ((e = launch_inside_bits(vol, n, thr, bits.p, bits.count, s)) != cudaSuccess) return e;
+        ball_surface_kernel<<<(unsigned)nballs, kMeasureThreads, 0, s>>>(
+            m, bits.p, thr, centres, radii, counts, areas);
+        return cudaGetLastError();
+    }
     ball_measure_kernel<<<nballs, kMeasureThreads, 0, s>>>(m, thr, centres, radii, counts, areas);
     return cudaGetLastError();
 }

@@ -663,10 +663,16 @@ __global__ void lut_range_kernel(const double *lut, int nbins, double lut_lo, do
     }
 }
 
+// one CTA per view: blocks_visited of view v into out[5 v + 2] (hits may be
+// null: only the counters), the frame's visibility counters into [5 v + 3..4]
 __global__ void count_hits_kernel(const uint8_t *hits, int n, unsigned long long *out,
                                   const unsigned long long *vis_counters) {
     pdl_enter();
-    if (vis_counters && threadIdx.x < 2) out[1 + threadIdx.x] = vis_counters[threadIdx.x];
+    const long long v = blockIdx.x;
+    out += 5 * v;
+    if (threadIdx.x < 2) out[3 + threadIdx.x] = vis_counters ? vis_counters[threadIdx.x] : 0ull;
+    if (!hits) return;
+    hits += v * n;
     unsigned long long c = 0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) c += hits[i] ? 1 : 0;
     c = warp_sum(c);
@@ -676,7 +682,7 @@ __global__ void count_hits_kernel(const uint8_t *hits, int n, unsigned long long
     if (threadIdx.x == 0) {
         unsigned long long s = 0;
         for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
-        *out = s;
+        out[2] = s;
     }
 }
 
@@ -909,9 +915,9 @@ cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double
     return cudaGetLastError();
 }
 
-cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out,
+cudaError_t launch_count_hits(const uint8_t *hits, int n, int nviews, unsigned long long *totals,
                               const unsigned long long *vis_counters, cudaStream_t s) {
-    cudaError_t e = launch_pdl(count_hits_kernel, 1, 1024, 0, s, hits, n, out, vis_counters);
+    cudaError_t e = launch_pdl(count_hits_kernel, nviews, 1024, 0, s, hits, n, totals, vis_counters);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

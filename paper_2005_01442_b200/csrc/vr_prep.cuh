@@ -89,7 +89,7 @@ cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double
 // blocks_visited = sum(blocks_hit) -> *out (render.py:467)
 // also copies the two visibility counters (blocks_empty, empty-block errors)
 // to out[1..2] when vis_counters is given
-cudaError_t launch_count_hits(const uint8_t *hits, int n, unsigned long long *out,
+cudaError_t launch_count_hits(const uint8_t *hits, int n, int nviews, unsigned long long *totals,
                               const unsigned long long *vis_counters, cudaStream_t s);
 
 // preclassify_volume (transfer.py:142-145): 4 planar uint8 channels

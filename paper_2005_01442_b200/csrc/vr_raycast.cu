@@ -35,32 +35,100 @@ struct Ray {
     double ox, oy, oz, dx, dy, dz;
 };
 
+// One view's camera: basis and image-plane half extents.
+struct ViewCam {
+    double pos[3], fwd[3], right[3], up[3];
+    double half_w, half_h;
+};
+
+VR_D ViewCam view_cam(const RenderArgs &a, int v) {
+    ViewCam c;
+    if (a.views) {
+        const double *p = a.views + 14 * (long long)v;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            c.pos[k] = __ldg(p + k);
+            c.fwd[k] = __ldg(p + 3 + k);
+            c.right[k] = __ldg(p + 6 + k);
+            c.up[k] = __ldg(p + 9 + k);
+        }
+        c.half_w = __ldg(p + 12);
+        c.half_h = __ldg(p + 13);
+    } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            c.pos[k] = a.pos[k];
+            c.fwd[k] = a.fwd[k];
+            c.right[k] = a.right[k];
+            c.up[k] = a.up[k];
+        }
+        c.half_w = a.half_w;
+        c.half_h = a.half_h;
+    }
+    return c;
+}
+
 // render.py:125-144 (pinhole) per pixel, or the orthographic variant.
-VR_D Ray make_ray(const RenderArgs &a, int px, int py) {
+VR_D Ray make_ray(const RenderArgs &a, const ViewCam &c, int px, int py) {
     Ray r;
-    double v = (1.0 - 2.0 * ((double)py + 0.5) / (double)a.H) * a.half_h;
-    double u = (2.0 * ((double)px + 0.5) / (double)a.W - 1.0) * a.half_w;
+    double v = (1.0 - 2.0 * ((double)py + 0.5) / (double)a.H) * c.half_h;
+    double u = (2.0 * ((double)px + 0.5) / (double)a.W - 1.0) * c.half_w;
     if (a.projection == 0) {
-        double d0 = (a.fwd[0] + u * a.right[0]) + v * a.up[0];
-        double d1 = (a.fwd[1] + u * a.right[1]) + v * a.up[1];
-        double d2 = (a.fwd[2] + u * a.right[2]) + v * a.up[2];
+        double d0 = (c.fwd[0] + u * c.right[0]) + v * c.up[0];
+        double d1 = (c.fwd[1] + u * c.right[1]) + v * c.up[1];
+        double d2 = (c.fwd[2] + u * c.right[2]) + v * c.up[2];
         double nrm = sqrt((d0 * d0 + d1 * d1) + d2 * d2);
         r.dx = d0 / nrm;
         r.dy = d1 / nrm;
         r.dz = d2 / nrm;
-        r.ox = a.pos[0];
-        r.oy = a.pos[1];
-        r.oz = a.pos[2];
+        r.ox = c.pos[0];
+        r.oy = c.pos[1];
+        r.oz = c.pos[2];
     } else {
-        r.ox = (a.pos[0] + u * a.right[0]) + v * a.up[0];
-        r.oy = (a.pos[1] + u * a.right[1]) + v * a.up[1];
-        r.oz = (a.pos[2] + u * a.right[2]) + v * a.up[2];
-        r.dx = a.fwd[0];
-        r.dy = a.fwd[1];
-        r.dz = a.fwd[2];
+        r.ox = (c.pos[0] + u * c.right[0]) + v * c.up[0];
+        r.oy = (c.pos[1] + u * c.right[1]) + v * c.up[1];
+        r.oz = (c.pos[2] + u * c.right[2]) + v * c.up[2];
+        r.dx = c.fwd[0];
+        r.dy = c.fwd[1];
+        r.dz = c.fwd[2];
     }
     return r;
 }
+
+// Per-view sample counts of one lane: accumulated while the lane's rays belong
+// to one view, added to that view's totals when the view changes (a lane's
+// rays come in increasing item order, so at most once per view) and at exit.
+struct ViewTotals {
+    int view = -1;
+    unsigned long long taken = 0, skipped = 0;
+    VR_D void add(const RenderArgs &a, int v, long long t, long long s) {
+        if (v != view) {
+            flush(a);
+            view = v;
+        }
+        taken += (unsigned long long)t;
+        skipped += (unsigned long long)s;
+    }
+    VR_D void flush(const RenderArgs &a) {
+        if (view >= 0 && a.totals && (taken | skipped)) {
+            atomicAdd(a.totals + 5 * (long long)view, taken);
+            atomicAdd(a.totals + 5 * (long long)view + 1, skipped);
+        }
+        taken = skipped = 0;
+    }
+    // exit: lanes holding the same view combine their counts first (one
+    // atomic pair per view per warp; all lanes of the warp must call this)
+    VR_D void flush_warp(const RenderArgs &a) {
+        const unsigned same = __match_any_sync(0xffffffffu, view);
+        const unsigned t = __reduce_add_sync(same, (unsigned)taken);
+        const unsigned sk = __reduce_add_sync(same, (unsigned)skipped);
+        if ((int)(threadIdx.x & 31) == __ffs(same) - 1) {
+            taken = t;
+            skipped = sk;
+            flush(a);
+        }
+    }
+};
 
 // render.py:147-156
 VR_D void clip_to_bounds(const Ray &r, const double ext[3], double &tmin, double &tmax) {
@@ -363,7 +431,7 @@ struct RayResult {
 
 // One pixel of _kernels.march (:343-594).
 template <int KIND, bool CUBIC, bool LIGHT, bool SKIP>
-VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
+VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, uint8_t *hits) {
     constexpr bool chained = (KIND == kIso) || (KIND == kPreint);  // _kernels.py:341
     RayResult res;
     double acc_r = 0.0, acc_g = 0.0, acc_b = 0.0, acc_a = 0.0;
@@ -427,7 +495,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1) {
                 prev_skippable = skippable;
             }
             if (b != last_hit) {
-                if (a.blocks_hit) a.blocks_hit[b] = 1;
+                if (hits) hits[b] = 1;
                 last_hit = b;
             }
             n_taken += 1;
@@ -622,19 +690,23 @@ __global__ void __launch_bounds__(kThreads, VR_RAYCAST_MIN_BLOCKS) raycast_kerne
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int lx = (warp & 1) * 8 + (lane & 7);   // 0..15 inside the 16x8 cell
     const int ly = (warp >> 1) * 4 + (lane >> 3);  // 0..7; each warp an 8x4 tile
-    const int slot = blockIdx.x;
+    const int local_view = (int)(blockIdx.x / (unsigned)a.slots);
+    const int slot = (int)(blockIdx.x - (unsigned)local_view * (unsigned)a.slots);
+    const int view = a.view0 + local_view;
     const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
     const int cx = (cell % a.cells_x) * kTileW + lx;
     const int cy = (cell / a.cells_x) * kTileH + ly;
     const bool active = cell < a.ncells && cx < a.tw && cy < a.th;
     unsigned long long taken = 0, skipped = 0, shaded = 0, evals = 0, iters = 0;
     if (active) {
-        Ray r = make_ray(a, a.tx + cx, a.ty + cy);
+        Ray r = make_ray(a, view_cam(a, view), a.tx + cx, a.ty + cy);
         double t0, t1;
         clip_to_bounds(r, a.ext_mm, t0, t1);
-        RayResult res = march<KIND, CUBIC, LIGHT, SKIP>(a, r, t0, t1);
-        const long long p = a.il_packed ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx
-                                        : (long long)cy * a.tw + cx;
+        RayResult res = march<KIND, CUBIC, LIGHT, SKIP>(
+            a, r, t0, t1, a.blocks_hit ? a.blocks_hit + (long long)view * a.nblocks : nullptr);
+        const long long p = (long long)view * a.view_pix +
+                            (a.il_packed ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx
+                                         : (long long)cy * a.tw + cx);
         if (a.premult) {
             double4 *o = reinterpret_cast<double4 *>(a.premult) + p;
             *o = make_double4(res.r, res.g, res.b, res.a);
@@ -662,8 +734,8 @@ __global__ void __launch_bounds__(kThreads, VR_RAYCAST_MIN_BLOCKS) raycast_kerne
     taken = warp_sum(taken);
     skipped = warp_sum(skipped);
     if (lane == 0 && a.totals && (taken | skipped)) {
-        atomicAdd(a.totals, taken);
-        atomicAdd(a.totals + 1, skipped);
+        atomicAdd(a.totals + 5 * (long long)view, taken);
+        atomicAdd(a.totals + 5 * (long long)view + 1, skipped);
     }
     if (a.work) {
         shaded = warp_sum(shaded);
@@ -706,6 +778,7 @@ struct PostRay {
     int nvis;      // samples composited so far
     long long out;  // output index of the pixel
     long long item; // work item (pixel) the ray came from
+    int view;       // batched views: the view the item belongs to
     bool live;
 };
 
@@ -727,24 +800,29 @@ struct HeavyRay {
 };
 static_assert(sizeof(HeavyRay) == kHeavyRayBytes, "HeavyRay layout");
 
-// Work item -> pixel.  Items are numbered cell slot by cell slot, 128 per
-// slot, each 32-item group one 8x4 warp tile (the layout of raycast_kernel).
-// (cx, cy) in the rectangle and the output index; false for padding items
-VR_D bool item_pixel(const RenderArgs &a, long long item, int &cx, int &cy, long long &out) {
+// Work item -> pixel.  Items are numbered view by view, then cell slot by cell
+// slot, 128 per slot, each 32-item group one 8x4 warp tile (the layout of
+// raycast_kernel).  (cx, cy) in the rectangle, the output index and the view;
+// false for padding items
+VR_D bool item_pixel(const RenderArgs &a, long long item, int &cx, int &cy, long long &out, int &view) {
+    const int local_view = a.nviews > 1 ? (int)(item / a.items_per_view) : 0;
+    item -= (long long)local_view * a.items_per_view;
+    view = a.view0 + local_view;
     const int slot = (int)(item >> 7), local = (int)(item & 127);
     const int w = local >> 5, l = local & 31;
     const int lx = (w & 1) * 8 + (l & 7), ly = (w >> 1) * 4 + (l >> 3);
     const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
     cx = (cell % a.cells_x) * kTileW + lx;
     cy = (cell / a.cells_x) * kTileH + ly;
-    out = a.il_packed ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx : (long long)cy * a.tw + cx;
+    out = (long long)view * a.view_pix +
+          (a.il_packed ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx : (long long)cy * a.tw + cx);
     return !(cell >= a.ncells || cx >= a.tw || cy >= a.th);
 }
 
 VR_D bool start_ray(const RenderArgs &a, long long item, PostRay &R) {
     int cx, cy;
-    if (!item_pixel(a, item, cx, cy, R.out)) return false;
-    R.r = make_ray(a, a.tx + cx, a.ty + cy);
+    if (!item_pixel(a, item, cx, cy, R.out, R.view)) return false;
+    R.r = make_ray(a, view_cam(a, R.view), a.tx + cx, a.ty + cy);
     double t0, t1;
     clip_to_bounds(R.r, a.ext_mm, t0, t1);
     R.t0 = t0;
@@ -809,13 +887,14 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
 #endif
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
-    const long long total = (long long)a.slots * (kTileW * kTileH);
+    const long long total = a.items_per_view * a.nviews;
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
     const int first_vis = a.cull ? __ldg(a.lut_range + 2) : INT_MIN;  // value thresholds (vlo, vhi)
     const int last_vis = a.cull ? __ldg(a.lut_range + 3) : INT_MAX;
     // a LUT whose first and last bins are visible can never prove a sample transparent
     const bool cull = a.cull != 0 && (first_vis > -32768 || last_vis < 32767);
-    unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
+    unsigned long long c_shaded = 0, c_eval = 0, c_iter = 0;
+    ViewTotals vt;
     PostRay R;
     R.live = false;
     bool exhausted = false;
@@ -846,10 +925,21 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
         if (__all_sync(full, !R.live && exhausted)) break;
         // the queue head is global: a warp whose lanes are all busy with long
         // rays must still learn that the queue has drained
-        int head_done = 0;
-        if (lane == 0 && a.heavy)
-            head_done = *reinterpret_cast<volatile unsigned long long *>(a.work_counter) >= (unsigned long long)total;
-        const bool drained = __shfl_sync(full, head_done, 0) != 0 || __any_sync(full, exhausted);
+        // (batched views: "drained" per view -- the queue has moved past this
+        // ray's view, so it is one of that view's tail rays)
+        unsigned long long head = 0;
+        if (lane == 0 && a.heavy) head = *reinterpret_cast<volatile unsigned long long *>(a.work_counter);
+        head = __shfl_sync(full, head, 0);
+#ifndef VR_VIEW_DRAIN
+#define VR_VIEW_DRAIN 1
+#endif
+        const unsigned long long view_end =
+            (VR_VIEW_DRAIN && a.nviews > 1)
+                ? (unsigned long long)(R.view - a.view0 + 1) * (unsigned long long)a.items_per_view
+                : (unsigned long long)total;
+        // (the vote first: the per-lane test below may differ across lanes)
+        const bool any_exhausted = __any_sync(full, exhausted);
+        const bool drained = any_exhausted || (a.heavy && head >= view_end);
 #ifdef VR_DEBUG_TIMES
         if (drained && t_drain == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_drain));
         n_trips_after += drained ? 1 : 0;
@@ -929,7 +1019,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
                 }
             }
             if (b != R.last_hit) {
-                if (a.blocks_hit) a.blocks_hit[b] = 1;
+                if (a.blocks_hit) a.blocks_hit[(long long)R.view * a.nblocks + b] = 1;
                 R.last_hit = b;
             }
             const int pt = cull ? provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis) : 0;
@@ -1028,8 +1118,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
         // ---- finish: background, epilogue, per-pixel outputs
         if (finished) {
             finish_ray(a, R.out, R.acc_r, R.acc_g, R.acc_b, R.acc_a, R.taken, R.skipped);
-            c_taken += (unsigned long long)R.taken;
-            c_skip += (unsigned long long)R.skipped;
+            vt.add(a, R.view, R.taken, R.skipped);
             R.live = false;
 #ifdef VR_DEBUG_STATS
             dbg[R.taken == 0 ? 0 : 2] += 1;
@@ -1059,12 +1148,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
         }
     }
 #endif
-    c_taken = warp_sum(c_taken);
-    c_skip = warp_sum(c_skip);
-    if (lane == 0 && a.totals && (c_taken | c_skip)) {
-        atomicAdd(a.totals, c_taken);
-        atomicAdd(a.totals + 1, c_skip);
-    }
+    vt.flush_warp(a);
     if (a.work) {
         c_shaded = warp_sum(c_shaded);
         c_eval = warp_sum(c_eval);
@@ -1124,7 +1208,8 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
     const long long n_short = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
     const long long n_long = (long long)(pushed_long < (unsigned long long)a.heavy_cap ? pushed_long : a.heavy_cap);
     const long long count = n_long + n_short;
-    unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
+    unsigned long long c_shaded = 0, c_eval = 0, c_iter = 0;
+    ViewTotals vt;
 #ifdef VR_DEBUG_TIMES
     unsigned long long t_begin, n_rays = 0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
@@ -1146,8 +1231,9 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
         PostRay R;
         {
             int cx, cy;
-            item_pixel(a, h.item, cx, cy, R.out);
+            item_pixel(a, h.item, cx, cy, R.out, R.view);
         }
+        uint8_t *hits = a.blocks_hit ? a.blocks_hit + (long long)R.view * a.nblocks : nullptr;
         R.r.ox = h.o[0];
         R.r.oy = h.o[1];
         R.r.oz = h.o[2];
@@ -1333,7 +1419,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
                 if (et_lane < 32) st[6] += 1;
             }
 #endif
-            if (is_taken && lane <= et_lane && a.blocks_hit) a.blocks_hit[b] = 1;
+            if (is_taken && lane <= et_lane && hits) hits[b] = 1;
             if (et_lane < 32) break;
             // advance; a chunk with nothing to evaluate extends by a provable run
             long long next = n + 32;
@@ -1366,8 +1452,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
         }
         if (lane == 0) {
             finish_ray(a, R.out, acc_r, acc_g, acc_b, acc_a, taken, skipped);
-            c_taken += (unsigned long long)taken;
-            c_skip += (unsigned long long)skipped;
+            vt.add(a, R.view, taken, skipped);
         }
 #ifdef VR_DEBUG_TIMES
         ++n_rays;
@@ -1392,12 +1477,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
         a.debug_times[4 * w + 3] = n_rays;
     }
 #endif
-    c_taken = warp_sum(c_taken);
-    c_skip = warp_sum(c_skip);
-    if (lane == 0 && a.totals && (c_taken | c_skip)) {
-        atomicAdd(a.totals, c_taken);
-        atomicAdd(a.totals + 1, c_skip);
-    }
+    vt.flush_warp(a);
     if (a.work) {
         c_shaded = warp_sum(c_shaded);
         c_eval = warp_sum(c_eval);
@@ -1510,23 +1590,36 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
     if (a.tw <= 0 || a.th <= 0) return cudaSuccess;
     if (a.slots <= 0) return cudaSuccess;
     if (a.mode == 0 && a.classify == 0 && a.work_counter) {
-        // persistent: enough CTAs to fill every SM at the kernel's occupancy
+        // persistent: enough CTAs to fill every SM at the kernel's occupancy.
+        // A batched sweep runs in chunks of kViewChunk views, each a
+        // per-lane pass then the cooperative pass over its handed-over rays:
+        // the hand-off queues stay bounded and every chunk's long rays are
+        // handed over as its views' items drain (per view, as in a frame).
         KernelFn k = pick_persistent(a);
+        KernelFn h = a.heavy ? pick_cooperative(a) : nullptr;
         const int sms = device_sms(), per_sm = persistent_ctas_per_sm(k);
-        long long ctas = (long long)sms * per_sm;
-        const long long most = (long long)a.slots * (kThreads / kPersistThreads);  // a warp per 32 rays at most
-        if (ctas > most) ctas = most;
-        // (the queue counters were zeroed by the frame's setup kernel)
-        cudaError_t e = launch_pdl(k, (unsigned)ctas, kPersistThreads, 0, stream, a);
-        if (e != cudaSuccess) return e;
-        if (a.heavy) {
-            KernelFn h = pick_cooperative(a);
-            e = launch_pdl(h, (unsigned)(sms * persistent_ctas_per_sm(h)), kPersistThreads, 0, stream, a);
+        const int hctas = h ? sms * persistent_ctas_per_sm(h) : 0;
+        for (int v0 = 0; v0 < a.nviews; v0 += kViewChunk) {
+            RenderArgs c = a;
+            c.view0 = a.view0 + v0;
+            c.nviews = a.nviews - v0 < kViewChunk ? a.nviews - v0 : kViewChunk;
+            if (v0 > 0) {  // the first chunk's counters were zeroed by the frame's setup kernel
+                cudaError_t e = cudaMemsetAsync(a.work_counter, 0, 4 * sizeof(unsigned long long), stream);
+                if (e != cudaSuccess) return e;
+            }
+            long long ctas = (long long)sms * per_sm;
+            const long long most = (long long)c.slots * c.nviews * (kThreads / kPersistThreads);  // a warp per 32 rays at most
+            if (ctas > most) ctas = most;
+            cudaError_t e = launch_pdl(k, (unsigned)ctas, kPersistThreads, 0, stream, c);
             if (e != cudaSuccess) return e;
+            if (h) {
+                e = launch_pdl(h, (unsigned)hctas, kPersistThreads, 0, stream, c);
+                if (e != cudaSuccess) return e;
+            }
         }
         return cudaGetLastError();
     }
-    pick(a)<<<a.slots, kThreads, 0, stream>>>(a);
+    pick(a)<<<(unsigned)((long long)a.slots * a.nviews), kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

@@ -20,6 +20,16 @@ struct RenderArgs {
     int slots;             // CTAs launched (cells rendered by this call)
     double pos[3], fwd[3], right[3], up[3];
     double half_w, half_h;
+    // batched views (a turntable sweep): nviews frames of the same size, view
+    // v's camera at views[14 v ..] = pos, fwd, right, up, half_w, half_h
+    // (device; null: the one camera above).  Work items, outputs, totals and
+    // blocks_hit are laid out view after view.
+    int nviews;                // views in this launch (view0 .. view0 + nviews - 1)
+    int view0;
+    const double *views;
+    long long items_per_view;  // slots * 128
+    long long view_pix;        // output pixels per view
+    int nblocks;               // blocks_hit entries per view
 
     // settings (render.py:361-425 resolved)
     double step, ref_step;
@@ -75,7 +85,7 @@ struct RenderArgs {
     double *depth;
     long long *taken, *skipped;
     uint8_t *blocks_hit;
-    unsigned long long *totals;  // [0] taken, [1] skipped
+    unsigned long long *totals;  // per view [5 v + 0] taken, [5 v + 1] skipped
     unsigned long long *work;    // [0] gradient evaluations, [1] interpolations, [2] loop iterations
 };
 
@@ -90,6 +100,13 @@ constexpr int kThreads = 128;
 #endif
 constexpr int kPersistThreads = VR_PERSIST_THREADS;  // CTA size of the persistent ray casters
 constexpr size_t kHeavyRayBytes = 128;  // sizeof(HeavyRay) in vr_raycast.cu
+// views per persistent launch pair of a batched sweep; measured at C5:
+// 1 (901 views/s) > 4 (844) > 16 (831) -- each view's tail rays are best
+// handed to the cooperative kernel as in a single frame
+#ifndef VR_VIEW_CHUNK
+#define VR_VIEW_CHUNK 1
+#endif
+constexpr int kViewChunk = VR_VIEW_CHUNK;
 
 cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream);
 

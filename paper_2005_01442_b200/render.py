@@ -517,6 +517,38 @@ def render(target, camera, tf: TransferFunction, settings: RenderSettings = Rend
     return img
 
 
+def render_views(target, cameras, tf: TransferFunction, settings: RenderSettings = RenderSettings(), *,
+                 device: int = 0) -> list:
+    """Render a batch of views -- e.g. the viewer's 360-view turntable
+    (frontend/src/camera.ts:35-44) -- in one submission: the TF visibility is
+    computed once and one persistent ray-cast pass serves every view.  Returns
+    one ImageRGBA per camera, each equal to render(target, camera, tf, settings)."""
+    cameras = list(cameras)
+    t_start = time.perf_counter()
+    settings = as_settings(settings)
+    if isinstance(target, BlockGrid) or (not hasattr(target, "values") and hasattr(target, "block_size")):
+        settings = RenderSettings(**{**settings.__dict__, "use_blocks": True, "block_size": int(target.block_size),
+                                     "overlap": int(target.overlap)})
+        target = target.volume
+    r = Renderer(as_volume(target), cameras[0], tf, settings, device=device, views=len(cameras))
+    r.set_views(cameras)
+    r.render_async()
+    pixels = r.pixels.cpu().numpy()
+    depth = r.depth.cpu().numpy() if r.depth is not None else None
+    per_view = r.view_stats()
+    errors = r.totals.cpu().tolist()[4::5][:len(cameras)]
+    if settings.use_blocks and any(errors):
+        raise EmptyBlock(f"{max(errors)} block(s) pass the interval test without a visible voxel")
+    wall = time.perf_counter() - t_start
+    H, W = r.cam.tile_h, r.cam.tile_w
+    out = []
+    for v, st in enumerate(per_view):
+        px = pixels[v] if len(cameras) > 1 else pixels
+        dv = (depth[v] if len(cameras) > 1 else depth).reshape(H, W) if depth is not None else None
+        out.append(ImageRGBA(pixels=px, stats=RenderStats(wall_time_s=wall / len(cameras), **st), depth=dv))
+    return out
+
+
 class Renderer:
     """Device-resident renderer: volume and grid in HBM, tables and outputs
     as torch CUDA tensors, asynchronous on a CUDA stream.  One frame is one
@@ -525,7 +557,7 @@ class Renderer:
 
     def __init__(self, volume, camera, tf: TransferFunction, settings: RenderSettings = RenderSettings(),
                  *, device: int = 0, tile=None, interleave=None, keep_premultiplied: bool = False,
-                 per_pixel_counts: bool = False, time_kernel: bool = False, frame_out=None):
+                 per_pixel_counts: bool = False, time_kernel: bool = False, frame_out=None, views: int = 1):
         import torch
 
         settings = as_settings(settings)
@@ -568,10 +600,17 @@ class Renderer:
         # GPU's memory mapped here (distributed.SharedFrame) -- that this
         # rank's interleaved cells are stored into at their frame positions
         self.frame_out = frame_out
+        # views > 1: a batch of views of the same frame size rendered by one
+        # vr_render_views call (set_views); outputs gain a leading view axis
+        self.nviews = int(views)
+        if self.nviews < 1 or (self.nviews > 1 and frame_out is not None):
+            raise ValueError("views must be >= 1 (and batched views cannot store into frame_out)")
+        self.view_table = None
         self.set_camera(camera, tile)
         nblocks = self.dgrid.count if self.dgrid else 1
         n = output_pixels(self.cam)
         self.npix = n
+        V = self.nviews
         if frame_out is not None:
             if tuple(frame_out.shape) != (self.cam.tile_h, self.cam.tile_w, 4) or frame_out.dtype != torch.uint8:
                 raise ValueError(f"frame_out must be a ({self.cam.tile_h}, {self.cam.tile_w}, 4) uint8 tensor")
@@ -579,13 +618,15 @@ class Renderer:
         else:
             shape = (self.cam.tile_h, self.cam.tile_w, 4) if n == self.cam.tile_h * self.cam.tile_w and not (
                 interleave and interleave[0] > 1) else (n, 4)
-            self.pixels = torch.empty(shape, dtype=torch.uint8, device=self.device)
-        self.premult = torch.empty((n, 4), dtype=torch.float64, device=self.device) if keep_premultiplied else None
-        self.depth = torch.empty(n, dtype=torch.float64, device=self.device) if settings.mode == "isosurface" else None
-        self.taken = torch.empty(n, dtype=torch.int64, device=self.device) if per_pixel_counts else None
-        self.skipped = torch.empty(n, dtype=torch.int64, device=self.device) if per_pixel_counts else None
-        self.blocks_hit = torch.empty(nblocks, dtype=torch.uint8, device=self.device)
-        self.totals = torch.zeros(8, dtype=torch.int64, device=self.device)
+            self.pixels = torch.empty(((V,) if V > 1 else ()) + shape, dtype=torch.uint8, device=self.device)
+        lead = (V, n) if V > 1 else (n,)
+        self.premult = torch.empty(lead + (4,), dtype=torch.float64, device=self.device) if keep_premultiplied else None
+        self.depth = torch.empty(lead, dtype=torch.float64, device=self.device) if settings.mode == "isosurface" else None
+        self.taken = torch.empty(lead, dtype=torch.int64, device=self.device) if per_pixel_counts else None
+        self.skipped = torch.empty(lead, dtype=torch.int64, device=self.device) if per_pixel_counts else None
+        self.blocks_hit = torch.empty(V * nblocks, dtype=torch.uint8, device=self.device)
+        # per view [taken, skipped, blocks_visited, blocks_empty, empty-block errors], then work[3]
+        self.totals = torch.zeros(5 * V + 3, dtype=torch.int64, device=self.device)
         self._events = None
         if time_kernel:
             evs = []
@@ -628,7 +669,7 @@ class Renderer:
         o.skipped = _lib.ptr(self.skipped).value
         o.blocks_hit = _lib.ptr(self.blocks_hit).value
         o.totals = self.totals.data_ptr()
-        o.work = self.totals.data_ptr() + 5 * 8
+        o.work = self.totals.data_ptr() + 5 * self.nviews * 8
         if self._events:
             o.ev_start, o.ev_stop = self._events[0].value, self._events[1].value
         return o
@@ -638,13 +679,52 @@ class Renderer:
         torch = self.torch
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         out = self.outputs()  # (totals / work / blocks_hit are zeroed by vr_render itself)
+        if self.nviews > 1:
+            if self.view_table is None:
+                raise ValueError("batched Renderer: call set_views(cameras) first")
+            _lib.check(_lib.load().vr_render_views(
+                self.dvol.handle, self.dgrid.handle if self.dgrid else None, ctypes.byref(self.cam),
+                _lib.ptr(self.view_table), self.nviews, ctypes.byref(self.res.params), _lib.ptr(self.lut),
+                _lib.ptr(self.table), _lib.ptr(self.rgba), ctypes.byref(out), _lib.ptr_stream(s)))
+            return
         _lib.check(_lib.load().vr_render(
             self.dvol.handle, self.dgrid.handle if self.dgrid else None, ctypes.byref(self.cam),
             ctypes.byref(self.res.params), _lib.ptr(self.lut), _lib.ptr(self.table), _lib.ptr(self.rgba),
             ctypes.byref(out), _lib.ptr_stream(s)))
 
+    def set_views(self, cameras, tile=None):
+        """The batch's cameras (len == views, all of the frame's size and
+        projection): a (views, 14) float64 device table of position, basis and
+        half extents, as vr_render_views reads it."""
+        cams = [as_camera(c) for c in cameras]
+        if len(cams) != self.nviews:
+            raise ValueError(f"expected {self.nviews} cameras, got {len(cams)}")
+        rows = []
+        for c in cams:
+            cs = camera_struct(c, tile, self.interleave)
+            if (cs.width, cs.height, cs.projection) != (self.cam.width, self.cam.height, self.cam.projection):
+                raise ValueError("every view must have the frame's size and projection")
+            rows.append([*cs.position, *cs.fwd, *cs.right, *cs.up, cs.half_w, cs.half_h])
+        table = self.torch.tensor(rows, dtype=self.torch.float64)
+        self.view_table = table.to(self.device)
+        self.cameras = cams
+
+    def view_stats(self) -> list:
+        """Per-view RenderStats fields of the last batch (synchronising)."""
+        t = self.totals.cpu().tolist()
+        nb = self.dgrid.count if self.dgrid else 1
+        rays = self.cam.tile_w * self.cam.tile_h if not self.interleave else self.npix
+        return [{"rays": rays, "samples_taken": t[5 * v], "samples_skipped": t[5 * v + 1],
+                 "blocks_total": nb, "blocks_empty": t[5 * v + 3], "blocks_visited": t[5 * v + 2]}
+                for v in range(self.nviews)]
+
     def stats(self) -> dict:
         t = self.totals.cpu().tolist()
+        V = self.nviews
+        if V > 1:  # the batch: sums over views; the last view's block counts
+            w = t[5 * V:]
+            t = [sum(t[5 * v] for v in range(V)), sum(t[5 * v + 1] for v in range(V)), t[5 * V - 3],
+                 t[5 * V - 2], t[5 * V - 1], *w]
         return {"samples_taken": t[0], "samples_skipped": t[1], "blocks_visited": t[2],
                 "blocks_empty": t[3], "empty_block_errors": t[4], "shaded": t[5],
                 "interpolated": t[6], "march_iterations": t[7],

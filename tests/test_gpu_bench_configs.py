@@ -156,3 +156,65 @@ def test_full_frame_stats(vr, key):
     vol = _volume(vr, dims)
     img = vr.render(vol, _centered(vr, dims, size), vr.get_preset(tfname), vr.RenderSettings(**kw))
     assert (img.stats.samples_taken, img.stats.samples_skipped) == (taken, skipped)
+
+
+# ------------------------------------------------ batched views (C5 sweep)
+
+
+@pytest.mark.parametrize("mode", ["post_blocks", "post_mono", "preint", "iso"])
+def test_batched_views_equal_single_renders(vr, mode):
+    """render_views (one vr_render_views submission, one TF visibility, one
+    persistent pass over every view's rays) == render() per camera: pixels,
+    premultiplied floats, per-pixel counts and per-view stats."""
+    dims = (96, 80, 72)
+    vol = vr.generate_phantom("torso", dims)
+    kw = {"post_blocks": dict(interpolation="tricubic", use_blocks=True, block_size=32),
+          "post_mono": dict(interpolation="tricubic"),
+          "preint": dict(interpolation="trilinear", classification="preintegrated", use_blocks=True, block_size=32),
+          "iso": dict(interpolation="tricubic", mode="isosurface", isovalue=500.0)}[mode]
+    s = vr.RenderSettings(**kw)
+    tf = vr.get_preset("bone")
+    cams = [_orbit(vr, dims, 64, k, views=12, elevation_deg=e) for k, e in
+            [(0, 0.0), (1, 0.0), (2, 20.0), (3, 0.0), (5, -30.0), (7, 0.0), (11, 10.0)]]
+    r = vr.Renderer(vol, cams[0], tf, s, views=len(cams), keep_premultiplied=True, per_pixel_counts=True)
+    r.set_views(cams)
+    r.render_async()
+    per_view = r.view_stats()
+    imgs = vr.render_views(vol, cams, tf, s)
+    for v, cam in enumerate(cams):
+        one = vr.Renderer(vol, cam, tf, s, keep_premultiplied=True, per_pixel_counts=True)
+        one.render_async()
+        assert np.array_equal(r.pixels[v].cpu().numpy(), one.pixels.cpu().numpy()), v
+        assert np.array_equal(r.premult[v].cpu().numpy(), one.premult.cpu().numpy()), v
+        assert np.array_equal(r.taken[v].cpu().numpy(), one.taken.cpu().numpy()), v
+        assert np.array_equal(r.skipped[v].cpu().numpy(), one.skipped.cpu().numpy()), v
+        st = one.stats()
+        assert (per_view[v]["samples_taken"], per_view[v]["samples_skipped"], per_view[v]["blocks_visited"]) == (
+            st["samples_taken"], st["samples_skipped"], st["blocks_visited"]), v
+        ref = vr.render(vol, cam, tf, s)
+        assert np.array_equal(imgs[v].pixels, ref.pixels), v
+        assert imgs[v].stats.samples_taken == ref.stats.samples_taken
+        assert imgs[v].stats.blocks_visited == ref.stats.blocks_visited
+        if mode == "iso":
+            assert np.array_equal(np.isnan(imgs[v].depth), np.isnan(ref.depth))
+
+
+def test_turntable_sweep_views_match_oracle(vr):
+    """A 24-view C3 sweep in one submission; sampled views bit-exact vs the oracle."""
+    from oracle import oracle as O
+
+    dims = (512, 512, 512)
+    vol = _volume(vr, dims)
+    tf = vr.get_preset("bone")
+    s = vr.RenderSettings(interpolation="tricubic", use_blocks=True)
+    cams = [_orbit(vr, dims, 1024, k, views=24) for k in range(24)]
+    r = vr.Renderer(vol, cams[0], tf, s, views=24, keep_premultiplied=True)
+    r.set_views(cams)
+    r.render_async()
+    per_view = r.view_stats()
+    for v in (0, 5, 13):
+        ref = O.render(vol.values, vol.spacing, cams[v], tf.values, tf.rgba, tf.domain, s)
+        assert np.array_equal(r.premult[v].cpu().numpy(), ref.out), v
+        assert np.array_equal(r.pixels[v].cpu().numpy(), ref.pixels), v
+        assert (per_view[v]["samples_taken"], per_view[v]["samples_skipped"], per_view[v]["blocks_visited"]) == (
+            ref.samples_taken, ref.samples_skipped, ref.blocks_visited), v
