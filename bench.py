@@ -208,7 +208,8 @@ def committed_ncu(config):
     except Exception:
         return None
     return {k: d[k] for k in ("source", "kernels", "dram_bytes_per_launch", "issue_active_pct",
-                              "fp64_pipe_pct", "l1_hit_pct", "l2_hit_pct", "warps_active_pct") if k in d}
+                              "fp64_pipe_pct", "l1_hit_pct", "l2_hit_pct", "warps_active_pct", "per_kernel")
+            if k in d}
 
 
 def dist_setup(n, backend):

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -147,15 +148,21 @@ struct Scratch {
     }
 };
 
+// The device's default memory pool keeps up to 2 GiB of freed stream-ordered
+// scratch (hand-off queues, inside-bit arrays, per-call staging) cached
+// across frames instead of returning it to the driver at every sync; beyond
+// that, freed memory goes back.
 void configure_pool(int device) {
-    static bool done[64] = {false};
-    if (device < 0 || device >= 64 || done[device]) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;  // keep freed blocks cached across frames
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done[device] = true;
+    static std::once_flag once[64];
+    if (device < 0 || device >= 64) return;
+    std::call_once(once[device], [device] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = 2ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+    });
 }
 
 bool finite_positive(double v) { return std::isfinite(v) && v > 0.0; }
@@ -765,6 +772,28 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.nmx = vol->nmx;
         a.nmy = vol->nmy;
     }
+    // chained modes (iso, pre-integrated): transparency culling of runs
+    const bool chained_cull = vol->cells && !post &&
+                              (a.mode == VR_MODE_ISO || (a.mode == VR_MODE_DVR && a.classify == VR_CLS_PREINT));
+    Scratch tbl_nz(s);
+    if (chained_cull) {
+        a.cells = vol->cells;
+        a.ncx = vol->ncx;
+        a.ncy = vol->ncy;
+#ifndef VR_NO_CUBES
+        a.cubes = vol->cubes;
+#endif
+#ifndef VR_NO_MACRO
+        a.mcells = vol->mcells;
+#endif
+        a.nmx = vol->nmx;
+        a.nmy = vol->nmy;
+        a.cull = 1;
+        if (a.mode == VR_MODE_DVR) {
+            VR_CUDA(tbl_nz.alloc(sizeof(int) * (size_t)(a.ntbl + 1) * (a.ntbl + 1)));
+            a.tbl_nz = (const int *)tbl_nz.p;
+        }
+    }
     VisScratch vs(s);
     if (grid) {
         VR_CUDA(vs.init(grid, lut, prm->nlut, prm->lut_lo, prm->lut_hi, prm->margin, false));
@@ -784,6 +813,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
             if (zero.n[k]) VR_CUDA(cudaMemsetAsync(zero.p[k], 0, sizeof(unsigned long long) * zero.n[k], s));
         if (zero.nb) VR_CUDA(cudaMemsetAsync(zero.b, 0, zero.nb, s));
     }
+    if (a.tbl_nz) VR_CUDA(vr::launch_tbl_nonzero(a.table, a.ntbl, (int *)tbl_nz.p, s));
 #ifdef VR_DEBUG_TIMES
     a.debug_times = g_debug_times;
 #endif
@@ -802,6 +832,7 @@ int vr_render(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_rend
               const double *table, const uint8_t *rgba, const vr_render_outputs *out, void *stream) {
     if (!vol) return fail(VR_EINVALID, "null volume");
     DeviceGuard g(vol->device);
+    configure_pool(vol->device);  // stream-ordered scratch stays cached across calls
     return render_impl(vol, grid, cam, prm, lut, table, rgba, out, (cudaStream_t)stream);
 }
 
@@ -813,6 +844,7 @@ int vr_render_views(vr_volume *vol, vr_grid *grid, const vr_camera *frame, const
     if (frame && frame->interleave_n > 1 && frame->interleave_frame)
         return fail(VR_EINVALID, "views: interleave_frame is not supported for batched views");
     DeviceGuard g(vol->device);
+    configure_pool(vol->device);  // stream-ordered scratch stays cached across calls
     return render_impl(vol, grid, frame, prm, lut, table, rgba, out, (cudaStream_t)stream, views, nviews);
 }
 
@@ -918,6 +950,7 @@ int vr_threshold_count(const vr_volume *vol, int32_t thr, uint64_t *count, void 
 int vr_threshold_measure(const vr_volume *vol, int32_t thr, uint64_t *out, void *stream) {
     if (!vol || !out) return fail(VR_EINVALID, "null pointer");
     DeviceGuard g(vol->device);
+    configure_pool(vol->device);  // stream-ordered scratch stays cached across calls
     VR_CUDA(vr::launch_threshold_measure(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, vol->sx, vol->sy,
                                          vol->sz, thr, (unsigned long long *)out, (cudaStream_t)stream));
     return VR_OK;
@@ -928,6 +961,7 @@ int vr_ball_measure(const vr_volume *vol, int32_t thr, const double *centres, co
     if (!vol || (nballs > 0 && (!centres || !radii || !counts))) return fail(VR_EINVALID, "null pointer");
     if (nballs < 0 || nballs > (1 << 30)) return fail(VR_EINVALID, "ball count out of range");
     DeviceGuard g(vol->device);
+    configure_pool(vol->device);  // stream-ordered scratch stays cached across calls
     VR_CUDA(vr::launch_ball_measure(vol->data, (int)vol->nx, (int)vol->ny, (int)vol->nz, vol->sx, vol->sy, vol->sz,
                                     thr, centres, radii, (int)nballs, (unsigned long long *)counts,
                                     (unsigned long long *)area_fx, (cudaStream_t)stream));

@@ -686,6 +686,28 @@ __global__ void count_hits_kernel(const uint8_t *hits, int n, unsigned long long
     }
 }
 
+// ------------------------------------------- pre-integrated culling table
+// nz[i * (n+1) + j] = number of table cells (front f < i, back b < j) with
+// opacity > 0 (table (n, n, 4) float64, render.py:425): the square of bins
+// [i0, i1)^2 is transparent iff its four-corner difference is 0.  One CTA:
+// row prefixes, then column prefixes.
+__global__ void tbl_nonzero_kernel(const double *table, int n, int *nz) {
+    pdl_enter();
+    const int w = n + 1;
+    for (int i = threadIdx.x; i < w; i += blockDim.x) nz[i] = 0;  // row 0
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int run = 0;
+        nz[(i + 1) * w] = 0;
+        for (int j = 0; j < n; ++j) {
+            run += __ldg(table + 4 * ((long long)i * n + j) + 3) > 0.0 ? 1 : 0;
+            nz[(i + 1) * w + j + 1] = run;
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < w; j += blockDim.x)
+        for (int i = 1; i < w; ++i) nz[i * w + j] += nz[(i - 1) * w + j];
+}
+
 // --------------------------------------------------------- preclassify
 
 __global__ void __launch_bounds__(kBlock) preclassify_kernel(const int16_t *__restrict__ vol, long long n,
@@ -911,6 +933,12 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
 cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double lut_inv_w, int *range,
                              const ZeroSpec &zero, cudaStream_t s) {
     cudaError_t e = launch_pdl(lut_range_kernel, 1, kSetupThreads, 0, s, lut, nbins, lut_lo, lut_inv_w, range, zero);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tbl_nonzero(const double *table, int n, int *nz, cudaStream_t s) {
+    cudaError_t e = launch_pdl(tbl_nonzero_kernel, 1, 1024, 0, s, table, n, nz);
     if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }

@@ -297,6 +297,44 @@ VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z,
     return bounds_transparent(w, vlo, vhi) ? 2 : 0;
 }
 
+// Chained modes (iso, pre-integrated), the analogue of provably_transparent:
+// the level (3 macro cell, 1 cell, 2 unit cube; 0 none) of the largest
+// region around (x, y, z) whose interpolant bound [lo, hi] guarantees that
+// consecutive samples inside it change nothing the reference composites:
+//  - iso: the bound excludes the isovalue, so every sample lies strictly on
+//    one side -- no sign change, no exact hit (_kernels.py:446-465);
+//  - pre-integrated: every table cell (front bin, back bin) with both bins in
+//    [bin(lo), bin(hi)] has zero opacity (_kernels.py:555-558: seg_a == 0,
+//    nothing composited).  a.tbl_nz is the 2-D prefix count of cells with
+//    alpha > 0, so the square test is four lookups.
+template <int KIND>
+VR_D bool chain_bound_ok(const RenderArgs &a, short2 b) {
+    if (b.x <= -32768 || b.y >= 32767) return false;  // saturated: unbounded
+    if (KIND == kIso) return (double)b.y < a.isovalue || (double)b.x > a.isovalue;
+    const int i0 = lut_bin((double)b.x, a.tbl_lo, a.tbl_inv_w, a.ntbl);
+    const int i1 = lut_bin((double)b.y, a.tbl_lo, a.tbl_inv_w, a.ntbl) + 1;
+    const long long w = a.ntbl + 1;
+    const int cnt = __ldg(a.tbl_nz + i1 * w + i1) - __ldg(a.tbl_nz + i0 * w + i1) - __ldg(a.tbl_nz + i1 * w + i0) +
+                    __ldg(a.tbl_nz + i0 * w + i0);
+    return cnt == 0;
+}
+
+template <int KIND>
+VR_D int chain_transparent(const RenderArgs &a, double x, double y, double z) {
+    const int gx = clampi((int)x, 0, a.L.n[0] - 1);
+    const int gy = clampi((int)y, 0, a.L.n[1] - 1);
+    const int gz = clampi((int)z, 0, a.L.n[2] - 1);
+    if (a.mcells &&
+        chain_bound_ok<KIND>(a, __ldg(a.mcells + ((long long)(gz >> 4) * a.nmy + (gy >> 4)) * a.nmx + (gx >> 4))))
+        return 3;
+    if (chain_bound_ok<KIND>(a, __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2))))
+        return 1;
+    if (!a.cubes) return 0;
+    const short2 w = __ldg(a.cubes + (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
+                           ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3));
+    return chain_bound_ok<KIND>(a, w) ? 2 : 0;
+}
+
 // Parameter interval in which the (exact) ray lies inside the box [lo, hi]
 // expanded by delta on every side; returns false when it never does.  For an
 // axis the ray does not move along, the computed coordinate is exactly
@@ -385,7 +423,7 @@ VR_D long long leap_count(const RenderArgs &a, const Ray &r, const double inv[3]
 // the skip predicate stays false).  Computed positions are monotone in n, so
 // only the exit side of each interval needs the delta guard; the one-sample
 // slack absorbs the rounding of t.
-template <bool SKIP>
+template <bool SKIP, bool BOX = true>
 VR_D long long culled_run(const RenderArgs &a, const Ray &r, const double inv[3], double t0, long long n, double t,
                           const double p[3], const int bidx[3], const BlockRec &rec, int shift) {
     const double delta = 1e-6;
@@ -409,10 +447,12 @@ VR_D long long culled_run(const RenderArgs &a, const Ray &r, const double inv[3]
                 double X = (1.0 + (double)(bidx[k] * a.L.stride)) + delta;
                 t_safe = dmin(t_safe, (X * s[k] - o[k]) * inv[k]);
             }
-            const float lo_k = k == 0 ? rec.lo.x : (k == 1 ? rec.lo.y : rec.lo.z);
-            const float hi_k = k == 0 ? rec.hi.x : (k == 1 ? rec.hi.y : rec.hi.z);
-            const double edge = d[k] > 0.0 ? (double)hi_k - delta : (double)lo_k + delta;
-            t_safe = dmin(t_safe, (edge * s[k] - o[k]) * inv[k]);
+            if (BOX) {  // (iso's skip predicate is per block, without a box)
+                const float lo_k = k == 0 ? rec.lo.x : (k == 1 ? rec.lo.y : rec.lo.z);
+                const float hi_k = k == 0 ? rec.hi.x : (k == 1 ? rec.hi.y : rec.hi.z);
+                const double edge = d[k] > 0.0 ? (double)hi_k - delta : (double)lo_k + delta;
+                t_safe = dmin(t_safe, (edge * s[k] - o[k]) * inv[k]);
+            }
         }
     }
     if (!(t_safe > t)) return 1;
@@ -447,7 +487,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
         while (N > 0 && (t0 + ((double)(N - 1) + 0.5) * step) > t1) --N;
         const int nbx = a.L.nb[0], nby = a.L.nb[1];
         double inv[3] = {0.0, 0.0, 0.0};
-        if (SKIP || (KIND == kPost && a.cull)) {
+        if (SKIP || a.cull) {
             inv[0] = r.dx != 0.0 ? 1.0 / r.dx : 0.0;
             inv[1] = r.dy != 0.0 ? 1.0 / r.dy : 0.0;
             inv[2] = r.dz != 0.0 ? 1.0 / r.dz : 0.0;
@@ -457,6 +497,11 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
         int last_hit = -1;
         int first_vis = INT_MIN, last_vis = INT_MAX;  // value thresholds (vlo, vhi)
         const bool cull = KIND == kPost && a.cull;
+        // chained modes: after a culled run the previous sample's value was not
+        // computed; the next evaluated sample recomputes it at that sample's
+        // own position (the reference interpolated it there)
+        const bool chain_cull = (KIND == kIso || KIND == kPreint) && a.cull;
+        bool prev_pending = false;
         if (cull) {
             first_vis = __ldg(a.lut_range + 2);
             last_vis = __ldg(a.lut_range + 3);
@@ -489,6 +534,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
                     n_skip += m - n;
                     n = m;
                     prev_valid = false;
+                    prev_pending = false;
                     prev_skippable = true;
                     continue;
                 }
@@ -500,6 +546,14 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
             }
             n_taken += 1;
 
+            if (chain_cull && prev_pending) {
+                // sample n-1 was taken inside a culled run: its exact value
+                const double tq = t0 + ((double)(n - 1) + 0.5) * step;
+                prev_s = attr_sample<CUBIC>(a, divide(r.ox + tq * r.dx, a.dsx), divide(r.oy + tq * r.dy, a.dsy),
+                                            divide(r.oz + tq * r.dz, a.dsz));
+                prev_valid = true;
+                prev_pending = false;
+            }
             if (KIND == kIso) {
                 // _kernels.py:405-468
                 double s = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
@@ -552,6 +606,26 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
                 }
                 prev_s = s;
                 prev_valid = true;
+                // (not from a skippable sample taken as the first of a gap: the
+                // reference skips the samples after it)
+                if (chain_cull && !prev_skippable) {
+                    // samples n+1 .. n+k-1 lie in the region of sample n, whose
+                    // bound excludes the isovalue: no sign change, no hit
+                    const int lvl = chain_transparent<kIso>(a, x, y, z);
+                    if (lvl) {
+                        const double p[3] = {x, y, z};
+                        const int bidx[3] = {bi, bj, bk};
+                        long long k = culled_run<SKIP, false>(a, r, inv, t0, n, t, p, bidx, rec,
+                                                             lvl == 3 ? 4 : lvl == 1 ? 2 : 0);
+                        if (k > N - n) k = N - n;
+                        if (k > 1) {
+                            n_taken += k - 1;
+                            n += k;
+                            prev_pending = true;
+                            continue;
+                        }
+                    }
+                }
             } else if (KIND == kPre) {
                 // pre-classified (_kernels.py:471-507)
                 double sa = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 3);
@@ -648,6 +722,24 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
                 }
                 prev_s = s;
                 prev_valid = true;
+                if (chain_cull && !prev_skippable) {
+                    // samples n+1 .. n+k-1 lie in the region of sample n, every
+                    // segment between two of them has zero opacity
+                    const int lvl = chain_transparent<kPreint>(a, x, y, z);
+                    if (lvl) {
+                        const double p[3] = {x, y, z};
+                        const int bidx[3] = {bi, bj, bk};
+                        long long k = culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, rec,
+                                                       lvl == 3 ? 4 : lvl == 1 ? 2 : 0);
+                        if (k > N - n) k = N - n;
+                        if (k > 1) {
+                            n_taken += k - 1;
+                            n += k;
+                            prev_pending = true;
+                            continue;
+                        }
+                    }
+                }
             }
             ++n;
         }
@@ -804,25 +896,27 @@ static_assert(sizeof(HeavyRay) == kHeavyRayBytes, "HeavyRay layout");
 // slot, 128 per slot, each 32-item group one 8x4 warp tile (the layout of
 // raycast_kernel).  (cx, cy) in the rectangle, the output index and the view;
 // false for padding items
+template <bool MV>
 VR_D bool item_pixel(const RenderArgs &a, long long item, int &cx, int &cy, long long &out, int &view) {
-    const int local_view = a.nviews > 1 ? (int)(item / a.items_per_view) : 0;
+    const int local_view = MV ? (int)(item / a.items_per_view) : 0;
     item -= (long long)local_view * a.items_per_view;
-    view = a.view0 + local_view;
+    view = MV ? a.view0 + local_view : 0;
     const int slot = (int)(item >> 7), local = (int)(item & 127);
     const int w = local >> 5, l = local & 31;
     const int lx = (w & 1) * 8 + (l & 7), ly = (w >> 1) * 4 + (l >> 3);
     const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
     cx = (cell % a.cells_x) * kTileW + lx;
     cy = (cell / a.cells_x) * kTileH + ly;
-    out = (long long)view * a.view_pix +
+    out = (MV ? (long long)view * a.view_pix : 0ll) +
           (a.il_packed ? (long long)slot * (kTileW * kTileH) + ly * kTileW + lx : (long long)cy * a.tw + cx);
     return !(cell >= a.ncells || cx >= a.tw || cy >= a.th);
 }
 
+template <bool MV>
 VR_D bool start_ray(const RenderArgs &a, long long item, PostRay &R) {
     int cx, cy;
-    if (!item_pixel(a, item, cx, cy, R.out, R.view)) return false;
-    R.r = make_ray(a, view_cam(a, R.view), a.tx + cx, a.ty + cy);
+    if (!item_pixel<MV>(a, item, cx, cy, R.out, R.view)) return false;
+    R.r = make_ray(a, MV ? view_cam(a, R.view) : view_cam(a, 0), a.tx + cx, a.ty + cy);
     double t0, t1;
     clip_to_bounds(R.r, a.ext_mm, t0, t1);
     R.t0 = t0;
@@ -874,7 +968,9 @@ VR_D void finish_ray(const RenderArgs &a, long long p, double acc_r, double acc_
     if (a.skipped) a.skipped[p] = skipped;
 }
 
-template <bool CUBIC, bool LIGHT, bool SKIP>
+// MV: batched views (vr_render_views); the single-frame instantiation carries
+// no per-view indexing in its hot loop
+template <bool CUBIC, bool LIGHT, bool SKIP, bool MV>
 #ifndef VR_POST_MIN_BLOCKS
 #define VR_POST_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (latency-bound; swept 1..5)
 #endif
@@ -893,10 +989,11 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
     const int last_vis = a.cull ? __ldg(a.lut_range + 3) : INT_MAX;
     // a LUT whose first and last bins are visible can never prove a sample transparent
     const bool cull = a.cull != 0 && (first_vis > -32768 || last_vis < 32767);
-    unsigned long long c_shaded = 0, c_eval = 0, c_iter = 0;
+    unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
     ViewTotals vt;
     PostRay R;
     R.live = false;
+    R.view = 0;
     bool exhausted = false;
     // no more rays than lanes (the grid is capped at one lane per ray)
     const bool starved = total <= (long long)gridDim.x * blockDim.x;
@@ -919,7 +1016,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
                 if (item >= total)
                     exhausted = true;
                 else
-                    start_ray(a, item, R);
+                    start_ray<MV>(a, item, R);
             }
         }
         if (__all_sync(full, !R.live && exhausted)) break;
@@ -927,19 +1024,22 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
         // rays must still learn that the queue has drained
         // (batched views: "drained" per view -- the queue has moved past this
         // ray's view, so it is one of that view's tail rays)
-        unsigned long long head = 0;
-        if (lane == 0 && a.heavy) head = *reinterpret_cast<volatile unsigned long long *>(a.work_counter);
-        head = __shfl_sync(full, head, 0);
-#ifndef VR_VIEW_DRAIN
-#define VR_VIEW_DRAIN 1
-#endif
-        const unsigned long long view_end =
-            (VR_VIEW_DRAIN && a.nviews > 1)
-                ? (unsigned long long)(R.view - a.view0 + 1) * (unsigned long long)a.items_per_view
-                : (unsigned long long)total;
-        // (the vote first: the per-lane test below may differ across lanes)
-        const bool any_exhausted = __any_sync(full, exhausted);
-        const bool drained = any_exhausted || (a.heavy && head >= view_end);
+        bool drained;
+        if (MV) {
+            unsigned long long head = 0;
+            if (lane == 0 && a.heavy) head = *reinterpret_cast<volatile unsigned long long *>(a.work_counter);
+            head = __shfl_sync(full, head, 0);
+            const unsigned long long view_end =
+                (unsigned long long)(R.view - a.view0 + 1) * (unsigned long long)a.items_per_view;
+            // (the vote first: the per-lane test below may differ across lanes)
+            const bool any_exhausted = __any_sync(full, exhausted);
+            drained = any_exhausted || (a.heavy && head >= view_end);
+        } else {
+            int head_done = 0;
+            if (lane == 0 && a.heavy)
+                head_done = *reinterpret_cast<volatile unsigned long long *>(a.work_counter) >= (unsigned long long)total;
+            drained = __shfl_sync(full, head_done, 0) != 0 || __any_sync(full, exhausted);
+        }
 #ifdef VR_DEBUG_TIMES
         if (drained && t_drain == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_drain));
         n_trips_after += drained ? 1 : 0;
@@ -1019,7 +1119,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
                 }
             }
             if (b != R.last_hit) {
-                if (a.blocks_hit) a.blocks_hit[(long long)R.view * a.nblocks + b] = 1;
+                if (a.blocks_hit) a.blocks_hit[(MV ? (long long)R.view * a.nblocks : 0ll) + b] = 1;
                 R.last_hit = b;
             }
             const int pt = cull ? provably_transparent<CUBIC>(a, x, y, z, first_vis, last_vis) : 0;
@@ -1118,7 +1218,12 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
         // ---- finish: background, epilogue, per-pixel outputs
         if (finished) {
             finish_ray(a, R.out, R.acc_r, R.acc_g, R.acc_b, R.acc_a, R.taken, R.skipped);
-            vt.add(a, R.view, R.taken, R.skipped);
+            if (MV) {
+                vt.add(a, R.view, R.taken, R.skipped);
+            } else {
+                c_taken += (unsigned long long)R.taken;
+                c_skip += (unsigned long long)R.skipped;
+            }
             R.live = false;
 #ifdef VR_DEBUG_STATS
             dbg[R.taken == 0 ? 0 : 2] += 1;
@@ -1148,7 +1253,16 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
         }
     }
 #endif
-    vt.flush_warp(a);
+    if (MV) {
+        vt.flush_warp(a);
+    } else {
+        c_taken = warp_sum(c_taken);
+        c_skip = warp_sum(c_skip);
+        if (lane == 0 && a.totals && (c_taken | c_skip)) {
+            atomicAdd(a.totals, c_taken);
+            atomicAdd(a.totals + 1, c_skip);
+        }
+    }
     if (a.work) {
         c_shaded = warp_sum(c_shaded);
         c_eval = warp_sum(c_eval);
@@ -1190,7 +1304,7 @@ VR_D int nth_bit(unsigned m, int k) {
     return pos;
 }
 
-template <bool CUBIC, bool LIGHT, bool SKIP>
+template <bool CUBIC, bool LIGHT, bool SKIP, bool MV>
 #ifndef VR_HEAVY_MIN_BLOCKS
 #define VR_HEAVY_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (swept 3..8 with phase-A cap 32)
 #endif
@@ -1208,7 +1322,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
     const long long n_short = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
     const long long n_long = (long long)(pushed_long < (unsigned long long)a.heavy_cap ? pushed_long : a.heavy_cap);
     const long long count = n_long + n_short;
-    unsigned long long c_shaded = 0, c_eval = 0, c_iter = 0;
+    unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
     ViewTotals vt;
 #ifdef VR_DEBUG_TIMES
     unsigned long long t_begin, n_rays = 0;
@@ -1231,9 +1345,9 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
         PostRay R;
         {
             int cx, cy;
-            item_pixel(a, h.item, cx, cy, R.out, R.view);
+            item_pixel<MV>(a, h.item, cx, cy, R.out, R.view);
         }
-        uint8_t *hits = a.blocks_hit ? a.blocks_hit + (long long)R.view * a.nblocks : nullptr;
+        uint8_t *hits = a.blocks_hit ? a.blocks_hit + (MV ? (long long)R.view * a.nblocks : 0ll) : nullptr;
         R.r.ox = h.o[0];
         R.r.oy = h.o[1];
         R.r.oz = h.o[2];
@@ -1452,7 +1566,12 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
         }
         if (lane == 0) {
             finish_ray(a, R.out, acc_r, acc_g, acc_b, acc_a, taken, skipped);
-            vt.add(a, R.view, taken, skipped);
+            if (MV) {
+                vt.add(a, R.view, taken, skipped);
+            } else {
+                c_taken += (unsigned long long)taken;
+                c_skip += (unsigned long long)skipped;
+            }
         }
 #ifdef VR_DEBUG_TIMES
         ++n_rays;
@@ -1477,7 +1596,16 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
         a.debug_times[4 * w + 3] = n_rays;
     }
 #endif
-    vt.flush_warp(a);
+    if (MV) {
+        vt.flush_warp(a);
+    } else {
+        c_taken = warp_sum(c_taken);
+        c_skip = warp_sum(c_skip);
+        if (lane == 0 && a.totals && (c_taken | c_skip)) {
+            atomicAdd(a.totals, c_taken);
+            atomicAdd(a.totals + 1, c_skip);
+        }
+    }
     if (a.work) {
         c_shaded = warp_sum(c_shaded);
         c_eval = warp_sum(c_eval);
@@ -1492,26 +1620,34 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
 
 using KernelFn = void (*)(RenderArgs);
 
-template <bool CUBIC, bool LIGHT>
+template <bool CUBIC, bool LIGHT, bool MV>
 KernelFn pick_heavy(bool skip) {
-    return skip ? raycast_heavy_kernel<CUBIC, LIGHT, true> : raycast_heavy_kernel<CUBIC, LIGHT, false>;
+    return skip ? raycast_heavy_kernel<CUBIC, LIGHT, true, MV> : raycast_heavy_kernel<CUBIC, LIGHT, false, MV>;
 }
 
 KernelFn pick_cooperative(const RenderArgs &a) {
     const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
-    if (c) return l ? pick_heavy<true, true>(s) : pick_heavy<true, false>(s);
-    return l ? pick_heavy<false, true>(s) : pick_heavy<false, false>(s);
+    if (a.nviews > 1) {
+        if (c) return l ? pick_heavy<true, true, true>(s) : pick_heavy<true, false, true>(s);
+        return l ? pick_heavy<false, true, true>(s) : pick_heavy<false, false, true>(s);
+    }
+    if (c) return l ? pick_heavy<true, true, false>(s) : pick_heavy<true, false, false>(s);
+    return l ? pick_heavy<false, true, false>(s) : pick_heavy<false, false, false>(s);
 }
 
-template <bool CUBIC, bool LIGHT>
+template <bool CUBIC, bool LIGHT, bool MV>
 KernelFn pick_post(bool skip) {
-    return skip ? raycast_post_kernel<CUBIC, LIGHT, true> : raycast_post_kernel<CUBIC, LIGHT, false>;
+    return skip ? raycast_post_kernel<CUBIC, LIGHT, true, MV> : raycast_post_kernel<CUBIC, LIGHT, false, MV>;
 }
 
 KernelFn pick_persistent(const RenderArgs &a) {
     const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
-    if (c) return l ? pick_post<true, true>(s) : pick_post<true, false>(s);
-    return l ? pick_post<false, true>(s) : pick_post<false, false>(s);
+    if (a.nviews > 1) {
+        if (c) return l ? pick_post<true, true, true>(s) : pick_post<true, false, true>(s);
+        return l ? pick_post<false, true, true>(s) : pick_post<false, false, true>(s);
+    }
+    if (c) return l ? pick_post<true, true, false>(s) : pick_post<true, false, false>(s);
+    return l ? pick_post<false, true, false>(s) : pick_post<false, false, false>(s);
 }
 
 template <int KIND, bool CUBIC, bool LIGHT>

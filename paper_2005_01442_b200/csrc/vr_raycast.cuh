@@ -63,6 +63,10 @@ struct RenderArgs {
     int nmx, nmy;
     const int *lut_range;
     int cull;
+    // chained modes (iso, pre-integrated): transparency culling of runs whose
+    // interpolated values provably produce no hit / no opacity.  Pre-integrated:
+    // a (ntbl+1)^2 prefix count of table cells with alpha > 0 (square queries).
+    const int *tbl_nz;
 
     unsigned long long *work_counter;  // persistent kernel's ray queue head (zeroed per launch)
     unsigned long long *debug_times;   // VR_DEBUG_TIMES builds: per warp (start, end, smid, lanes used)

@@ -124,11 +124,38 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     elif sys.argv[1] == "traffic":
+        # kernels of one frame: DRAM bytes summed, utilisation duration-weighted
         parts = [json.loads(Path(p).read_text()) for p in sys.argv[3:]]
+
+        def metric(p, name):
+            m = p["metrics"].get(name)
+            return float(m[0]) if m and isinstance(m[0], (int, float)) else None
+
+        def weighted(name):
+            num = den = 0.0
+            for p in parts:
+                v, d = metric(p, name), p.get("duration_s") or 0.0
+                if v is not None:
+                    num += v * d
+                    den += d
+            return num / den if den else None
+
         Path(f"profiles/ncu_raycast_{sys.argv[2]}.json").write_text(json.dumps(
-            {"kernel": " + ".join(p["kernel"].split("(")[0] for p in parts),
+            {"kernels": " + ".join(p["kernel"].split("(")[0] for p in parts),
              "dram_bytes_per_launch": sum(p["dram_bytes_per_launch"] for p in parts),
-             "per_kernel": {p["kernel"].split("(")[0]: p["dram_bytes_per_launch"] for p in parts},
+             "per_kernel": {p["kernel"].split("(")[0]: {
+                 "dram_bytes": p["dram_bytes_per_launch"], "duration_s": p.get("duration_s"),
+                 "issue_active_pct": metric(p, "smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                 "fp64_pipe_pct": metric(p, "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                 "warps_active_pct": metric(p, "sm__warps_active.avg.pct_of_peak_sustained_active"),
+                 "l1_hit_pct": metric(p, "l1tex__t_sector_hit_rate.pct"),
+                 "l1_bytes": metric(p, "l1tex__t_bytes.sum"), "l2_bytes": metric(p, "lts__t_bytes.sum")}
+                 for p in parts},
+             "issue_active_pct": weighted("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+             "fp64_pipe_pct": weighted("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+             "warps_active_pct": weighted("sm__warps_active.avg.pct_of_peak_sustained_active"),
+             "l1_hit_pct": weighted("l1tex__t_sector_hit_rate.pct"),
+             "l2_hit_pct": weighted("lts__t_sector_hit_rate.pct"),
              "source": [Path(p).name for p in sys.argv[3:]]}, indent=1))
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
