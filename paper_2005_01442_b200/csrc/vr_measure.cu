@@ -24,11 +24,13 @@
 // none); tests/test_measure.py pins it to the analytic oracles of
 // SPEC.md:472-473 (flat face SVR -> 3/(2R), enclosed sphere SVR -> 3/a).
 //
-// The whole-volume pass is HBM-bound: each thread owns a run of 8 cells along
-// x, loads its four voxel rows as 16-byte vectors (every voxel row is read by
-// 4 neighbouring cell rows of the same CTA: one DRAM read, three L1/L2 hits),
-// classifies the 32 corner voxels with bit masks and runs the tetrahedra only
-// for cells that straddle the level (a few per cent of the volume).
+// The whole-volume measure is three passes: (1) the only pass over the int16
+// voxels -- every voxel's inside bit into a flat bit array (1/16 of the
+// volume, L2-resident) and the count V, HBM-bound; (2a) a scan of the bit
+// array for cells whose eight corners disagree, appended to a list; (2b) the
+// tetrahedra for the listed cells, one per thread.  The ball form scans the
+// bit array inside each ball's bounding box.  Generic volumes (unaligned
+// base pointer) use the one-pass kernels kept below.
 #include <cstdint>
 
 #include "vr_common.cuh"
@@ -40,11 +42,23 @@ namespace {
 constexpr int kMeasureThreads = 256;
 constexpr double kAreaScale = 16777216.0;  // 2^24
 
-VR_D void edge_point(const double *P, const double *Q, double fp, double fq, double *out) {
+// Cell corner c (bit 0: x, 1: y, 2: z) of the cell with base voxel (cx, cy,
+// cz), in mm (voxel centres at index * spacing).
+struct CellGeom {
+    int cx, cy, cz;
+    double sx, sy, sz;
+    VR_D double px(int c) const { return (double)(cx + (c & 1)) * sx; }
+    VR_D double py(int c) const { return (double)(cy + ((c >> 1) & 1)) * sy; }
+    VR_D double pz(int c) const { return (double)(cz + ((c >> 2) & 1)) * sz; }
+};
+
+// the level-set point on edge (p inside, q outside): t = f_p / (f_p - f_q) from p
+VR_D void edge_point(const CellGeom &G, int p, int q, double fp, double fq, double *out) {
     const double t = fp / (fp - fq);
-    out[0] = P[0] + t * (Q[0] - P[0]);
-    out[1] = P[1] + t * (Q[1] - P[1]);
-    out[2] = P[2] + t * (Q[2] - P[2]);
+    const double Px = G.px(p), Py = G.py(p), Pz = G.pz(p);
+    out[0] = Px + t * (G.px(q) - Px);
+    out[1] = Py + t * (G.py(q) - Py);
+    out[2] = Pz + t * (G.pz(q) - Pz);
 }
 
 VR_D double cross_half_norm(double ux, double uy, double uz, double wx, double wy, double wz) {
@@ -55,12 +69,14 @@ VR_D double cross_half_norm(double ux, double uy, double uz, double wx, double w
 }
 
 // Fixed-point area of one cell's level-set polygons (corner c = x | y<<1 | z<<2
-// with field f[c] = v - L and position P[c] in mm); BALL keeps only polygons
-// whose centroid lies in the closed ball (bx, by, bz, r2).
+// with field f[c] = v - L); BALL keeps only polygons whose centroid lies in
+// the closed ball (bx, by, bz, r2).
 template <bool BALL>
-VR_D unsigned long long cell_area_fx(const double f[8], const double P[8][3], double bx, double by, double bz,
-                                     double r2) {
+VR_D unsigned long long cell_area_fx(const double f[8], const CellGeom &G, double bx, double by, double bz, double r2) {
     unsigned long long acc = 0;
+    unsigned inside = 0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) inside |= (f[c] > 0.0 ? 1u : 0u) << c;
 #pragma unroll 1
     for (int t = 0; t < 6; ++t) {
         // Kuhn permutations (0,1,2),(0,2,1),(1,0,2),(1,2,0),(2,0,1),(2,1,0)
@@ -71,7 +87,7 @@ VR_D unsigned long long cell_area_fx(const double f[8], const double P[8][3], do
         int in[4], out[4], ni = 0, no = 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-            if (f[v[c]] > 0.0)
+            if ((inside >> v[c]) & 1u)
                 in[ni++] = v[c];
             else
                 out[no++] = v[c];
@@ -80,13 +96,13 @@ VR_D unsigned long long cell_area_fx(const double f[8], const double P[8][3], do
         double a[3], b[3], c3[3], d[3], area, gx, gy, gz;
         if (ni == 1 || no == 1) {
             if (ni == 1) {
-                edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
-                edge_point(P[in[0]], P[out[1]], f[in[0]], f[out[1]], b);
-                edge_point(P[in[0]], P[out[2]], f[in[0]], f[out[2]], c3);
+                edge_point(G, in[0], out[0], f[in[0]], f[out[0]], a);
+                edge_point(G, in[0], out[1], f[in[0]], f[out[1]], b);
+                edge_point(G, in[0], out[2], f[in[0]], f[out[2]], c3);
             } else {
-                edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
-                edge_point(P[in[1]], P[out[0]], f[in[1]], f[out[0]], b);
-                edge_point(P[in[2]], P[out[0]], f[in[2]], f[out[0]], c3);
+                edge_point(G, in[0], out[0], f[in[0]], f[out[0]], a);
+                edge_point(G, in[1], out[0], f[in[1]], f[out[0]], b);
+                edge_point(G, in[2], out[0], f[in[2]], f[out[0]], c3);
             }
             area = cross_half_norm(b[0] - a[0], b[1] - a[1], b[2] - a[2], c3[0] - a[0], c3[1] - a[1], c3[2] - a[2]);
             if (BALL) {
@@ -96,10 +112,10 @@ VR_D unsigned long long cell_area_fx(const double f[8], const double P[8][3], do
             }
         } else {
             // planar quad (in0,out0) (in0,out1) (in1,out1) (in1,out0)
-            edge_point(P[in[0]], P[out[0]], f[in[0]], f[out[0]], a);
-            edge_point(P[in[0]], P[out[1]], f[in[0]], f[out[1]], b);
-            edge_point(P[in[1]], P[out[1]], f[in[1]], f[out[1]], c3);
-            edge_point(P[in[1]], P[out[0]], f[in[1]], f[out[0]], d);
+            edge_point(G, in[0], out[0], f[in[0]], f[out[0]], a);
+            edge_point(G, in[0], out[1], f[in[0]], f[out[1]], b);
+            edge_point(G, in[1], out[1], f[in[1]], f[out[1]], c3);
+            edge_point(G, in[1], out[0], f[in[1]], f[out[0]], d);
             area = cross_half_norm(c3[0] - a[0], c3[1] - a[1], c3[2] - a[2], d[0] - b[0], d[1] - b[1], d[2] - b[2]);
             if (BALL) {
                 gx = (((a[0] + b[0]) + c3[0]) + d[0]) * 0.25;
@@ -235,17 +251,14 @@ __global__ void __launch_bounds__(kMeasureThreads) threshold_measure_kernel(Meas
             const int b = __ffs(straddle) - 1;  // cell x0-1+b, corners at row positions b, b+1
             straddle &= straddle - 1;
             const int cx = x0 - 1 + b;
-            double f[8], P[8][3];
+            double f[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 const int rr = (c >> 1);  // (y, z) bits -> row index y | z<<1
-                const int p = b + (c & 1);
-                f[c] = (double)row_voxel(pv[rr], lo[rr], hi[rr], p) - level;
-                P[c][0] = (double)(cx + (c & 1)) * m.sx;
-                P[c][1] = (double)(cy + ((c >> 1) & 1)) * m.sy;
-                P[c][2] = (double)(cz + ((c >> 2) & 1)) * m.sz;
+                f[c] = (double)row_voxel(pv[rr], lo[rr], hi[rr], b + (c & 1)) - level;
             }
-            area += cell_area_fx<false>(f, P, 0.0, 0.0, 0.0, 0.0);
+            const CellGeom G{cx, cy, cz, m.sx, m.sy, m.sz};
+            area += cell_area_fx<false>(f, G, 0.0, 0.0, 0.0, 0.0);
         }
     }
     cta_accumulate(count, area, out, out + 1, false);
@@ -294,23 +307,20 @@ __global__ void __launch_bounds__(kMeasureThreads) ball_measure_kernel(MeasureVo
             const int i = i0 + (int)(t % wx);
             const long long r = t / wx;
             const int j = j0 + (int)(r % wy), k = k0 + (int)(r / wy);
-            double f[8], P[8][3];
+            double f[8];
             bool any_in = false, any_out = false;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                const int a = i + (c & 1), b = j + ((c >> 1) & 1), e = k + ((c >> 2) & 1);
-                f[c] = (double)voxel_or_pad(m, a, b, e) - level;
-                P[c][0] = (double)a * m.sx;
-                P[c][1] = (double)b * m.sy;
-                P[c][2] = (double)e * m.sz;
+                f[c] = (double)voxel_or_pad(m, i + (c & 1), j + ((c >> 1) & 1), k + ((c >> 2) & 1)) - level;
                 if (f[c] > 0.0) any_in = true; else any_out = true;
             }
+            const CellGeom G{i, j, k, m.sx, m.sy, m.sz};
             if (i >= 0 && j >= 0 && k >= 0 && f[0] > 0.0) {
                 // the cell's base voxel (i, j, k): centre in the closed ball (vro_ball_counts)
                 const double dx = (double)i * m.sx - cx, dy = (double)j * m.sy - cy, dz = (double)k * m.sz - cz;
                 count += ((dx * dx + dy * dy) + dz * dz <= r2) ? 1 : 0;
             }
-            if (any_in && any_out) area += cell_area_fx<true>(f, P, cx, cy, cz, r2);
+            if (any_in && any_out) area += cell_area_fx<true>(f, G, cx, cy, cz, r2);
         }
     }
     cta_accumulate(count, area, counts + q, areas ? areas + q : nullptr, true);
@@ -326,6 +336,20 @@ __global__ void __launch_bounds__(kMeasureThreads) ball_measure_kernel(MeasureVo
 // windows of its four voxel rows locate the cells whose corners are not all
 // equal; only those (a few per mille at CT thresholds) read their 8 voxels
 // and run the tetrahedra.
+// 8 inside bits (v >= thr) of the 8 voxels of a 16-byte group
+VR_D unsigned group_bits(const int4 q, int thr) {
+    const unsigned w[4] = {(unsigned)q.x, (unsigned)q.y, (unsigned)q.z, (unsigned)q.w};
+    unsigned b = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        b |= ((int)(short)(w[k] & 0xffffu) >= thr ? 1u : 0u) << (2 * k);
+        b |= ((int)(short)(w[k] >> 16) >= thr ? 1u : 0u) << (2 * k + 1);
+    }
+    return b;
+}
+
+constexpr int kBitsUnroll = 4;  // 16-byte loads in flight per lane (HBM latency x bandwidth)
+
 __global__ void __launch_bounds__(kMeasureThreads) inside_bits_kernel(const int16_t *__restrict__ v, long long n,
                                                                       int thr, unsigned *__restrict__ bits,
                                                                       unsigned long long *count) {
@@ -333,27 +357,29 @@ __global__ void __launch_bounds__(kMeasureThreads) inside_bits_kernel(const int1
     const int lane = threadIdx.x & 31;
     unsigned long long c = 0;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    // the loop bound is warp-uniform (whole warps of groups), so the shuffles
-    // below always run converged
-    for (long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) & ~31ll; g0 < n8; g0 += stride) {
-        const long long g = g0 + lane;
-        unsigned b = 0;
-        if (g < n8) {
-            const int4 q = __ldg(reinterpret_cast<const int4 *>(v) + g);
-            const unsigned w[4] = {(unsigned)q.x, (unsigned)q.y, (unsigned)q.z, (unsigned)q.w};
+    const int4 *v4 = reinterpret_cast<const int4 *>(v);
+    const long long tail_word = (n & 31) ? (n >> 5) : -1;  // owned by the tail thread
+    // warp-uniform trip counts (whole warps of groups): the shuffles below run
+    // converged; kBitsUnroll independent loads are issued before any is used
+    for (long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) & ~31ll; g0 < n8;
+         g0 += kBitsUnroll * stride) {
+        int4 q[kBitsUnroll];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                b |= ((int)(short)(w[k] & 0xffffu) >= thr ? 1u : 0u) << (2 * k);
-                b |= ((int)(short)(w[k] >> 16) >= thr ? 1u : 0u) << (2 * k + 1);
-            }
-            c += (unsigned long long)__popc(b);
+        for (int u = 0; u < kBitsUnroll; ++u) {
+            const long long g = g0 + u * stride + lane;
+            q[u] = g < n8 ? __ldcs(v4 + g) : make_int4(0, 0, 0, 0);  // streamed: read once
         }
-        // lanes 4m .. 4m+3 hold voxels 32m' .. 32m'+31 of one word
-        unsigned word = b << (8 * (lane & 3));
-        word |= __shfl_xor_sync(0xffffffffu, word, 1);
-        word |= __shfl_xor_sync(0xffffffffu, word, 2);
-        // (the word holding the last n % 32 voxels belongs to the tail thread)
-        if ((lane & 3) == 0 && g < n8 && !((n & 31) && (g >> 2) == (n >> 5))) bits[g >> 2] = word;
+#pragma unroll
+        for (int u = 0; u < kBitsUnroll; ++u) {
+            const long long g = g0 + u * stride + lane;
+            const unsigned b = g < n8 ? group_bits(q[u], thr) : 0u;
+            c += (unsigned long long)__popc(b);
+            // lanes 4m .. 4m+3 hold voxels 32m' .. 32m'+31 of one word
+            unsigned word = b << (8 * (lane & 3));
+            word |= __shfl_xor_sync(0xffffffffu, word, 1);
+            word |= __shfl_xor_sync(0xffffffffu, word, 2);
+            if ((lane & 3) == 0 && g < n8 && (g >> 2) != tail_word) bits[g >> 2] = word;
+        }
     }
     // tail voxels (n % 8) and the tail word's missing lanes: one thread
     if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 31)) {
@@ -380,9 +406,8 @@ VR_D unsigned long long row_bits33(const MeasureVol &m, const unsigned *bits, in
     const long long b0 = ((long long)k * m.ny + j) * m.nx + lo;
     const long long w = b0 >> 5;
     const int sh = (int)(b0 & 31);
-    const long long nwords = ((long long)m.nx * m.ny * m.nz + 31) >> 5;
-    const unsigned long long win =
-        (unsigned long long)__ldg(bits + w) | ((w + 1 < nwords ? (unsigned long long)__ldg(bits + w + 1) : 0ull) << 32);
+    // (the bit array has a spare word after the last one: reading w + 1 is safe)
+    const unsigned long long win = (unsigned long long)__ldg(bits + w) | ((unsigned long long)__ldg(bits + w + 1) << 32);
     unsigned long long r = win >> sh;  // >= 33 valid bits (sh <= 31)
     const int len = hi - lo + 1;
     r &= len >= 64 ? ~0ull : ((1ull << len) - 1ull);
@@ -438,16 +463,12 @@ VR_D unsigned long long warp_cells_area(const MeasureVol &m, unsigned st, int x0
         const int sx0 = __shfl_sync(full, x0, src), scy = __shfl_sync(full, cy, src), scz = __shfl_sync(full, cz, src);
         if (id < total) {
             const int cx = sx0 + nth_set_bit(ms, k);
-            double f[8], P[8][3];
+            double f[8];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int a = cx + (c & 1), jj = scy + ((c >> 1) & 1), kk = scz + ((c >> 2) & 1);
-                f[c] = (double)voxel_or_pad(m, a, jj, kk) - level;
-                P[c][0] = (double)a * m.sx;
-                P[c][1] = (double)jj * m.sy;
-                P[c][2] = (double)kk * m.sz;
-            }
-            area += cell_area_fx<BALL>(f, P, bx, by, bz, r2);
+            for (int c = 0; c < 8; ++c)
+                f[c] = (double)voxel_or_pad(m, cx + (c & 1), scy + ((c >> 1) & 1), scz + ((c >> 2) & 1)) - level;
+            const CellGeom G{cx, scy, scz, m.sx, m.sy, m.sz};
+            area += cell_area_fx<BALL>(f, G, bx, by, bz, r2);
         }
     }
     return area;
@@ -464,14 +485,84 @@ VR_D unsigned long long chunk_straddle(const MeasureVol &m, const unsigned *bits
     return st;
 }
 
-// Pass 2, whole volume: thread = (32-cell chunk, cell row cy), CTA row =
-// chunks of one cell row; blockIdx.y = cell row, blockIdx.z = slab chunk.
+// Pass 2a, whole volume: the straddling cells of every (32-cell chunk, cell
+// row, cell slab), appended to a list (one warp-aggregated atomic per warp);
+// a lean kernel (no float64), so it runs at full occupancy over the L2-
+// resident bit array.  Cells are packed as (cx + 1) | (cy + 1) << 21 |
+// (cz + 1) << 42.  Returns the list length in *ncells (capped at cap; the
+// overflow count is what tells the host to fall back, see the launcher).
+__global__ void __launch_bounds__(kMeasureThreads) straddle_scan_kernel(MeasureVol m, const unsigned *__restrict__ bits,
+                                                                        int nchunks, unsigned long long *list,
+                                                                        unsigned long long cap,
+                                                                        unsigned long long *ncells) {
+    // (32-bit index arithmetic: the item count is checked < 2^31 by the launcher)
+    const int total = nchunks * (m.ny + 1) * (m.nz + 1);
+    const int lane = threadIdx.x & 31;
+    for (int t0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) & ~31u); t0 < total; t0 += gridDim.x * blockDim.x) {
+        const int t = t0 + lane;
+        unsigned st = 0;
+        int x0 = 0, cy = 0, cz = 0;
+        if (t < total) {
+            const int c = t % nchunks;
+            const int r = t / nchunks;
+            cy = r % (m.ny + 1) - 1;
+            cz = r / (m.ny + 1) - 1;
+            x0 = 32 * c - 1;
+            st = (unsigned)chunk_straddle(m, bits, x0, cy, cz);
+        }
+        const int cnt = __popc(st);
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+        }
+        const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
+        if (wtotal == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(ncells, (unsigned long long)wtotal);
+        base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - cnt);
+        const unsigned long long yz = ((unsigned long long)(cy + 1) << 21) | ((unsigned long long)(cz + 1) << 42);
+        while (st) {
+            const int b = __ffs(st) - 1;
+            st &= st - 1;
+            if (base < cap) list[base] = (unsigned long long)(x0 + b + 1) | yz;
+            ++base;
+        }
+    }
+}
+
+// Pass 2b: one straddling cell per thread: its 8 voxels, the tetrahedra.
+__global__ void __launch_bounds__(kMeasureThreads) cell_area_kernel(MeasureVol m, int thr,
+                                                                    const unsigned long long *__restrict__ list,
+                                                                    const unsigned long long *ncells,
+                                                                    unsigned long long cap, unsigned long long *out) {
+    const double level = (double)thr - 0.5;
+    const unsigned long long n = *ncells <= cap ? *ncells : 0ull;  // overflow: surface_kernel instead
+    unsigned long long area = 0;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const unsigned long long e = __ldg(list + i);
+        const int cx = (int)(e & 0x1fffff) - 1, cy = (int)((e >> 21) & 0x1fffff) - 1, cz = (int)(e >> 42) - 1;
+        double f[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+            f[c] = (double)voxel_or_pad(m, cx + (c & 1), cy + ((c >> 1) & 1), cz + ((c >> 2) & 1)) - level;
+        const CellGeom G{cx, cy, cz, m.sx, m.sy, m.sz};
+        area += cell_area_fx<false>(f, G, 0.0, 0.0, 0.0, 0.0);
+    }
+    cta_accumulate(0, area, nullptr, out + 1, false);
+}
+
+// Pass 2 (fallback when the cell list overflows): thread = (32-cell chunk,
+// cell row), the tetrahedra shared out warp-wide.
 __global__ void __launch_bounds__(kMeasureThreads) surface_kernel(MeasureVol m, const unsigned *__restrict__ bits,
-                                                                  int thr, int nchunks, unsigned long long *out) {
+                                                                  int thr, int nchunks, const unsigned long long *ncells,
+                                                                  unsigned long long cap, unsigned long long *out) {
+    if (*ncells <= cap) return;  // the list held every straddling cell: cell_area_kernel did the work
     const double level = (double)thr - 0.5;
     unsigned long long area = 0;
     const long long total = (long long)nchunks * (m.ny + 1) * (m.nz + 1);
-    // warp-uniform trip count: the tetrahedra are shared out warp-wide
     for (long long t0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) & ~31ll; t0 < total;
          t0 += (long long)gridDim.x * blockDim.x) {
         const long long t = t0 + (threadIdx.x & 31);
@@ -577,11 +668,29 @@ cudaError_t launch_threshold_measure(const int16_t *vol, int nx, int ny, int nz,
         if ((e = launch_inside_bits(vol, n, thr, bits.p, out, s)) != cudaSuccess) return e;
         const int nchunks = (nx + 1 + 31) / 32;  // cells -1 .. nx-1 in chunks of 32
         const long long total = (long long)nchunks * (ny + 1) * (nz + 1);
+        if (total >= (1ll << 31)) return cudaErrorInvalidValue;  // > 2^36 voxels: not a CT volume
         long long grid = (total + kMeasureThreads - 1) / kMeasureThreads;
-        const long long cap = (long long)device_sms() * 16;
-        if (grid > cap) grid = cap;
-        surface_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, thr, nchunks, out);
-        return cudaGetLastError();
+        const long long cap_ctas = (long long)device_sms() * 16;
+        if (grid > cap_ctas) grid = cap_ctas;
+        // straddling cells: the list holds up to 1/16 of all cells (every
+        // boundary of a 512^3 CT at its bone threshold is ~0.2 %); beyond
+        // that the one-pass surface kernel (correct for any count) runs
+        // instead, chosen on the device so nothing waits on the host
+        const unsigned long long cap = (unsigned long long)((long long)(nx + 1) * (ny + 1) * (nz + 1) / 16 + 1024);
+        void *lst = nullptr;
+        if ((e = cudaMallocAsync(&lst, (size_t)cap * 8 + 16, s)) != cudaSuccess) return e;
+        unsigned long long *ncells = reinterpret_cast<unsigned long long *>((char *)lst + (size_t)cap * 8);
+        e = cudaMemsetAsync(ncells, 0, 8, s);
+        if (e == cudaSuccess) {
+            straddle_scan_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, nchunks,
+                                                                            (unsigned long long *)lst, cap, ncells);
+            cell_area_kernel<<<(unsigned)device_sms() * 8, kMeasureThreads, 0, s>>>(
+                m, thr, (const unsigned long long *)lst, ncells, cap, out);
+            surface_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, thr, nchunks, ncells, cap, out);
+            e = cudaGetLastError();
+        }
+        cudaError_t e2 = cudaFreeAsync(lst, s);
+        return e != cudaSuccess ? e : e2;
     }
     const int runs = (nx + 1 + 7) / 8;  // cells -1 .. nx-1 in runs of 8
     const long long total = (long long)runs * (ny + 1) * (nz + 1);

@@ -755,16 +755,24 @@ __global__ void __launch_bounds__(kBlock) sample_points_kernel(const int16_t *vo
 
 __global__ void __launch_bounds__(kBlock) threshold_kernel(const int16_t *__restrict__ v, long long n, int thr,
                                                            unsigned long long *count) {
+    constexpr int U = 4;  // 16-byte loads in flight per thread (HBM latency x bandwidth)
     unsigned long long c = 0;
-    long long nvec = n / 8;
+    const long long nvec = n / 8;
     const int4 *v8 = reinterpret_cast<const int4 *>(v);
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
-        int4 q = __ldg(v8 + i);
-        const int16_t *h = reinterpret_cast<const int16_t *>(&q);
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < nvec; i0 += U * stride) {
+        int4 q[U];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) c += (h[k] >= thr) ? 1 : 0;
+        for (int u = 0; u < U; ++u) q[u] = i0 + u * stride < nvec ? __ldcs(v8 + i0 + u * stride) : make_int4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (i0 + u * stride >= nvec) continue;
+            const int16_t *h = reinterpret_cast<const int16_t *>(&q[u]);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) c += (h[k] >= thr) ? 1 : 0;
+        }
     }
-    for (long long i = nvec * 8 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    for (long long i = nvec * 8 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += stride)
         c += (v[i] >= thr) ? 1 : 0;
     c = warp_sum(c);
     __shared__ unsigned long long part[kBlock / 32];
