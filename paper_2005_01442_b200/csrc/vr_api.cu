@@ -56,9 +56,15 @@ struct vr_volume {
     short2 *cubes;    // per unit cube: bounds of the interpolant (vr_prep.cuh launch_interp_bounds), brick order
     short2 *mcells;   // per 16^3 macro cell: union of its cells
     int nmx, nmy, nmz;
+    // VR_SAMPLER_TEX builds only (sampling-path A/B): a 3-D texture of x-quads,
+    // texel (x, y, z) = voxels x .. x+3 of row (y, z) as short4
+    cudaArray_t qarr = nullptr;
+    unsigned long long qtex = 0;
 };
 
 static void free_volume(vr_volume *v) {
+    if (v->qtex) cudaDestroyTextureObject((cudaTextureObject_t)v->qtex);
+    if (v->qarr) cudaFreeArray(v->qarr);
     cudaFree(v->data);
     cudaFree(v->cells);
     cudaFree(v->bricks);
@@ -249,6 +255,28 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
     if (e == cudaSuccess)
         e = vr::launch_interp_bounds(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->bnx, v->bny, v->cubes, v->ncx,
                                      v->ncy, v->ncz, v->cells, v->nmx, v->nmy, v->nmz, v->mcells, s);
+#if VR_SAMPLER_TEX
+    if (e == cudaSuccess) {
+        const cudaChannelFormatDesc fd = cudaCreateChannelDesc(16, 16, 16, 16, cudaChannelFormatKindSigned);
+        e = cudaMalloc3DArray(&v->qarr, &fd, make_cudaExtent(v->nx, v->ny, v->nz), cudaArraySurfaceLoadStore);
+        cudaResourceDesc rd = {};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = v->qarr;
+        cudaSurfaceObject_t surf = 0;
+        if (e == cudaSuccess) e = cudaCreateSurfaceObject(&surf, &rd);
+        if (e == cudaSuccess) e = vr::launch_xquads(v->data, (int)v->nx, (int)v->ny, (int)v->nz, surf, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (surf) cudaDestroySurfaceObject(surf);
+        cudaTextureDesc td = {};
+        td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        cudaTextureObject_t tex = 0;
+        if (e == cudaSuccess) e = cudaCreateTextureObject(&tex, &rd, &td, nullptr);
+        v->qtex = (unsigned long long)tex;
+    }
+#endif
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
     if (e == cudaSuccess) e = vr::launch_value_range(v->data, n, d_range, s);
     int h[2] = {0, 0};
@@ -618,6 +646,7 @@ static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
     a.bv.p = vol->bricks;
     a.bv.bpy = (long long)vol->bnx * 64;
     a.bv.bpz = (long long)vol->bnx * vol->bny * 64;
+    a.tv.tex = vol->qtex;
     a.L = grid ? grid->L : monolithic_layout(vol);
     a.dsx = vr::make_divisor(vol->sx);
     a.dsy = vr::make_divisor(vol->sy);
@@ -775,7 +804,14 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     // chained modes (iso, pre-integrated): transparency culling of runs
     const bool chained_cull = vol->cells && !post &&
                               (a.mode == VR_MODE_ISO || (a.mode == VR_MODE_DVR && a.classify == VR_CLS_PREINT));
-    Scratch tbl_nz(s);
+    Scratch tbl_nz(s), chain_q(s);
+    if (chained_cull && nviews == 1) {
+        // the persistent chained-mode kernel's ray queue head
+        VR_CUDA(chain_q.alloc(32));
+        a.work_counter = (unsigned long long *)chain_q.p;
+        zero.p[0] = a.work_counter;
+        zero.n[0] = 1;
+    }
     if (chained_cull) {
         a.cells = vol->cells;
         a.ncx = vol->ncx;
@@ -809,7 +845,7 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     } else if (post) {
         VR_CUDA(vr::launch_lut_range(lut, prm->nlut, prm->lut_lo, a.lut_inv_w, (int *)lut_range.p, zero, s));
     } else {
-        for (int k = 1; k < 3; ++k)
+        for (int k = 0; k < 3; ++k)
             if (zero.n[k]) VR_CUDA(cudaMemsetAsync(zero.p[k], 0, sizeof(unsigned long long) * zero.n[k], s));
         if (zero.nb) VR_CUDA(cudaMemsetAsync(zero.b, 0, zero.nb, s));
     }

@@ -407,6 +407,9 @@ VR_D double cub_sample(const Block<V> &b, double x, double y, double z) {
 }
 
 // ---------------------------------------------------- brick-layout sampling
+#ifndef VR_RUN_FUNNEL
+#define VR_RUN_FUNNEL 0
+#endif
 // The brick volume is read in 8-voxel windows: the 8-byte row of the brick
 // holding `base` (= first tap index rounded down to a multiple of 4) and the
 // same row of the next brick in x.  Every tap of a row lies in that window
@@ -514,6 +517,28 @@ VR_D double cub_sample(const Block<BrickVol> &b, double x, double y, double z) {
             hi[4 * c + r] = need_hi ? __ldg(q + 16) : 0ull;
         }
     double pl[4];
+#if VR_RUN_FUNNEL
+    // four consecutive taps (the row is not clamped at the block's edge): one
+    // funnel shift brings them into one 64-bit word, each tap is a 16-bit
+    // half converted directly (no per-tap shift and select)
+    const bool run = s1 == s0 + 16u && s2 == s0 + 32u && s3 == s0 + 48u;
+    if (run) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            double s[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const unsigned long long l = lo[4 * c + r], h = hi[4 * c + r];
+                const unsigned long long w = s0 == 0u ? l : ((l >> s0) | (h << (64u - s0)));
+                const unsigned wl = (unsigned)w, wh = (unsigned)(w >> 32);
+                s[r] = ((wx0 * (double)(short)wl + wx1 * (double)(short)(wl >> 16)) + wx2 * (double)(short)wh) +
+                       wx3 * (double)(short)(wh >> 16);
+            }
+            pl[c] = ((wy0 * s[0] + wy1 * s[1]) + wy2 * s[2]) + wy3 * s[3];
+        }
+        return ((wz0 * pl[0] + wz1 * pl[1]) + wz2 * pl[2]) + wz3 * pl[3];
+    }
+#endif
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         double s[4];
@@ -522,6 +547,95 @@ VR_D double cub_sample(const Block<BrickVol> &b, double x, double y, double z) {
             const unsigned long long l = lo[4 * c + r], h = hi[4 * c + r];
             s[r] = ((wx0 * window_tap(l, h, s0) + wx1 * window_tap(l, h, s1)) + wx2 * window_tap(l, h, s2)) +
                    wx3 * window_tap(l, h, s3);
+        }
+        pl[c] = ((wy0 * s[0] + wy1 * s[1]) + wy2 * s[2]) + wy3 * s[3];
+    }
+    return ((wz0 * pl[0] + wz1 * pl[1]) + wz2 * pl[2]) + wz3 * pl[3];
+}
+
+// ------------------------------------------------- texture sampling path
+// The sampling-path A/B of the north star ("texture path or shared-memory-
+// staged bricks, whichever ncu shows is faster"), built with
+// -DVR_SAMPLER_TEX=1: a 3-D texture of x-quads (texel (x, y, z) = the int16
+// voxels x .. x+3 of row (y, z), short4, point-sampled), so a row of four
+// consecutive Catmull-Rom taps is ONE texture fetch through the texture
+// cache's 3-D-blocked layout instead of one or two 8-byte brick-window loads
+// and per-tap shifts.  Same taps, same sums: bit-identical results.
+#ifndef VR_SAMPLER_TEX
+#define VR_SAMPLER_TEX 0
+#endif
+struct TexVol {
+    unsigned long long tex;  // cudaTextureObject_t
+    VR_D short4 quad(int x, int y, int z) const {
+        return tex3D<short4>((cudaTextureObject_t)tex, (float)x + 0.5f, (float)y + 0.5f, (float)z + 0.5f);
+    }
+};
+
+// _kernels.py:52-80 through the texture
+VR_D double tri_sample(const Block<TexVol> &b, double x, double y, double z) {
+    x = clampf(x, 0.0, b.ex - 1.0);
+    y = clampf(y, 0.0, b.ey - 1.0);
+    z = clampf(z, 0.0, b.ez - 1.0);
+    int i0 = clampi((int)x, 0, b.ex - 2);
+    int j0 = clampi((int)y, 0, b.ey - 2);
+    int k0 = clampi((int)z, 0, b.ez - 2);
+    double fx = x - (double)i0;
+    double fy = y - (double)j0;
+    double fz = z - (double)k0;
+    const int gx = b.ox + i0, gy = b.oy + j0, gz = b.oz + k0;
+    const short4 q00 = b.vol.quad(gx, gy, gz), q10 = b.vol.quad(gx, gy + 1, gz);
+    const short4 q01 = b.vol.quad(gx, gy, gz + 1), q11 = b.vol.quad(gx, gy + 1, gz + 1);
+    double c00 = (double)q00.x + ((double)q00.y - (double)q00.x) * fx;
+    double c10 = (double)q10.x + ((double)q10.y - (double)q10.x) * fx;
+    double c01 = (double)q01.x + ((double)q01.y - (double)q01.x) * fx;
+    double c11 = (double)q11.x + ((double)q11.y - (double)q11.x) * fx;
+    double c0 = c00 + (c10 - c00) * fy;
+    double c1 = c01 + (c11 - c01) * fy;
+    return c0 + (c1 - c0) * fz;
+}
+
+// _kernels.py:94-143 through the texture: a row of consecutive taps is one
+// fetch; a row clamped at the block's edge fetches each tap
+VR_D double cub_sample(const Block<TexVol> &b, double x, double y, double z) {
+    x = clampf(x, 0.0, b.ex - 1.0);
+    y = clampf(y, 0.0, b.ey - 1.0);
+    z = clampf(z, 0.0, b.ez - 1.0);
+    int i0 = clampi((int)x, 0, b.ex - 1);
+    int j0 = clampi((int)y, 0, b.ey - 1);
+    int k0 = clampi((int)z, 0, b.ez - 1);
+    double wx0, wx1, wx2, wx3, wy0, wy1, wy2, wy3, wz0, wz1, wz2, wz3;
+    cr_weights(x - (double)i0, wx0, wx1, wx2, wx3);
+    cr_weights(y - (double)j0, wy0, wy1, wy2, wy3);
+    cr_weights(z - (double)k0, wz0, wz1, wz2, wz3);
+    const int gx[4] = {b.ox + max(i0 - 1, 0), b.ox + i0, b.ox + min(i0 + 1, b.ex - 1), b.ox + min(i0 + 2, b.ex - 1)};
+    const int gy[4] = {b.oy + max(j0 - 1, 0), b.oy + j0, b.oy + min(j0 + 1, b.ey - 1), b.oy + min(j0 + 2, b.ey - 1)};
+    const int gz[4] = {b.oz + max(k0 - 1, 0), b.oz + k0, b.oz + min(k0 + 1, b.ez - 1), b.oz + min(k0 + 2, b.ez - 1)};
+    const bool run = i0 >= 1 && i0 + 2 <= b.ex - 1;
+    short4 q[16];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) q[4 * c + r] = b.vol.quad(gx[0], gy[r], gz[c]);
+    double pl[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        double s[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            double v0, v1, v2, v3;
+            if (run) {
+                const short4 w = q[4 * c + r];
+                v0 = w.x;
+                v1 = w.y;
+                v2 = w.z;
+                v3 = w.w;
+            } else {
+                v0 = q[4 * c + r].x;
+                v1 = b.vol.quad(gx[1], gy[r], gz[c]).x;
+                v2 = b.vol.quad(gx[2], gy[r], gz[c]).x;
+                v3 = b.vol.quad(gx[3], gy[r], gz[c]).x;
+            }
+            s[r] = ((wx0 * v0 + wx1 * v1) + wx2 * v2) + wx3 * v3;
         }
         pl[c] = ((wy0 * s[0] + wy1 * s[1]) + wy2 * s[2]) + wy3 * s[3];
     }

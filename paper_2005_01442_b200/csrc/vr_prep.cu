@@ -951,6 +951,25 @@ cudaError_t launch_tbl_nonzero(const double *table, int n, int *nz, cudaStream_t
     return cudaGetLastError();
 }
 
+// x-quad texture for the sampling-path A/B (VR_SAMPLER_TEX builds)
+__global__ void xquad_kernel(const int16_t *__restrict__ v, int nx, int ny, int nz, cudaSurfaceObject_t surf) {
+    const long long n = (long long)nx * ny * nz;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const int x = (int)(i % nx);
+        const long long r = i / nx;
+        const int y = (int)(r % ny), z = (int)(r / ny);
+        const int16_t *row = v + r * nx;
+        const short4 q = make_short4(row[x], row[min(x + 1, nx - 1)], row[min(x + 2, nx - 1)], row[min(x + 3, nx - 1)]);
+        surf3Dwrite(q, surf, x * (int)sizeof(short4), y, z);
+    }
+}
+
+cudaError_t launch_xquads(const int16_t *vol, int nx, int ny, int nz, unsigned long long surf, cudaStream_t s) {
+    xquad_kernel<<<grid_for((long long)nx * ny * nz, kBlock, 16), kBlock, 0, s>>>(vol, nx, ny, nz,
+                                                                                (cudaSurfaceObject_t)surf);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_count_hits(const uint8_t *hits, int n, int nviews, unsigned long long *totals,
                               const unsigned long long *vis_counters, cudaStream_t s) {
     cudaError_t e = launch_pdl(count_hits_kernel, nviews, 1024, 0, s, hits, n, totals, vis_counters);

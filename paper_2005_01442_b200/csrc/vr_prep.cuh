@@ -91,6 +91,7 @@ cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double
 // blocks_visited = sum(blocks_hit) -> *out (render.py:467)
 // also copies the two visibility counters (blocks_empty, empty-block errors)
 // to out[1..2] when vis_counters is given
+cudaError_t launch_xquads(const int16_t *vol, int nx, int ny, int nz, unsigned long long surf, cudaStream_t s);
 cudaError_t launch_count_hits(const uint8_t *hits, int n, int nviews, unsigned long long *totals,
                               const unsigned long long *vis_counters, cudaStream_t s);
 

@@ -172,9 +172,20 @@ VR_D double sample_in(const V &vol, const RenderArgs &a, int bi, int bj, int bk,
     return CUBIC ? cub_sample(b, lx, ly, lz) : tri_sample(b, lx, ly, lz);
 }
 
+// the ray casters' interpolant: brick windows through L1 (default) or the
+// x-quad texture (VR_SAMPLER_TEX A/B builds)
+template <bool CUBIC>
+VR_D double vol_sample(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z) {
+#if VR_SAMPLER_TEX
+    return sample_in<CUBIC>(a.tv, a, bi, bj, bk, x, y, z);
+#else
+    return sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
+#endif
+}
+
 template <bool CUBIC>
 VR_D double attr_sample(const RenderArgs &a, double x, double y, double z) {
-    return sample_in<CUBIC>(a.bv, a, owner(a, 0, x), owner(a, 1, y), owner(a, 2, z), x, y, z);
+    return vol_sample<CUBIC>(a, owner(a, 0, x), owner(a, 1, y), owner(a, 2, z), x, y, z);
 }
 
 // _attr_grad (_kernels.py:236-253): six taps at +-0.5 voxel, each attributed
@@ -199,7 +210,7 @@ VR_D void attr_grad(const RenderArgs &a, double x, double y, double z, int bi, i
             pz = z + h;
             qk = owner(a, 2, pz);
         }
-        double s = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
+        double s = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
         if (q & 1)
             g[axis] = plus - s;
         else
@@ -556,7 +567,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
             }
             if (KIND == kIso) {
                 // _kernels.py:405-468
-                double s = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
+                double s = vol_sample<CUBIC>(a, bi, bj, bk, x, y, z);
                 if (!prev_valid && n > 0) {
                     double tp = t - step;
                     prev_s = attr_sample<CUBIC>(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
@@ -662,7 +673,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
                     continue;
                 }
                 ++n_eval;
-                double s = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
+                double s = vol_sample<CUBIC>(a, bi, bj, bk, x, y, z);
                 int sbin = lut_bin(s, a.lut_lo, a.lut_inv_w, a.nlut);
                 double sa = __ldg(a.lut + 4 * sbin + 3);
                 if (sa > 0.0) {
@@ -685,7 +696,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
                 }
             } else {
                 // pre-integrated (_kernels.py:538-581)
-                double s = sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
+                double s = vol_sample<CUBIC>(a, bi, bj, bk, x, y, z);
                 if (!prev_valid && n > 0) {
                     double tp = t - step;
                     prev_s = attr_sample<CUBIC>(a, divide(r.ox + tp * r.dx, a.dsx), divide(r.oy + tp * r.dy, a.dsy),
@@ -1160,7 +1171,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
                     qk = owner(a, 2, pz);
                 }
             }
-            const double v = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
+            const double v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
             c_eval += R.stage == 0;  // sample interpolations (gradient taps: 6 per shaded sample)
             bool composite = false;
             if (R.stage == 0) {
@@ -1436,7 +1447,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
                 }
                 // every lane interpolates (inactive lanes at a valid position):
                 // no divergent branch around the interpolant
-                const double v = sample_in<CUBIC>(a.bv, a, qi, qj, qk, px, py, pz);
+                const double v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
                 if (base < 0) {
                     if (act) {
                         const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
@@ -1618,6 +1629,401 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
     }
 }
 
+// ---------------------------------------- persistent chained modes (iso, preint)
+// The isosurface and pre-integrated modes (_kernels.py:405-468, 538-581) on
+// the persistent scheduler: every lane pulls rays from the global queue (as
+// raycast_post_kernel) and advances its ray by trips -- cheap steps (skip
+// leaps) until an interpolation is needed, then ONE interpolation per trip,
+// whatever it is for: the sample itself, the previous sample (after a gap,
+// at t - step, as the reference re-evaluates it; after a culled run, at its
+// own position), one of the 8 bisection points of an iso crossing, or one of
+// the 6 gradient taps.  The lanes of a warp stay on one instruction stream
+// while their rays are at different places, and a lane whose ray ends takes
+// the next ray at once.  After each evaluated sample, a run of samples whose
+// interpolant bound rules out any contribution (chain_transparent) is
+// counted as taken and leapt over, exactly as raycast_kernel does.
+enum ChainStage { kcNone = -1, kcSample = 0, kcPrevExact = 1, kcPrevGap = 2, kcBisect = 3, kcGrad = 11 };
+
+struct ChainRay {
+    Ray r;
+    double inv[3];
+    double t0;
+    long long n, N;
+    double acc_r, acc_g, acc_b, acc_a;
+    double x, y, z, t;      // the current sample
+    double prev_s, s;
+    double lo_t, hi_t, lo_s, t_hit;  // iso bisection
+    double hx, hy, hz;      // gradient centre
+    double cr, cg, cb, ca;  // colour pending composite (iso: LUT colour; preint: segment)
+    double gplus, gx, gy, gz;
+    long long taken, skipped;
+    long long out;
+    int bi, bj, bk, hbi, hbj, hbk;
+    int stage;
+    int last_hit;
+    bool prev_valid, prev_pending, prev_skippable, live;
+};
+
+template <int KIND, bool CUBIC, bool LIGHT, bool SKIP>
+#ifndef VR_CHAIN_MIN_BLOCKS
+#define VR_CHAIN_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThreads / kPersistThreads))
+    raycast_chain_kernel(const __grid_constant__ RenderArgs a) {
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const long long total = a.items_per_view;
+    const int nbx = a.L.nb[0], nby = a.L.nb[1];
+    const bool chain_cull = a.cull != 0;
+    unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
+    ChainRay R;
+    R.live = false;
+    bool exhausted = false;
+    for (;;) {
+        // ---- fetch rays for idle lanes (one atomic per warp)
+        const bool want = !R.live && !exhausted;
+        const unsigned m = __ballot_sync(full, want);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(a.work_counter, (unsigned long long)__popc(m));
+            base = __shfl_sync(full, base, leader);
+            if (want) {
+                const long long item = (long long)base + __popc(m & ((1u << lane) - 1u));
+                int cx, cy, view;
+                if (item >= total) {
+                    exhausted = true;
+                } else if (item_pixel<false>(a, item, cx, cy, R.out, view)) {
+                    R.r = make_ray(a, view_cam(a, 0), a.tx + cx, a.ty + cy);
+                    double t0, t1;
+                    clip_to_bounds(R.r, a.ext_mm, t0, t1);
+                    R.t0 = t0;
+                    R.N = 0;
+                    if (t1 >= t0) {
+                        long long nsteps = (long long)ceil((t1 - t0) / a.step);
+                        if (nsteps < 1) nsteps = 1;
+                        long long N = nsteps;
+                        while (N > 0 && (t0 + ((double)(N - 1) + 0.5) * a.step) > t1) --N;
+                        R.N = N;
+                    }
+                    R.inv[0] = R.r.dx != 0.0 ? 1.0 / R.r.dx : 0.0;
+                    R.inv[1] = R.r.dy != 0.0 ? 1.0 / R.r.dy : 0.0;
+                    R.inv[2] = R.r.dz != 0.0 ? 1.0 / R.r.dz : 0.0;
+                    R.n = 0;
+                    R.acc_r = R.acc_g = R.acc_b = R.acc_a = 0.0;
+                    R.taken = R.skipped = 0;
+                    R.prev_s = 0.0;
+                    R.prev_valid = R.prev_pending = R.prev_skippable = false;
+                    R.t_hit = __longlong_as_double(0x7ff8000000000000LL);  // NaN: no hit
+                    R.stage = kcNone;
+                    R.last_hit = -1;
+                    R.live = true;
+                }
+            }
+        }
+        if (__all_sync(full, !R.live && exhausted)) break;
+        if (!R.live) continue;
+
+        // ---- phase A: skip leaps until a taken sample needs an interpolation
+        int steps = 0;
+        while (R.stage == kcNone && R.n < R.N && steps < kPhaseACap) {
+            ++steps;
+            ++c_iter;
+            const long long n = R.n;
+            const double t = R.t0 + ((double)n + 0.5) * a.step;
+            const double x = divide(R.r.ox + t * R.r.dx, a.dsx);
+            const double y = divide(R.r.oy + t * R.r.dy, a.dsy);
+            const double z = divide(R.r.oz + t * R.r.dz, a.dsz);
+            const int bi = owner(a, 0, x), bj = owner(a, 1, y), bk = owner(a, 2, z);
+            const int b = (bk * nby + bj) * nbx + bi;
+            if (SKIP) {
+                bool skippable, cell_only = true;
+                BlockRec rec = {};
+                if (KIND == kIso) {
+                    skippable = (double)__ldg(a.vmax + b) < a.isovalue || (double)__ldg(a.vmin + b) > a.isovalue;
+                } else {
+                    rec = block_rec(a, b);
+                    skippable = dvr_skippable(rec, x, y, z);
+                    cell_only = rec.lo.w != 0.0f;
+                }
+                if (skippable && R.prev_skippable) {  // chained: the first sample of a gap is taken
+                    const double p[3] = {x, y, z};
+                    const int bidx[3] = {bi, bj, bk};
+                    long long k = leap_count<KIND>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec, cell_only);
+                    if (k > R.N - n) k = R.N - n;
+                    R.skipped += k;
+                    R.n = n + k;
+                    R.prev_valid = false;
+                    R.prev_pending = false;
+                    continue;
+                }
+                R.prev_skippable = skippable;
+            }
+            if (b != R.last_hit) {
+                if (a.blocks_hit) a.blocks_hit[b] = 1;
+                R.last_hit = b;
+            }
+            R.taken += 1;
+            R.x = x;
+            R.y = y;
+            R.z = z;
+            R.t = t;
+            R.bi = bi;
+            R.bj = bj;
+            R.bk = bk;
+            R.stage = R.prev_pending ? kcPrevExact : ((!R.prev_valid && n > 0) ? kcPrevGap : kcSample);
+        }
+
+        // ---- phase B: one interpolation
+        bool finished = false;
+        if (R.stage != kcNone) {
+            double px = R.x, py = R.y, pz = R.z;
+            int qi = R.bi, qj = R.bj, qk = R.bk;
+            bool own = false;  // position not attributed yet (owner from the position)
+            if (R.stage == kcPrevExact || R.stage == kcPrevGap) {
+                const double tq = R.stage == kcPrevExact ? R.t0 + ((double)(R.n - 1) + 0.5) * a.step : R.t - a.step;
+                px = divide(R.r.ox + tq * R.r.dx, a.dsx);
+                py = divide(R.r.oy + tq * R.r.dy, a.dsy);
+                pz = divide(R.r.oz + tq * R.r.dz, a.dsz);
+                own = true;
+            } else if (KIND == kIso && R.stage >= kcBisect && R.stage < kcGrad) {
+                const double mid = 0.5 * (R.lo_t + R.hi_t);
+                px = divide(R.r.ox + mid * R.r.dx, a.dsx);
+                py = divide(R.r.oy + mid * R.r.dy, a.dsy);
+                pz = divide(R.r.oz + mid * R.r.dz, a.dsz);
+                own = true;
+            } else if (R.stage >= kcGrad) {
+                const int q = R.stage - kcGrad;
+                const double h = (q & 1) ? -0.5 : 0.5;
+                px = R.hx;
+                py = R.hy;
+                pz = R.hz;
+                qi = R.hbi;
+                qj = R.hbj;
+                qk = R.hbk;
+                if (q < 2) {
+                    px = R.hx + h;
+                    qi = owner(a, 0, px);
+                } else if (q < 4) {
+                    py = R.hy + h;
+                    qj = owner(a, 1, py);
+                } else {
+                    pz = R.hz + h;
+                    qk = owner(a, 2, pz);
+                }
+            }
+            if (own) {
+                qi = owner(a, 0, px);
+                qj = owner(a, 1, py);
+                qk = owner(a, 2, pz);
+            }
+            const double v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
+            if (R.stage == kcPrevExact || R.stage == kcPrevGap) {
+                R.prev_s = v;
+                R.prev_valid = true;
+                R.prev_pending = false;
+                R.stage = kcSample;
+            } else if (R.stage == kcSample) {
+                ++c_eval;
+                R.s = v;
+                bool cont = true;  // the ray goes on past this sample
+                if (KIND == kIso) {
+                    if (R.prev_valid && (R.prev_s - a.isovalue) * (v - a.isovalue) < 0.0) {
+                        R.lo_t = R.t - a.step;
+                        R.hi_t = R.t;
+                        R.lo_s = R.prev_s;
+                        R.stage = kcBisect;
+                        cont = false;
+                    } else if (v == a.isovalue) {
+                        R.t_hit = R.t;
+                        R.hx = R.x;
+                        R.hy = R.y;
+                        R.hz = R.z;
+                        R.hbi = owner(a, 0, R.hx);
+                        R.hbj = owner(a, 1, R.hy);
+                        R.hbk = owner(a, 2, R.hz);
+                        R.stage = kcGrad;
+                        cont = false;
+                    }
+                } else {
+                    const double sf = R.prev_valid ? R.prev_s : v;
+                    const int fbin = lut_bin(sf, a.tbl_lo, a.tbl_inv_w, a.ntbl);
+                    const int bbin = lut_bin(v, a.tbl_lo, a.tbl_inv_w, a.ntbl);
+                    const double *cell = a.table + 4 * ((long long)fbin * a.ntbl + bbin);
+                    const double seg_a = __ldg(cell + 3);
+                    if (seg_a > 0.0) {
+                        R.cr = __ldg(cell);
+                        R.cg = __ldg(cell + 1);
+                        R.cb = __ldg(cell + 2);
+                        R.ca = seg_a;
+                        if (LIGHT) {
+                            R.hx = R.x;
+                            R.hy = R.y;
+                            R.hz = R.z;
+                            R.hbi = R.bi;
+                            R.hbj = R.bj;
+                            R.hbk = R.bk;
+                            R.stage = kcGrad;
+                            cont = false;
+                        } else {
+                            const double w = 1.0 - R.acc_a;
+                            R.acc_r += w * R.cr;
+                            R.acc_g += w * R.cg;
+                            R.acc_b += w * R.cb;
+                            R.acc_a += w * R.ca;
+                            if (R.acc_a >= a.term_alpha) finished = true;
+                        }
+                    }
+                }
+                if (cont && !finished) {
+                    // sample done: a run of samples that provably change nothing
+                    R.prev_s = v;
+                    R.prev_valid = true;
+                    R.stage = kcNone;
+                    long long k = 1;
+                    if (chain_cull && !R.prev_skippable) {
+                        const int lvl = chain_transparent<KIND>(a, R.x, R.y, R.z);
+                        if (lvl) {
+                            const double p[3] = {R.x, R.y, R.z};
+                            const int bidx[3] = {R.bi, R.bj, R.bk};
+                            BlockRec rec = {};
+                            if (SKIP && KIND != kIso) rec = block_rec(a, (R.bk * nby + R.bj) * nbx + R.bi);
+                            k = KIND == kIso ? culled_run<SKIP, false>(a, R.r, R.inv, R.t0, R.n, R.t, p, bidx, rec,
+                                                                        lvl == 3 ? 4 : lvl == 1 ? 2 : 0)
+                                             : culled_run<SKIP>(a, R.r, R.inv, R.t0, R.n, R.t, p, bidx, rec,
+                                                                lvl == 3 ? 4 : lvl == 1 ? 2 : 0);
+                            if (k > R.N - R.n) k = R.N - R.n;
+                            if (k < 1) k = 1;
+                        }
+                    }
+                    if (k > 1) {
+                        R.taken += k - 1;
+                        R.prev_pending = true;
+                    }
+                    R.n += k;
+                }
+            } else if (KIND == kIso && R.stage < kcGrad) {
+                // bisection round (_kernels.py:447-461)
+                const double mid = 0.5 * (R.lo_t + R.hi_t);
+                if ((R.lo_s - a.isovalue) * (v - a.isovalue) <= 0.0) {
+                    R.hi_t = mid;
+                } else {
+                    R.lo_t = mid;
+                    R.lo_s = v;
+                }
+                if (++R.stage == kcGrad) {
+                    R.t_hit = 0.5 * (R.lo_t + R.hi_t);
+                    R.hx = divide(R.r.ox + R.t_hit * R.r.dx, a.dsx);
+                    R.hy = divide(R.r.oy + R.t_hit * R.r.dy, a.dsy);
+                    R.hz = divide(R.r.oz + R.t_hit * R.r.dz, a.dsz);
+                    R.hbi = owner(a, 0, R.hx);
+                    R.hbj = owner(a, 1, R.hy);
+                    R.hbk = owner(a, 2, R.hz);
+                }
+            } else {
+                // gradient tap (_kernels.py:236-253): +x, -x, +y, -y, +z, -z
+                const int q = R.stage - kcGrad;
+                if (q & 1) {
+                    const double dg = R.gplus - v;
+                    if (q == 1) R.gx = dg;
+                    else if (q == 3) R.gy = dg;
+                    else R.gz = dg;
+                } else {
+                    R.gplus = v;
+                }
+                if (q < 5) {
+                    R.stage += 1;
+                } else {
+                    const double gx = divide(R.gx, a.dsx), gy = divide(R.gy, a.dsy), gz = divide(R.gz, a.dsz);
+                    ++c_shaded;
+                    const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                    if (KIND == kIso) {
+                        // _kernels.py:466-483: LUT colour at the isovalue, shaded, opaque
+                        const int ib = lut_bin(a.isovalue, a.lut_lo, a.lut_inv_w, a.nlut);
+                        double cr = __ldg(a.lut + 4 * ib), cg = __ldg(a.lut + 4 * ib + 1), cb = __ldg(a.lut + 4 * ib + 2);
+                        if (LIGHT && norm > 1e-12)
+                            shade(a, cr, cg, cb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
+                        R.acc_r = cr;
+                        R.acc_g = cg;
+                        R.acc_b = cb;
+                        R.acc_a = 1.0;
+                        finished = true;
+                    } else {
+                        // _kernels.py:560-581
+                        double seg_r = R.cr, seg_g = R.cg, seg_b = R.cb;
+                        const double seg_a = R.ca;
+                        if (norm > 1e-12) {
+                            const double ndl = fabs(((gx * -R.r.dx + gy * -R.r.dy) + gz * -R.r.dz) / norm);
+                            const double scale = a.ka + a.kd * ndl;
+                            const double spec = a.ks * vr_pow(ndl, a.shin) * seg_a;
+                            seg_r = clampf(scale * seg_r + spec, 0.0, 1.0);
+                            seg_g = clampf(scale * seg_g + spec, 0.0, 1.0);
+                            seg_b = clampf(scale * seg_b + spec, 0.0, 1.0);
+                        }
+                        const double w = 1.0 - R.acc_a;
+                        R.acc_r += w * seg_r;
+                        R.acc_g += w * seg_g;
+                        R.acc_b += w * seg_b;
+                        R.acc_a += w * seg_a;
+                        if (R.acc_a >= a.term_alpha) {
+                            finished = true;
+                        } else {
+                            R.prev_s = R.s;
+                            R.prev_valid = true;
+                            R.stage = kcNone;
+                            R.n += 1;  // (no culled run after a contributing segment: the next may contribute)
+                        }
+                    }
+                }
+            }
+        }
+        if (R.stage == kcNone && R.n >= R.N) finished = true;
+
+        if (finished) {
+            // background, epilogue, per-pixel outputs (_kernels.py:583-594)
+            const double w = 1.0 - R.acc_a;
+            const double rr = R.acc_r + w * a.bg[0] * a.bg[3];
+            const double gg = R.acc_g + w * a.bg[1] * a.bg[3];
+            const double bb = R.acc_b + w * a.bg[2] * a.bg[3];
+            const double aa = R.acc_a + w * a.bg[3];
+            const long long p = R.out;
+            if (a.premult) reinterpret_cast<double4 *>(a.premult)[p] = make_double4(rr, gg, bb, aa);
+            if (a.pixels) {
+                double r0 = 0.0, g0 = 0.0, b0 = 0.0;
+                if (aa > 0.0) {
+                    const double den = aa > 1e-12 ? aa : 1e-12;
+                    r0 = rr / den;
+                    g0 = gg / den;
+                    b0 = bb / den;
+                }
+                reinterpret_cast<uchar4 *>(a.pixels)[p] = make_uchar4(to_u8(r0), to_u8(g0), to_u8(b0), to_u8(aa));
+            }
+            if (a.depth) a.depth[p] = R.t_hit;
+            if (a.taken) a.taken[p] = R.taken;
+            if (a.skipped) a.skipped[p] = R.skipped;
+            c_taken += (unsigned long long)R.taken;
+            c_skip += (unsigned long long)R.skipped;
+            R.live = false;
+        }
+    }
+    c_taken = warp_sum(c_taken);
+    c_skip = warp_sum(c_skip);
+    if (lane == 0 && a.totals && (c_taken | c_skip)) {
+        atomicAdd(a.totals, c_taken);
+        atomicAdd(a.totals + 1, c_skip);
+    }
+    if (a.work) {
+        c_shaded = warp_sum(c_shaded);
+        c_eval = warp_sum(c_eval);
+        c_iter = warp_sum(c_iter);
+        if (lane == 0) {
+            if (c_shaded) atomicAdd(a.work, c_shaded);
+            if (c_eval) atomicAdd(a.work + 1, c_eval);
+            if (c_iter) atomicAdd(a.work + 2, c_iter);
+        }
+    }
+}
+
 using KernelFn = void (*)(RenderArgs);
 
 template <bool CUBIC, bool LIGHT, bool MV>
@@ -1693,6 +2099,22 @@ int persistent_ctas_per_sm(KernelFn k) {
     return per_sm;
 }
 
+template <int KIND, bool CUBIC, bool LIGHT>
+KernelFn pick_chain_skip(bool skip) {
+    return skip ? raycast_chain_kernel<KIND, CUBIC, LIGHT, true> : raycast_chain_kernel<KIND, CUBIC, LIGHT, false>;
+}
+
+template <int KIND>
+KernelFn pick_chain_kind(const RenderArgs &a) {
+    const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
+    if (c) return l ? pick_chain_skip<KIND, true, true>(s) : pick_chain_skip<KIND, true, false>(s);
+    return l ? pick_chain_skip<KIND, false, true>(s) : pick_chain_skip<KIND, false, false>(s);
+}
+
+KernelFn pick_chain(const RenderArgs &a) {
+    return a.mode == 1 ? pick_chain_kind<kIso>(a) : pick_chain_kind<kPreint>(a);
+}
+
 KernelFn pick(const RenderArgs &a) {
     const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
     if (a.mode == 1) return pick_cubic<kIso>(c, l, s);
@@ -1753,6 +2175,16 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
                 if (e != cudaSuccess) return e;
             }
         }
+        return cudaGetLastError();
+    }
+    const bool chained = a.mode == 1 || (a.mode == 0 && a.classify == 2);
+    if (chained && a.work_counter && a.nviews == 1) {
+        // persistent chained modes (queue counters zeroed by the frame's first kernel)
+        KernelFn k = pick_chain(a);
+        long long ctas = (long long)device_sms() * persistent_ctas_per_sm(k);
+        const long long most = (long long)a.slots * (kThreads / kPersistThreads);
+        if (ctas > most) ctas = most;
+        k<<<(unsigned)ctas, kPersistThreads, 0, stream>>>(a);
         return cudaGetLastError();
     }
     pick(a)<<<(unsigned)((long long)a.slots * a.nviews), kThreads, 0, stream>>>(a);

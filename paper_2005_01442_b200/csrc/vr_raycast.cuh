@@ -8,6 +8,7 @@ struct RenderArgs {
     // volume and its block layout (monolithic = one block spanning the volume)
     const int16_t *vol;
     BrickVol bv;  // the same voxels in 4^3 bricks (K1), read by every interpolation
+    TexVol tv;    // VR_SAMPLER_TEX builds: the x-quad texture (sampling-path A/B)
     Layout L;
     Divisor dsx, dsy, dsz;  // spacing divisors (x = (o + t*d) / s)
     double ext_mm[3];       // (n-1)*s, volume.py:62-67
