@@ -806,11 +806,21 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
                               (a.mode == VR_MODE_ISO || (a.mode == VR_MODE_DVR && a.classify == VR_CLS_PREINT));
     Scratch tbl_nz(s), chain_q(s);
     if (chained_cull && nviews == 1) {
-        // the persistent chained-mode kernel's ray queue head
+        // the persistent chained-mode kernel's ray queue head, then the
+        // hand-off queue's pushed / claimed counters
         VR_CUDA(chain_q.alloc(32));
         a.work_counter = (unsigned long long *)chain_q.p;
         zero.p[0] = a.work_counter;
-        zero.n[0] = 1;
+        zero.n[0] = 3;
+        a.heavy_count = a.work_counter + 1;
+        a.heavy_head = a.work_counter + 2;
+        const long long items = a.items_per_view;
+        a.heavy_cap = items < (1LL << 20) ? items : (1LL << 20);
+        a.heavy_min_left = VR_HEAVY_MIN_LEFT;
+        if (a.heavy_min_left > 0) {
+            VR_CUDA(heavy.alloc((size_t)a.heavy_cap * vr::kChainRecBytes));
+            a.heavy = heavy.p;
+        }
     }
     if (chained_cull) {
         a.cells = vol->cells;

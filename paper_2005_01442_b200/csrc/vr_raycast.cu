@@ -331,19 +331,28 @@ VR_D bool chain_bound_ok(const RenderArgs &a, short2 b) {
 }
 
 template <int KIND>
-VR_D int chain_transparent(const RenderArgs &a, double x, double y, double z) {
+VR_D int chain_transparent(const RenderArgs &a, double x, double y, double z, short2 *bound = nullptr) {
     const int gx = clampi((int)x, 0, a.L.n[0] - 1);
     const int gy = clampi((int)y, 0, a.L.n[1] - 1);
     const int gz = clampi((int)z, 0, a.L.n[2] - 1);
-    if (a.mcells &&
-        chain_bound_ok<KIND>(a, __ldg(a.mcells + ((long long)(gz >> 4) * a.nmy + (gy >> 4)) * a.nmx + (gx >> 4))))
-        return 3;
-    if (chain_bound_ok<KIND>(a, __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2))))
+    if (a.mcells) {
+        const short2 w = __ldg(a.mcells + ((long long)(gz >> 4) * a.nmy + (gy >> 4)) * a.nmx + (gx >> 4));
+        if (chain_bound_ok<KIND>(a, w)) {
+            if (bound) *bound = w;
+            return 3;
+        }
+    }
+    const short2 c = __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2));
+    if (chain_bound_ok<KIND>(a, c)) {
+        if (bound) *bound = c;
         return 1;
+    }
     if (!a.cubes) return 0;
     const short2 w = __ldg(a.cubes + (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
                            ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3));
-    return chain_bound_ok<KIND>(a, w) ? 2 : 0;
+    if (!chain_bound_ok<KIND>(a, w)) return 0;
+    if (bound) *bound = w;
+    return 2;
 }
 
 // Parameter interval in which the (exact) ray lies inside the box [lo, hi]
@@ -1644,6 +1653,20 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
 // counted as taken and leapt over, exactly as raycast_kernel does.
 enum ChainStage { kcNone = -1, kcSample = 0, kcPrevExact = 1, kcPrevGap = 2, kcBisect = 3, kcGrad = 11 };
 
+// A chained-mode ray handed to the cooperative kernel: everything needed to
+// continue it exactly where it stopped.
+struct ChainRec {
+    long long out, n, N;
+    double t0;
+    double o[3], d[3];
+    double acc[4];
+    long long taken, skipped;
+    double prev_s;
+    int flags;  // 1 prev_valid, 2 prev_pending (previous sample culled), 4 prev_skippable
+    int pad;
+};
+static_assert(sizeof(ChainRec) == kChainRecBytes, "ChainRec layout");
+
 struct ChainRay {
     Ray r;
     double inv[3];
@@ -1722,7 +1745,44 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
             }
         }
         if (__all_sync(full, !R.live && exhausted)) break;
+        // the queue head is global: a warp whose lanes are all busy must still
+        // learn that it has drained
+        int head_done = 0;
+        if (lane == 0 && a.heavy)
+            head_done = *reinterpret_cast<volatile unsigned long long *>(a.work_counter) >= (unsigned long long)total;
+        const bool drained = __shfl_sync(full, head_done, 0) != 0 || __any_sync(full, exhausted);
         if (!R.live) continue;
+
+        // ---- once the queue has drained, long rays go to the cooperative
+        // kernel at a clean point (the frame would otherwise end with a few
+        // lanes walking long rays alone)
+        if (a.heavy && drained && R.stage == kcNone && R.N - R.n >= a.heavy_min_left) {
+            const unsigned long long slot = atomicAdd(a.heavy_count, 1ull);
+            if (slot < (unsigned long long)a.heavy_cap) {
+                ChainRec h;
+                h.out = R.out;
+                h.n = R.n;
+                h.N = R.N;
+                h.t0 = R.t0;
+                h.o[0] = R.r.ox;
+                h.o[1] = R.r.oy;
+                h.o[2] = R.r.oz;
+                h.d[0] = R.r.dx;
+                h.d[1] = R.r.dy;
+                h.d[2] = R.r.dz;
+                h.acc[0] = R.acc_r;
+                h.acc[1] = R.acc_g;
+                h.acc[2] = R.acc_b;
+                h.acc[3] = R.acc_a;
+                h.taken = R.taken;
+                h.skipped = R.skipped;
+                h.prev_s = R.prev_s;
+                h.flags = (R.prev_valid ? 1 : 0) | (R.prev_pending ? 2 : 0) | (R.prev_skippable ? 4 : 0);
+                static_cast<ChainRec *>(a.heavy)[slot] = h;
+                R.live = false;
+                continue;
+            }
+        }
 
         // ---- phase A: skip leaps until a taken sample needs an interpolation
         int steps = 0;
@@ -1764,6 +1824,40 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                 R.last_hit = b;
             }
             R.taken += 1;
+            if (KIND == kIso && chain_cull && !R.prev_pending && (R.prev_valid || n == 0)) {
+                // A sample whose region bound excludes the isovalue needs no
+                // interpolation: only the sign of s - iso is ever used (the
+                // crossing test, the bisection bracket), and the bound's end
+                // nearest the isovalue has it.  No crossing into it: the whole
+                // run in the region is hit-free; a crossing: bisect.
+                short2 bd;
+                if (chain_transparent<kIso>(a, x, y, z, &bd)) {
+                    const double stand = (double)bd.x > a.isovalue ? (double)bd.x : (double)bd.y;
+                    if (R.prev_valid && (R.prev_s - a.isovalue) * (stand - a.isovalue) < 0.0) {
+                        R.lo_t = t - a.step;
+                        R.hi_t = t;
+                        R.lo_s = R.prev_s;
+                        R.stage = kcBisect;
+                        break;
+                    }
+                    long long k = 1;
+                    if (!R.prev_skippable) {
+                        const double p[3] = {x, y, z};
+                        const int bidx[3] = {bi, bj, bk};
+                        const BlockRec rec = {};
+                        const int lvl = chain_transparent<kIso>(a, x, y, z);
+                        k = culled_run<SKIP, false>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec,
+                                                    lvl == 3 ? 4 : lvl == 1 ? 2 : 0);
+                        if (k > R.N - n) k = R.N - n;
+                        if (k < 1) k = 1;
+                    }
+                    R.taken += k - 1;
+                    R.n = n + k;
+                    R.prev_s = stand;
+                    R.prev_valid = true;
+                    continue;
+                }
+            }
             R.x = x;
             R.y = y;
             R.z = z;
@@ -2099,6 +2193,397 @@ int persistent_ctas_per_sm(KernelFn k) {
     return per_sm;
 }
 
+// ------------------------------------- warp-cooperative chained-mode long rays
+// Continues the rays raycast_chain_kernel handed over: one warp per ray, 32
+// consecutive samples per chunk, one per lane.  Every lane evaluates its
+// sample's skip predicate (the chained gap rule -- a skippable sample is
+// taken when its predecessor was not -- needs only the neighbour's flag),
+// interpolates it if taken, and, when its predecessor was skipped (or, for
+// the chunk's first lane, culled in the per-lane kernel), the previous sample
+// as the reference re-evaluates it.  Then, in sample order:
+//  - iso: the first lane whose pair (prev, s) changes sign or hits exactly is
+//    the hit; its 8 bisection points run on that lane, its 6 gradient taps on
+//    6 lanes (_kernels.py:405-468);
+//  - pre-integrated: the segment opacities decide the terminating sample by
+//    replaying A += (1 - A) a; the gradient taps of the contributing samples
+//    up to it are spread over the lanes, 32 per round; colours composite in
+//    order (_kernels.py:538-581).
+// Counts stop at the hit / terminating sample, as the sequential march does.
+template <int KIND, bool CUBIC, bool LIGHT, bool SKIP>
+#ifndef VR_CHAIN_COOP_MIN_BLOCKS
+#define VR_CHAIN_COOP_MIN_BLOCKS 4
+#endif
+__global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_COOP_MIN_BLOCKS *(kThreads / kPersistThreads))
+    raycast_chain_coop_kernel(const __grid_constant__ RenderArgs a) {
+    pdl_enter();
+    const int lane = threadIdx.x & 31;
+    const unsigned full = 0xffffffffu;
+    const unsigned lower = (1u << lane) - 1u;
+    const int nbx = a.L.nb[0], nby = a.L.nb[1];
+    const unsigned long long pushed = *a.heavy_count;
+    const long long count = (long long)(pushed < (unsigned long long)a.heavy_cap ? pushed : a.heavy_cap);
+    unsigned long long c_taken = 0, c_skip = 0, c_shaded = 0, c_eval = 0, c_iter = 0;
+    for (;;) {
+        unsigned long long idx = 0;
+        if (lane == 0) idx = atomicAdd(a.heavy_head, 1ull);
+        idx = __shfl_sync(full, idx, 0);
+        if ((long long)idx >= count) break;
+        const ChainRec h = static_cast<const ChainRec *>(a.heavy)[idx];
+        Ray r;
+        r.ox = h.o[0];
+        r.oy = h.o[1];
+        r.oz = h.o[2];
+        r.dx = h.d[0];
+        r.dy = h.d[1];
+        r.dz = h.d[2];
+        double inv[3];
+        inv[0] = r.dx != 0.0 ? 1.0 / r.dx : 0.0;
+        inv[1] = r.dy != 0.0 ? 1.0 / r.dy : 0.0;
+        inv[2] = r.dz != 0.0 ? 1.0 / r.dz : 0.0;
+        double acc_r = h.acc[0], acc_g = h.acc[1], acc_b = h.acc[2], acc_a = h.acc[3];
+        long long taken = h.taken, skipped = h.skipped;
+        // carried state of the sample before the chunk
+        double c_prev = h.prev_s;
+        bool c_prev_valid = (h.flags & 1) != 0, c_pending = (h.flags & 2) != 0, c_prev_skip = (h.flags & 4) != 0;
+        double t_hit = __longlong_as_double(0x7ff8000000000000LL);
+        long long n = h.n;
+        bool done = false;
+        while (n < h.N && !done) {
+            ++c_iter;
+            const long long m = n + lane;
+            const bool valid = m < h.N;
+            double t = 0.0, x = 0.0, y = 0.0, z = 0.0;
+            int bi = 0, bj = 0, bk = 0, b = 0;
+            bool skippable = false, cell_only = true;
+            BlockRec rec = {};
+            if (valid) {
+                t = h.t0 + ((double)m + 0.5) * a.step;
+                x = divide(r.ox + t * r.dx, a.dsx);
+                y = divide(r.oy + t * r.dy, a.dsy);
+                z = divide(r.oz + t * r.dz, a.dsz);
+                bi = owner(a, 0, x);
+                bj = owner(a, 1, y);
+                bk = owner(a, 2, z);
+                b = (bk * nby + bj) * nbx + bi;
+                if (SKIP) {
+                    if (KIND == kIso) {
+                        skippable = (double)__ldg(a.vmax + b) < a.isovalue || (double)__ldg(a.vmin + b) > a.isovalue;
+                    } else {
+                        rec = block_rec(a, b);
+                        skippable = dvr_skippable(rec, x, y, z);
+                        cell_only = rec.lo.w != 0.0f;
+                    }
+                }
+            }
+            // the chained gap rule: skipped iff skippable and the previous sample was
+            const bool pskip_lane = __shfl_up_sync(full, skippable, 1);
+            const bool prev_skip = lane == 0 ? c_prev_skip : pskip_lane;
+            const bool tk = valid && !(skippable && prev_skip);
+            const unsigned tmask = __ballot_sync(full, tk);
+            const unsigned vmask = __ballot_sync(full, valid);
+            // a chunk with nothing taken extends by a provable leap from its last sample
+            if (tmask == 0u) {
+                const unsigned smask = vmask;
+                long long k = 1;
+                if (lane == 31 && valid && skippable) {
+                    const double p[3] = {x, y, z};
+                    const int bidx[3] = {bi, bj, bk};
+                    k = leap_count<KIND>(a, r, inv, h.t0, m, t, p, bidx, rec, cell_only);
+                }
+                k = __shfl_sync(full, k, 31);
+                const long long last = n + 31;
+                skipped += __popc(smask);
+                long long next = n + 32;
+                if (last < h.N && k > 1) {
+                    if (k > h.N - last) k = h.N - last;
+                    skipped += k - 1;
+                    next = last + k;
+                }
+                c_prev_valid = false;
+                c_pending = false;
+                c_prev_skip = __shfl_sync(full, skippable, 31) || !__shfl_sync(full, valid, 31);
+                n = next;
+                continue;
+            }
+            // round 1: every taken sample -- except, for iso, samples whose
+            // region bound excludes the isovalue: only the sign of s - iso is
+            // ever used for them (crossing tests, bisection bracket), and the
+            // bound's end nearest the isovalue carries it
+            double sv = 0.0;
+            bool cull_iso = false;
+            if (KIND == kIso && tk && a.cull) {
+                short2 bd;
+                if (chain_transparent<kIso>(a, x, y, z, &bd)) {
+                    cull_iso = true;
+                    sv = (double)bd.x > a.isovalue ? (double)bd.x : (double)bd.y;
+                }
+            }
+            if (tk && !cull_iso) {
+                sv = vol_sample<CUBIC>(a, bi, bj, bk, x, y, z);
+            }
+            // round 2: previous values the chunk does not hold -- after a
+            // skipped predecessor (t - step, the reference's gap rule) or, on
+            // lane 0, after a culled run (the predecessor's own position)
+            const bool pred_taken_lane = __shfl_up_sync(full, tk, 1);
+            const double pred_s_lane = __shfl_up_sync(full, sv, 1);
+            bool pvalid;
+            double pv = 0.0;
+            bool need = false;
+            double tq = 0.0;
+            if (lane == 0) {
+                if (c_pending) {
+                    need = tk;
+                    tq = h.t0 + ((double)(m - 1) + 0.5) * a.step;
+                    pvalid = true;
+                } else if (c_prev_valid) {
+                    pvalid = true;
+                    pv = c_prev;
+                } else {
+                    need = tk && m > 0;
+                    tq = t - a.step;
+                    pvalid = m > 0;
+                }
+            } else if (pred_taken_lane) {
+                pvalid = true;
+                pv = pred_s_lane;
+            } else {
+                need = tk;  // predecessor skipped: prev at t - step (m > 0 here)
+                tq = t - a.step;
+                pvalid = true;
+            }
+            if (__any_sync(full, need)) {
+                double qx = x, qy = y, qz = z;
+                int qi = bi, qj = bj, qk = bk;
+                if (need) {
+                    qx = divide(r.ox + tq * r.dx, a.dsx);
+                    qy = divide(r.oy + tq * r.dy, a.dsy);
+                    qz = divide(r.oz + tq * r.dz, a.dsz);
+                    qi = owner(a, 0, qx);
+                    qj = owner(a, 1, qy);
+                    qk = owner(a, 2, qz);
+                }
+                const double q = vol_sample<CUBIC>(a, qi, qj, qk, qx, qy, qz);
+                if (need) pv = q;
+            }
+            if (!tk) pvalid = false;
+            int stop = 32;  // the lane whose sample ends the ray (hit / termination); 32: none
+            if (KIND == kIso) {
+                const bool crossing = tk && pvalid && (pv - a.isovalue) * (sv - a.isovalue) < 0.0;
+                const bool exact = tk && sv == a.isovalue;
+                const unsigned hm = __ballot_sync(full, crossing || exact);
+                if (hm) {
+                    const int hl = __ffs(hm) - 1;
+                    stop = hl;
+                    const bool hc = __shfl_sync(full, crossing, hl);
+                    const double ht = __shfl_sync(full, t, hl);
+                    double thit = ht;
+                    if (hc) {
+                        // 8 bisection rounds on the warp (the hit lane's interval)
+                        double lo_t = ht - a.step, hi_t = ht, lo_s = __shfl_sync(full, pv, hl);
+                        for (int it = 0; it < 8; ++it) {
+                            const double mid = 0.5 * (lo_t + hi_t);
+                            const double mx = divide(r.ox + mid * r.dx, a.dsx);
+                            const double my = divide(r.oy + mid * r.dy, a.dsy);
+                            const double mz = divide(r.oz + mid * r.dz, a.dsz);
+                            const double ms = vol_sample<CUBIC>(a, owner(a, 0, mx), owner(a, 1, my), owner(a, 2, mz),
+                                                                mx, my, mz);
+                            if ((lo_s - a.isovalue) * (ms - a.isovalue) <= 0.0) {
+                                hi_t = mid;
+                            } else {
+                                lo_t = mid;
+                                lo_s = ms;
+                            }
+                        }
+                        thit = 0.5 * (lo_t + hi_t);
+                    }
+                    const double hx = divide(r.ox + thit * r.dx, a.dsx);
+                    const double hy = divide(r.oy + thit * r.dy, a.dsy);
+                    const double hz = divide(r.oz + thit * r.dz, a.dsz);
+                    const int hbi = owner(a, 0, hx), hbj = owner(a, 1, hy), hbk = owner(a, 2, hz);
+                    // gradient: lane q < 6 takes tap q (+x,-x,+y,-y,+z,-z)
+                    double gpx = hx, gpy = hy, gpz = hz;
+                    int gi = hbi, gj = hbj, gk = hbk;
+                    const int q = lane < 6 ? lane : 0;
+                    const double hh = (q & 1) ? -0.5 : 0.5;
+                    const int axis = q >> 1;
+                    gpx = axis == 0 ? hx + hh : hx;
+                    gpy = axis == 1 ? hy + hh : hy;
+                    gpz = axis == 2 ? hz + hh : hz;
+                    const int o = owner(a, axis, axis == 0 ? gpx : axis == 1 ? gpy : gpz);
+                    gi = axis == 0 ? o : gi;
+                    gj = axis == 1 ? o : gj;
+                    gk = axis == 2 ? o : gk;
+                    const double tv = vol_sample<CUBIC>(a, gi, gj, gk, gpx, gpy, gpz);
+                    const double tp0 = __shfl_sync(full, tv, 0), tp1 = __shfl_sync(full, tv, 1);
+                    const double tp2 = __shfl_sync(full, tv, 2), tp3 = __shfl_sync(full, tv, 3);
+                    const double tp4 = __shfl_sync(full, tv, 4), tp5 = __shfl_sync(full, tv, 5);
+                    const double gx = divide(tp0 - tp1, a.dsx), gy = divide(tp2 - tp3, a.dsy),
+                                 gz = divide(tp4 - tp5, a.dsz);
+                    if (lane == 0) ++c_shaded;
+                    const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                    const int ib = lut_bin(a.isovalue, a.lut_lo, a.lut_inv_w, a.nlut);
+                    double cr = __ldg(a.lut + 4 * ib), cg = __ldg(a.lut + 4 * ib + 1), cb = __ldg(a.lut + 4 * ib + 2);
+                    if (LIGHT && norm > 1e-12)
+                        shade(a, cr, cg, cb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                    acc_r = cr;
+                    acc_g = cg;
+                    acc_b = cb;
+                    acc_a = 1.0;
+                    t_hit = thit;
+                }
+            } else {
+                // pre-integrated segments
+                bool contrib = false;
+                double sr = 0.0, sg = 0.0, sb = 0.0, sa = 0.0;
+                if (tk) {
+                    const double sf = pvalid ? pv : sv;
+                    const int fbin = lut_bin(sf, a.tbl_lo, a.tbl_inv_w, a.ntbl);
+                    const int bbin = lut_bin(sv, a.tbl_lo, a.tbl_inv_w, a.ntbl);
+                    const double *cell = a.table + 4 * ((long long)fbin * a.ntbl + bbin);
+                    sa = __ldg(cell + 3);
+                    if (sa > 0.0) {
+                        contrib = true;
+                        sr = __ldg(cell);
+                        sg = __ldg(cell + 1);
+                        sb = __ldg(cell + 2);
+                    }
+                }
+                // the terminating sample: replay A += (1 - A) a in order
+                unsigned cm = __ballot_sync(full, contrib);
+                {
+                    double A = acc_a;
+                    unsigned mm = cm;
+                    while (mm) {
+                        const int src = __ffs(mm) - 1;
+                        mm &= mm - 1;
+                        A += (1.0 - A) * __shfl_sync(full, sa, src);
+                        if (A >= a.term_alpha) {
+                            stop = src;
+                            break;
+                        }
+                    }
+                }
+                const unsigned upto = stop >= 31 ? full : ((2u << stop) - 1u);
+                const unsigned vis = cm & upto;
+                if (LIGHT && vis) {
+                    // 6 gradient taps per contributing sample, 32 per round
+                    const int ntaps = 6 * __popc(vis);
+                    const int rank = __popc(vis & lower);
+                    double tp[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                    for (int base = 0; base < ntaps; base += 32) {
+                        const int id = base + lane;
+                        const bool act = id < ntaps;
+                        const int k = id / 6, g = id - 6 * k;
+                        const int src = act ? nth_bit(vis, k) : lane;
+                        double px = __shfl_sync(full, x, src), py = __shfl_sync(full, y, src);
+                        double pz = __shfl_sync(full, z, src);
+                        int qi = __shfl_sync(full, bi, src), qj = __shfl_sync(full, bj, src);
+                        int qk = __shfl_sync(full, bk, src);
+                        const double hh = (g & 1) ? -0.5 : 0.5;
+                        const int axis = g >> 1;
+                        px = axis == 0 ? px + hh : px;
+                        py = axis == 1 ? py + hh : py;
+                        pz = axis == 2 ? pz + hh : pz;
+                        const int o = owner(a, axis, axis == 0 ? px : axis == 1 ? py : pz);
+                        qi = axis == 0 ? o : qi;
+                        qj = axis == 1 ? o : qj;
+                        qk = axis == 2 ? o : qk;
+                        const double v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
+#pragma unroll
+                        for (int gg = 0; gg < 6; ++gg) {
+                            const int sidx = 6 * rank + gg - base;
+                            const double w = __shfl_sync(full, v, sidx & 31);
+                            if (sidx >= 0 && sidx < 32) tp[gg] = w;
+                        }
+                    }
+                    if ((vis >> lane) & 1u) {
+                        const double gx = divide(tp[0] - tp[1], a.dsx), gy = divide(tp[2] - tp[3], a.dsy),
+                                     gz = divide(tp[4] - tp[5], a.dsz);
+                        const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                        if (norm > 1e-12) {
+                            const double ndl = fabs(((gx * -r.dx + gy * -r.dy) + gz * -r.dz) / norm);
+                            const double scale = a.ka + a.kd * ndl;
+                            const double spec = a.ks * vr_pow(ndl, a.shin) * sa;
+                            sr = clampf(scale * sr + spec, 0.0, 1.0);
+                            sg = clampf(scale * sg + spec, 0.0, 1.0);
+                            sb = clampf(scale * sb + spec, 0.0, 1.0);
+                        }
+                    }
+                    if (lane == 0) c_shaded += __popc(vis);
+                }
+                // composite in sample order (_kernels.py:574-579)
+                unsigned mm = vis;
+                while (mm) {
+                    const int src = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    const double w = 1.0 - acc_a;
+                    acc_r += w * __shfl_sync(full, sr, src);
+                    acc_g += w * __shfl_sync(full, sg, src);
+                    acc_b += w * __shfl_sync(full, sb, src);
+                    acc_a += w * __shfl_sync(full, sa, src);
+                }
+            }
+            // counts up to and including the stopping sample; blocks hit
+            const unsigned upto = stop >= 31 ? full : ((2u << stop) - 1u);
+            taken += __popc(tmask & upto);
+            skipped += __popc(vmask & ~tmask & upto);
+            if (lane == 0) c_eval += __popc(tmask & upto);  // (samples evaluated or provably one-sided)
+            if (tk && lane <= stop && a.blocks_hit) a.blocks_hit[b] = 1;
+            if (stop < 32) {
+                done = true;
+                break;
+            }
+            // carry the chunk's last sample into the next chunk
+            const bool last_tk = __shfl_sync(full, tk, 31);
+            c_prev = __shfl_sync(full, sv, 31);
+            c_prev_valid = last_tk;
+            c_pending = false;
+            c_prev_skip = __shfl_sync(full, skippable, 31);
+            n += 32;
+        }
+        if (lane == 0) {
+            const double w = 1.0 - acc_a;
+            const double rr = acc_r + w * a.bg[0] * a.bg[3];
+            const double gg = acc_g + w * a.bg[1] * a.bg[3];
+            const double bb = acc_b + w * a.bg[2] * a.bg[3];
+            const double aa = acc_a + w * a.bg[3];
+            const long long p = h.out;
+            if (a.premult) reinterpret_cast<double4 *>(a.premult)[p] = make_double4(rr, gg, bb, aa);
+            if (a.pixels) {
+                double r0 = 0.0, g0 = 0.0, b0 = 0.0;
+                if (aa > 0.0) {
+                    const double den = aa > 1e-12 ? aa : 1e-12;
+                    r0 = rr / den;
+                    g0 = gg / den;
+                    b0 = bb / den;
+                }
+                reinterpret_cast<uchar4 *>(a.pixels)[p] = make_uchar4(to_u8(r0), to_u8(g0), to_u8(b0), to_u8(aa));
+            }
+            if (a.depth) a.depth[p] = t_hit;
+            if (a.taken) a.taken[p] = taken;
+            if (a.skipped) a.skipped[p] = skipped;
+            c_taken += (unsigned long long)taken;
+            c_skip += (unsigned long long)skipped;
+        }
+    }
+    c_taken = warp_sum(c_taken);
+    c_skip = warp_sum(c_skip);
+    if (lane == 0 && a.totals && (c_taken | c_skip)) {
+        atomicAdd(a.totals, c_taken);
+        atomicAdd(a.totals + 1, c_skip);
+    }
+    if (a.work) {
+        c_shaded = warp_sum(c_shaded);
+        c_eval = warp_sum(c_eval);
+        c_iter = warp_sum(c_iter);
+        if (lane == 0) {
+            if (c_shaded) atomicAdd(a.work, c_shaded);
+            if (c_eval) atomicAdd(a.work + 1, c_eval);
+            if (c_iter) atomicAdd(a.work + 2, c_iter);
+        }
+    }
+}
+
 template <int KIND, bool CUBIC, bool LIGHT>
 KernelFn pick_chain_skip(bool skip) {
     return skip ? raycast_chain_kernel<KIND, CUBIC, LIGHT, true> : raycast_chain_kernel<KIND, CUBIC, LIGHT, false>;
@@ -2113,6 +2598,22 @@ KernelFn pick_chain_kind(const RenderArgs &a) {
 
 KernelFn pick_chain(const RenderArgs &a) {
     return a.mode == 1 ? pick_chain_kind<kIso>(a) : pick_chain_kind<kPreint>(a);
+}
+
+template <int KIND, bool CUBIC, bool LIGHT>
+KernelFn pick_chain_coop_skip(bool skip) {
+    return skip ? raycast_chain_coop_kernel<KIND, CUBIC, LIGHT, true> : raycast_chain_coop_kernel<KIND, CUBIC, LIGHT, false>;
+}
+
+template <int KIND>
+KernelFn pick_chain_coop_kind(const RenderArgs &a) {
+    const bool c = a.cubic != 0, l = a.lighting != 0, s = a.skip_empty != 0;
+    if (c) return l ? pick_chain_coop_skip<KIND, true, true>(s) : pick_chain_coop_skip<KIND, true, false>(s);
+    return l ? pick_chain_coop_skip<KIND, false, true>(s) : pick_chain_coop_skip<KIND, false, false>(s);
+}
+
+KernelFn pick_chain_coop(const RenderArgs &a) {
+    return a.mode == 1 ? pick_chain_coop_kind<kIso>(a) : pick_chain_coop_kind<kPreint>(a);
 }
 
 KernelFn pick(const RenderArgs &a) {
@@ -2185,6 +2686,12 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
         const long long most = (long long)a.slots * (kThreads / kPersistThreads);
         if (ctas > most) ctas = most;
         k<<<(unsigned)ctas, kPersistThreads, 0, stream>>>(a);
+        if (a.heavy) {
+            KernelFn h = pick_chain_coop(a);
+            cudaError_t e = launch_pdl(h, (unsigned)(device_sms() * persistent_ctas_per_sm(h)), kPersistThreads, 0,
+                                       stream, a);
+            if (e != cudaSuccess) return e;
+        }
         return cudaGetLastError();
     }
     pick(a)<<<(unsigned)((long long)a.slots * a.nviews), kThreads, 0, stream>>>(a);

@@ -105,6 +105,7 @@ constexpr int kThreads = 128;
 #endif
 constexpr int kPersistThreads = VR_PERSIST_THREADS;  // CTA size of the persistent ray casters
 constexpr size_t kHeavyRayBytes = 128;  // sizeof(HeavyRay) in vr_raycast.cu
+constexpr size_t kChainRecBytes = 144;  // sizeof(ChainRec): chained-mode hand-off record
 // views per persistent launch pair of a batched sweep; measured at C5:
 // 1 (901 views/s) > 4 (844) > 16 (831) -- each view's tail rays are best
 // handed to the cooperative kernel as in a single frame
