@@ -56,6 +56,8 @@ struct vr_volume {
     short2 *cubes;    // per unit cube: bounds of the interpolant (vr_prep.cuh launch_interp_bounds), brick order
     short2 *mcells;   // per 16^3 macro cell: union of its cells
     int nmx, nmy, nmz;
+    short2 *rcells = nullptr;   // pre-classified culling: raw voxel range of each cell's sample footprint
+    short2 *rmcells = nullptr;  // ... and its union per 16^3 macro cell
     // VR_SAMPLER_TEX builds only (sampling-path A/B): a 3-D texture of x-quads,
     // texel (x, y, z) = voxels x .. x+3 of row (y, z) as short4
     cudaArray_t qarr = nullptr;
@@ -70,6 +72,8 @@ static void free_volume(vr_volume *v) {
     cudaFree(v->bricks);
     cudaFree(v->cubes);
     cudaFree(v->mcells);
+    cudaFree(v->rcells);
+    cudaFree(v->rmcells);
     delete v;
 }
 
@@ -277,6 +281,11 @@ static int finish_volume(vr_volume *v, cudaStream_t s, vr_volume **out) {
         v->qtex = (unsigned long long)tex;
     }
 #endif
+    if (e == cudaSuccess) e = cudaMalloc((void **)&v->rcells, sizeof(short2) * (size_t)v->ncx * v->ncy * v->ncz);
+    if (e == cudaSuccess) e = cudaMalloc((void **)&v->rmcells, sizeof(short2) * (size_t)v->nmx * v->nmy * v->nmz);
+    if (e == cudaSuccess)
+        e = vr::launch_raw_bounds(v->data, (int)v->nx, (int)v->ny, (int)v->nz, v->ncx, v->ncy, v->ncz, v->rcells,
+                                  v->nmx, v->nmy, v->nmz, v->rmcells, s);
     if (e == cudaSuccess) e = cudaMallocAsync((void **)&d_range, 2 * sizeof(int), s);
     if (e == cudaSuccess) e = vr::launch_value_range(v->data, n, d_range, s);
     int h[2] = {0, 0};
@@ -804,10 +813,25 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
     // chained modes (iso, pre-integrated): transparency culling of runs
     const bool chained_cull = vol->cells && !post &&
                               (a.mode == VR_MODE_ISO || (a.mode == VR_MODE_DVR && a.classify == VR_CLS_PREINT));
+    // pre-classified: culling on raw footprint bounds against the frame's
+    // non-zero-alpha value range (computed after the setup kernel)
+    Scratch pre_rng(s);
+    const bool pre_cull = vol->rcells && a.mode == VR_MODE_DVR && a.classify == VR_CLS_PRE;
+    if (pre_cull) {
+        VR_CUDA(pre_rng.alloc(16));
+        a.pre_range = (const int *)pre_rng.p;
+        a.cells = vol->rcells;
+        a.ncx = vol->ncx;
+        a.ncy = vol->ncy;
+        a.mcells = vol->rmcells;
+        a.nmx = vol->nmx;
+        a.nmy = vol->nmy;
+        a.cull = 1;
+    }
     Scratch tbl_nz(s), chain_q(s);
-    if (chained_cull && nviews == 1) {
-        // the persistent chained-mode kernel's ray queue head, then the
-        // hand-off queue's pushed / claimed counters
+    if ((chained_cull || pre_cull) && nviews == 1) {
+        // the persistent per-lane kernel's ray queue head (iso, pre-integrated,
+        // pre-classified), then the hand-off queue's pushed / claimed counters
         VR_CUDA(chain_q.alloc(32));
         a.work_counter = (unsigned long long *)chain_q.p;
         zero.p[0] = a.work_counter;
@@ -817,6 +841,10 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         const long long items = a.items_per_view;
         a.heavy_cap = items < (1LL << 20) ? items : (1LL << 20);
         a.heavy_min_left = VR_HEAVY_MIN_LEFT;
+        // dense lit rays hand over early, as in the post-classified path (iso
+        // rays composite once, at their hit: never)
+        a.heavy_vis_alpha = VR_HEAVY_VIS_ALPHA;
+        a.heavy_vis = prm->lighting && prm->term_alpha < 1.0 && a.mode == VR_MODE_DVR ? VR_HEAVY_VIS : 1 << 30;
         if (a.heavy_min_left > 0) {
             VR_CUDA(heavy.alloc((size_t)a.heavy_cap * vr::kChainRecBytes));
             a.heavy = heavy.p;
@@ -860,6 +888,9 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         if (zero.nb) VR_CUDA(cudaMemsetAsync(zero.b, 0, zero.nb, s));
     }
     if (a.tbl_nz) VR_CUDA(vr::launch_tbl_nonzero(a.table, a.ntbl, (int *)tbl_nz.p, s));
+    if (pre_cull)
+        VR_CUDA(vr::launch_pre_range(lut, prm->nlut, prm->lut_lo, (prm->lut_hi - prm->lut_lo) / (double)prm->nlut,
+                                     vol->vmin, vol->vmax, (int *)pre_rng.p, s));
 #ifdef VR_DEBUG_TIMES
     a.debug_times = g_debug_times;
 #endif

@@ -925,6 +925,78 @@ __global__ void __launch_bounds__(kBlock) macro_from_cells_kernel(const short2 *
     }
 }
 
+// Raw footprint bounds for the pre-classified mode: rcells[c] = min / max of
+// the voxels a sample based in cell c can read -- [4c-1, 4c+5] per axis (a
+// Catmull-Rom base voxel g in [4c, 4c+3] reads g-1 .. g+2; block-local
+// clamping only pulls taps inwards), clipped to the volume.  A cell whose raw
+// voxels all classify to a zero alpha plane interpolates alpha exactly 0.
+__global__ void __launch_bounds__(kBlock) raw_cell_kernel(const int16_t *__restrict__ vol, int nx, int ny, int nz,
+                                                          int ncx, int ncy, int ncz, short2 *rcells) {
+    const long long n = (long long)ncx * ncy * ncz;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < n; c += (long long)gridDim.x * blockDim.x) {
+        const int cx = (int)(c % ncx);
+        const long long r = c / ncx;
+        const int cy = (int)(r % ncy), cz = (int)(r / ncy);
+        const int x0 = max(4 * cx - 1, 0), x1 = min(4 * cx + 5, nx - 1);
+        const int y0 = max(4 * cy - 1, 0), y1 = min(4 * cy + 5, ny - 1);
+        const int z0 = max(4 * cz - 1, 0), z1 = min(4 * cz + 5, nz - 1);
+        int lo = INT_MAX, hi = INT_MIN;
+        for (int z = z0; z <= z1; ++z)
+            for (int y = y0; y <= y1; ++y) {
+                const int16_t *row = vol + ((long long)z * ny + y) * nx;
+                for (int x = x0; x <= x1; ++x) {
+                    const int v = __ldg(row + x);
+                    lo = min(lo, v);
+                    hi = max(hi, v);
+                }
+            }
+        rcells[c] = make_short2((short)lo, (short)hi);
+    }
+}
+
+cudaError_t launch_raw_bounds(const int16_t *vol, int nx, int ny, int nz, int ncx, int ncy, int ncz, short2 *rcells,
+                              int nmx, int nmy, int nmz, short2 *rmcells, cudaStream_t s) {
+    const long long nc = (long long)ncx * ncy * ncz;
+    raw_cell_kernel<<<grid_for(nc, kBlock, 32), kBlock, 0, s>>>(vol, nx, ny, nz, ncx, ncy, ncz, rcells);
+    const long long nm = (long long)nmx * nmy * nmz;
+    macro_from_cells_kernel<<<grid_for(nm, kBlock, 32), kBlock, 0, s>>>(rcells, ncx, ncy, ncz, nmx, nmy, nmz,
+                                                                             rmcells);
+    return cudaGetLastError();
+}
+
+// Per frame, pre-classified mode: the smallest and largest int16 value in
+// [vmin, vmax] whose pre-classified alpha plane is non-zero, i.e.
+// rint(lut[classified_bin(v)].alpha * 255) >= 1 (as preclassify_kernel paints
+// it); out = (INT_MAX, INT_MIN) when none.
+__global__ void pre_range_kernel(const double *lut, int nbins, double lo, double bw, int vmin, int vmax, int *out) {
+    pdl_enter();
+    __shared__ int first, last;
+    if (threadIdx.x == 0) {
+        first = INT_MAX;
+        last = INT_MIN;
+    }
+    __syncthreads();
+    for (int v = vmin + (int)threadIdx.x; v <= vmax; v += blockDim.x) {
+        const int k = classified_bin((double)v, lo, bw, nbins);
+        if ((uint8_t)rint(__ldg(lut + 4 * k + 3) * 255.0) != 0) {
+            atomicMin(&first, v);
+            atomicMax(&last, v);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        out[0] = first;
+        out[1] = last;
+    }
+}
+
+cudaError_t launch_pre_range(const double *lut, int nbins, double lut_lo, double bin_width, int vmin, int vmax,
+                             int *out, cudaStream_t s) {
+    cudaError_t e = launch_pdl(pre_range_kernel, 1, 1024, 0, s, lut, nbins, lut_lo, bin_width, vmin, vmax, out);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int bnx, int bny, short2 *cubes,
                                  int ncx, int ncy, int ncz, short2 *cells, int nmx, int nmy, int nmz, short2 *mcells,
                                  cudaStream_t s) {

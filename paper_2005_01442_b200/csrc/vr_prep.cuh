@@ -84,6 +84,12 @@ cudaError_t launch_interp_bounds(const int16_t *vol, int nx, int ny, int nz, int
 // range[0..1] as above, range[2..3] = the integer value thresholds of that bin range
 // under the march's bin formula (visible_value_range, lut_inv_w = nbins / (hi - lo))
 // 2-D prefix count of pre-integrated table cells with opacity > 0 ((n+1)^2 ints)
+// pre-classified culling: raw footprint bounds per cell / macro cell (once per
+// volume) and the per-frame non-zero-alpha value range
+cudaError_t launch_raw_bounds(const int16_t *vol, int nx, int ny, int nz, int ncx, int ncy, int ncz, short2 *rcells,
+                              int nmx, int nmy, int nmz, short2 *rmcells, cudaStream_t s);
+cudaError_t launch_pre_range(const double *lut, int nbins, double lut_lo, double bin_width, int vmin, int vmax,
+                             int *out, cudaStream_t s);
 cudaError_t launch_tbl_nonzero(const double *table, int n, int *nz, cudaStream_t s);
 cudaError_t launch_lut_range(const double *lut, int nbins, double lut_lo, double lut_inv_w, int *range,
                              const ZeroSpec &zero, cudaStream_t s);

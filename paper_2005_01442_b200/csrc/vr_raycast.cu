@@ -355,6 +355,20 @@ VR_D int chain_transparent(const RenderArgs &a, double x, double y, double z, sh
     return 2;
 }
 
+// Pre-classified culling: the level (4 macro cell, 2 cell; 0 none) of the
+// region around (x, y, z) whose raw footprint bound (a.cells / a.mcells hold
+// raw voxel ranges in this mode) lies outside the frame's non-zero-alpha
+// value range: every tap of every sample based there has a zero alpha plane.
+VR_D int pre_transparent(const RenderArgs &a, double x, double y, double z) {
+    const int gx = clampi((int)x, 0, a.L.n[0] - 1), gy = clampi((int)y, 0, a.L.n[1] - 1);
+    const int gz = clampi((int)z, 0, a.L.n[2] - 1);
+    const int plo = __ldg(a.pre_range), phi = __ldg(a.pre_range + 1);
+    const short2 mb = __ldg(a.mcells + ((long long)(gz >> 4) * a.nmy + (gy >> 4)) * a.nmx + (gx >> 4));
+    if ((int)mb.y < plo || (int)mb.x > phi) return 4;
+    const short2 cb = __ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2));
+    return ((int)cb.y < plo || (int)cb.x > phi) ? 2 : 0;
+}
+
 // Parameter interval in which the (exact) ray lies inside the box [lo, hi]
 // expanded by delta on every side; returns false when it never does.  For an
 // axis the ray does not move along, the computed coordinate is exactly
@@ -647,7 +661,22 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
                     }
                 }
             } else if (KIND == kPre) {
-                // pre-classified (_kernels.py:471-507)
+                // pre-classified (_kernels.py:471-507).  Culling: when every voxel
+                // a sample in this cell (macro cell) can read has a zero alpha
+                // plane, its interpolated alpha is exactly 0 -- nothing composited
+                if (a.cull) {
+                    const int lvl = pre_transparent(a, x, y, z);
+                    if (lvl) {
+                        const double p[3] = {x, y, z};
+                        const int bidx[3] = {bi, bj, bk};
+                        long long k = culled_run<SKIP>(a, r, inv, t0, n, t, p, bidx, rec, lvl);
+                        if (k > N - n) k = N - n;
+                        n_taken += k - 1;
+                        n += k;
+                        continue;
+                    }
+                }
+                ++n_eval;
                 double sa = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 3);
                 if (sa > 0.0) {
                     double sr = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 0);
@@ -778,7 +807,7 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
     res.taken = n_taken;
     res.skipped = n_skip;
     res.shaded = n_shaded;
-    res.eval = KIND == kPost ? n_eval : n_taken;
+    res.eval = (KIND == kPost || KIND == kPre) ? n_eval : n_taken;
     res.iter = n_iter;
     return res;
 }
@@ -1651,7 +1680,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
 // the next ray at once.  After each evaluated sample, a run of samples whose
 // interpolant bound rules out any contribution (chain_transparent) is
 // counted as taken and leapt over, exactly as raycast_kernel does.
-enum ChainStage { kcNone = -1, kcSample = 0, kcPrevExact = 1, kcPrevGap = 2, kcBisect = 3, kcGrad = 11 };
+enum ChainStage { kcNone = -1, kcSample = 0, kcPrevExact = 1, kcPrevGap = 2, kcBisect = 3, kcGrad = 11, kcRGB = 17 };
 
 // A chained-mode ray handed to the cooperative kernel: everything needed to
 // continue it exactly where it stopped.
@@ -1684,6 +1713,7 @@ struct ChainRay {
     int bi, bj, bk, hbi, hbj, hbk;
     int stage;
     int last_hit;
+    int nvis;  // samples composited so far (dense-ray hand-off)
     bool prev_valid, prev_pending, prev_skippable, live;
 };
 
@@ -1740,6 +1770,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                     R.t_hit = __longlong_as_double(0x7ff8000000000000LL);  // NaN: no hit
                     R.stage = kcNone;
                     R.last_hit = -1;
+                    R.nvis = 0;
                     R.live = true;
                 }
             }
@@ -1756,7 +1787,11 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
         // ---- once the queue has drained, long rays go to the cooperative
         // kernel at a clean point (the frame would otherwise end with a few
         // lanes walking long rays alone)
-        if (a.heavy && drained && R.stage == kcNone && R.N - R.n >= a.heavy_min_left) {
+        // (dense lit rays -- several composited samples, still far from
+        // termination -- go at once: the cooperative kernel spreads their
+        // gradient taps over the warp)
+        if (a.heavy && R.stage == kcNone && R.N - R.n >= a.heavy_min_left &&
+            (drained || (R.nvis >= a.heavy_vis && R.acc_a < a.heavy_vis_alpha))) {
             const unsigned long long slot = atomicAdd(a.heavy_count, 1ull);
             if (slot < (unsigned long long)a.heavy_cap) {
                 ChainRec h;
@@ -1796,9 +1831,9 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
             const double z = divide(R.r.oz + t * R.r.dz, a.dsz);
             const int bi = owner(a, 0, x), bj = owner(a, 1, y), bk = owner(a, 2, z);
             const int b = (bk * nby + bj) * nbx + bi;
+            BlockRec rec = {};
             if (SKIP) {
                 bool skippable, cell_only = true;
-                BlockRec rec = {};
                 if (KIND == kIso) {
                     skippable = (double)__ldg(a.vmax + b) < a.isovalue || (double)__ldg(a.vmin + b) > a.isovalue;
                 } else {
@@ -1806,7 +1841,8 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                     skippable = dvr_skippable(rec, x, y, z);
                     cell_only = rec.lo.w != 0.0f;
                 }
-                if (skippable && R.prev_skippable) {  // chained: the first sample of a gap is taken
+                // chained modes take the first sample of a gap; pre skips every skippable sample
+                if (skippable && (KIND == kPre || R.prev_skippable)) {
                     const double p[3] = {x, y, z};
                     const int bidx[3] = {bi, bj, bk};
                     long long k = leap_count<KIND>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec, cell_only);
@@ -1824,6 +1860,21 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                 R.last_hit = b;
             }
             R.taken += 1;
+            if (KIND == kPre && chain_cull) {
+                // every voxel a sample in this (macro) cell can read has a zero
+                // alpha plane: its interpolated alpha is exactly 0
+                const int lvl = pre_transparent(a, x, y, z);
+                if (lvl) {
+                    const double p[3] = {x, y, z};
+                    const int bidx[3] = {bi, bj, bk};
+                    long long k = culled_run<SKIP>(a, R.r, R.inv, R.t0, n, t, p, bidx, rec, lvl);
+                    if (k > R.N - n) k = R.N - n;
+                    if (k < 1) k = 1;
+                    R.taken += k - 1;
+                    R.n = n + k;
+                    continue;
+                }
+            }
             if (KIND == kIso && chain_cull && !R.prev_pending && (R.prev_valid || n == 0)) {
                 // A sample whose region bound excludes the isovalue needs no
                 // interpolation: only the sign of s - iso is ever used (the
@@ -1865,7 +1916,8 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
             R.bi = bi;
             R.bj = bj;
             R.bk = bk;
-            R.stage = R.prev_pending ? kcPrevExact : ((!R.prev_valid && n > 0) ? kcPrevGap : kcSample);
+            R.stage = KIND == kPre ? kcSample
+                                   : (R.prev_pending ? kcPrevExact : ((!R.prev_valid && n > 0) ? kcPrevGap : kcSample));
         }
 
         // ---- phase B: one interpolation
@@ -1911,8 +1963,50 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                 qj = owner(a, 1, py);
                 qk = owner(a, 2, pz);
             }
-            const double v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
-            if (R.stage == kcPrevExact || R.stage == kcPrevGap) {
+            double v;
+            if (KIND == kPre && (R.stage == kcSample || R.stage >= kcRGB)) {
+                // a pre-classified plane (_attr_rgba, _kernels.py:256-276): alpha first, then r, g, b
+                v = attr_rgba<CUBIC>(a, R.bi, R.bj, R.bk, R.x, R.y, R.z, R.stage == kcSample ? 3 : R.stage - kcRGB);
+            } else {
+                v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
+            }
+            if (KIND == kPre && R.stage == kcSample) {
+                // _kernels.py:471-507
+                ++c_eval;
+                if (v > 0.0) {
+                    R.ca = 1.0 - vr_pow(1.0 - v, a.corr);  // ahat
+                    R.stage = kcRGB;
+                } else {
+                    R.stage = kcNone;
+                    R.n += 1;
+                }
+            } else if (KIND == kPre && R.stage >= kcRGB) {
+                const int ch = R.stage - kcRGB;
+                if (ch == 0) R.cr = v;
+                else if (ch == 1) R.cg = v;
+                else R.cb = v;
+                if (ch < 2) {
+                    R.stage += 1;
+                } else if (LIGHT) {
+                    R.hx = R.x;
+                    R.hy = R.y;
+                    R.hz = R.z;
+                    R.hbi = R.bi;
+                    R.hbj = R.bj;
+                    R.hbk = R.bk;
+                    R.stage = kcGrad;
+                } else {
+                    const double w = (1.0 - R.acc_a) * R.ca;
+                    R.acc_r += w * R.cr;
+                    R.acc_g += w * R.cg;
+                    R.acc_b += w * R.cb;
+                    R.acc_a += w;
+                    ++R.nvis;
+                    R.stage = kcNone;
+                    R.n += 1;
+                    if (R.acc_a >= a.term_alpha) finished = true;
+                }
+            } else if (R.stage == kcPrevExact || R.stage == kcPrevGap) {
                 R.prev_s = v;
                 R.prev_valid = true;
                 R.prev_pending = false;
@@ -1965,6 +2059,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                             R.acc_g += w * R.cg;
                             R.acc_b += w * R.cb;
                             R.acc_a += w * R.ca;
+                            ++R.nvis;
                             if (R.acc_a >= a.term_alpha) finished = true;
                         }
                     }
@@ -2031,7 +2126,21 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                     const double gx = divide(R.gx, a.dsx), gy = divide(R.gy, a.dsy), gz = divide(R.gz, a.dsz);
                     ++c_shaded;
                     const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
-                    if (KIND == kIso) {
+                    if (KIND == kPre) {
+                        // _kernels.py:495-507
+                        double sr = R.cr, sg = R.cg, sb = R.cb;
+                        if (norm > 1e-12)
+                            shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
+                        const double w = (1.0 - R.acc_a) * R.ca;
+                        R.acc_r += w * sr;
+                        R.acc_g += w * sg;
+                        R.acc_b += w * sb;
+                        R.acc_a += w;
+                        ++R.nvis;
+                        R.stage = kcNone;
+                        R.n += 1;
+                        if (R.acc_a >= a.term_alpha) finished = true;
+                    } else if (KIND == kIso) {
                         // _kernels.py:466-483: LUT colour at the isovalue, shaded, opaque
                         const int ib = lut_bin(a.isovalue, a.lut_lo, a.lut_inv_w, a.nlut);
                         double cr = __ldg(a.lut + 4 * ib), cg = __ldg(a.lut + 4 * ib + 1), cb = __ldg(a.lut + 4 * ib + 2);
@@ -2059,6 +2168,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                         R.acc_g += w * seg_g;
                         R.acc_b += w * seg_b;
                         R.acc_a += w * seg_a;
+                        ++R.nvis;
                         if (R.acc_a >= a.term_alpha) {
                             finished = true;
                         } else {
@@ -2248,7 +2358,155 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_COOP_MIN_BLOCKS *(kT
         double t_hit = __longlong_as_double(0x7ff8000000000000LL);
         long long n = h.n;
         bool done = false;
-        while (n < h.N && !done) {
+        while (KIND == kPre && n < h.N) {
+            // ---- pre-classified chunk (_kernels.py:471-507): not chained
+            ++c_iter;
+            const long long m = n + lane;
+            const bool valid = m < h.N;
+            double t = 0.0, x = 0.0, y = 0.0, z = 0.0;
+            int bi = 0, bj = 0, bk = 0, b = 0, lvl = 0;
+            bool skippable = false, cell_only = true;
+            BlockRec rec = {};
+            if (valid) {
+                t = h.t0 + ((double)m + 0.5) * a.step;
+                x = divide(r.ox + t * r.dx, a.dsx);
+                y = divide(r.oy + t * r.dy, a.dsy);
+                z = divide(r.oz + t * r.dz, a.dsz);
+                bi = owner(a, 0, x);
+                bj = owner(a, 1, y);
+                bk = owner(a, 2, z);
+                b = (bk * nby + bj) * nbx + bi;
+                if (SKIP) {
+                    rec = block_rec(a, b);
+                    skippable = dvr_skippable(rec, x, y, z);
+                    cell_only = rec.lo.w != 0.0f;
+                }
+                if (!skippable && a.cull) lvl = pre_transparent(a, x, y, z);
+            }
+            const bool tk = valid && !skippable;
+            const bool cand = tk && lvl == 0;
+            const unsigned tmask = __ballot_sync(full, tk), vmask = __ballot_sync(full, valid);
+            const unsigned candm = __ballot_sync(full, cand);
+            if (candm == 0u) {
+                // nothing to evaluate: extend by a provable run from the last sample
+                long long k = 1;
+                if (lane == 31 && valid) {
+                    const double p[3] = {x, y, z};
+                    const int bidx[3] = {bi, bj, bk};
+                    k = skippable ? leap_count<kPre>(a, r, inv, h.t0, m, t, p, bidx, rec, cell_only)
+                                  : culled_run<SKIP>(a, r, inv, h.t0, m, t, p, bidx, rec, lvl);
+                }
+                k = __shfl_sync(full, k, 31);
+                const bool last_skip = __shfl_sync(full, skippable, 31);
+                taken += __popc(tmask);
+                skipped += __popc(vmask & ~tmask);
+                if (tk && a.blocks_hit) a.blocks_hit[b] = 1;
+                long long next = n + 32;
+                const long long last = n + 31;
+                if (last < h.N && k > 1) {
+                    if (k > h.N - last) k = h.N - last;
+                    if (last_skip)
+                        skipped += k - 1;
+                    else
+                        taken += k - 1;
+                    next = last + k;
+                }
+                n = next;
+                continue;
+            }
+            // alpha of every candidate, then the terminating sample by replaying
+            // A += (1 - A) ahat in sample order
+            double sa = 0.0, ahat = 0.0;
+            if (cand) sa = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 3);
+            const bool contrib = cand && sa > 0.0;
+            if (contrib) ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
+            const unsigned cm = __ballot_sync(full, contrib);
+            int stop = 32;
+            {
+                double A = acc_a;
+                unsigned mm = cm;
+                while (mm) {
+                    const int src = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    A += (1.0 - A) * __shfl_sync(full, ahat, src);
+                    if (A >= a.term_alpha) {
+                        stop = src;
+                        break;
+                    }
+                }
+            }
+            const unsigned upto = stop >= 31 ? full : ((2u << stop) - 1u);
+            const unsigned vis = cm & upto;
+            // r, g, b (and 6 gradient taps with lighting) of every visible sample,
+            // spread over the lanes, 32 per round
+            constexpr int J = LIGHT ? 9 : 3;
+            double jv[J];
+#pragma unroll
+            for (int g = 0; g < J; ++g) jv[g] = 0.0;
+            if (vis) {
+                const int njobs = J * __popc(vis);
+                const int rank = __popc(vis & lower);
+                for (int base = 0; base < njobs; base += 32) {
+                    const int id = base + lane;
+                    const bool act = id < njobs;
+                    const int k = id / J, g = id - J * k;
+                    const int src = act ? nth_bit(vis, k) : lane;
+                    double px = __shfl_sync(full, x, src), py = __shfl_sync(full, y, src);
+                    double pz = __shfl_sync(full, z, src);
+                    int qi = __shfl_sync(full, bi, src), qj = __shfl_sync(full, bj, src);
+                    int qk = __shfl_sync(full, bk, src);
+                    double v = 0.0;
+                    if (g < 3) {
+                        v = attr_rgba<CUBIC>(a, qi, qj, qk, px, py, pz, g);
+                    } else {
+                        const int q = g - 3;
+                        const double hh = (q & 1) ? -0.5 : 0.5;
+                        const int axis = q >> 1;
+                        px = axis == 0 ? px + hh : px;
+                        py = axis == 1 ? py + hh : py;
+                        pz = axis == 2 ? pz + hh : pz;
+                        const int o = owner(a, axis, axis == 0 ? px : axis == 1 ? py : pz);
+                        qi = axis == 0 ? o : qi;
+                        qj = axis == 1 ? o : qj;
+                        qk = axis == 2 ? o : qk;
+                        v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
+                    }
+#pragma unroll
+                    for (int gg = 0; gg < J; ++gg) {
+                        const int sidx = J * rank + gg - base;
+                        const double w = __shfl_sync(full, v, sidx & 31);
+                        if (sidx >= 0 && sidx < 32) jv[gg] = w;
+                    }
+                }
+            }
+            double sr = jv[0], sg = jv[1], sb = jv[2];
+            if (LIGHT && ((vis >> lane) & 1u)) {
+                const double gx = divide(jv[J - 6] - jv[J - 5], a.dsx), gy = divide(jv[J - 4] - jv[J - 3], a.dsy),
+                             gz = divide(jv[J - 2] - jv[J - 1], a.dsz);
+                const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                if (norm > 1e-12) shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+            }
+            if (LIGHT && lane == 0) c_shaded += __popc(vis);
+            {
+                unsigned mm = vis;
+                while (mm) {
+                    const int src = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    const double w = (1.0 - acc_a) * __shfl_sync(full, ahat, src);
+                    acc_r += w * __shfl_sync(full, sr, src);
+                    acc_g += w * __shfl_sync(full, sg, src);
+                    acc_b += w * __shfl_sync(full, sb, src);
+                    acc_a += w;
+                }
+            }
+            taken += __popc(tmask & upto);
+            skipped += __popc(vmask & ~tmask & upto);
+            if (lane == 0) c_eval += __popc(candm & upto);
+            if (tk && lane <= stop && a.blocks_hit) a.blocks_hit[b] = 1;
+            if (stop < 32) break;
+            n += 32;
+        }
+        while (KIND != kPre && n < h.N && !done) {
             ++c_iter;
             const long long m = n + lane;
             const bool valid = m < h.N;
@@ -2597,7 +2855,8 @@ KernelFn pick_chain_kind(const RenderArgs &a) {
 }
 
 KernelFn pick_chain(const RenderArgs &a) {
-    return a.mode == 1 ? pick_chain_kind<kIso>(a) : pick_chain_kind<kPreint>(a);
+    if (a.mode == 1) return pick_chain_kind<kIso>(a);
+    return a.classify == 1 ? pick_chain_kind<kPre>(a) : pick_chain_kind<kPreint>(a);
 }
 
 template <int KIND, bool CUBIC, bool LIGHT>
@@ -2613,7 +2872,8 @@ KernelFn pick_chain_coop_kind(const RenderArgs &a) {
 }
 
 KernelFn pick_chain_coop(const RenderArgs &a) {
-    return a.mode == 1 ? pick_chain_coop_kind<kIso>(a) : pick_chain_coop_kind<kPreint>(a);
+    if (a.mode == 1) return pick_chain_coop_kind<kIso>(a);
+    return a.classify == 1 ? pick_chain_coop_kind<kPre>(a) : pick_chain_coop_kind<kPreint>(a);
 }
 
 KernelFn pick(const RenderArgs &a) {
@@ -2678,7 +2938,7 @@ cudaError_t launch_raycast(const RenderArgs &a, cudaStream_t stream) {
         }
         return cudaGetLastError();
     }
-    const bool chained = a.mode == 1 || (a.mode == 0 && a.classify == 2);
+    const bool chained = a.mode == 1 || (a.mode == 0 && a.classify != 0);  // iso, pre-integrated, pre
     if (chained && a.work_counter && a.nviews == 1) {
         // persistent chained modes (queue counters zeroed by the frame's first kernel)
         KernelFn k = pick_chain(a);

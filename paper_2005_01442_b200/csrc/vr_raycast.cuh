@@ -68,6 +68,9 @@ struct RenderArgs {
     // interpolated values provably produce no hit / no opacity.  Pre-integrated:
     // a (ntbl+1)^2 prefix count of table cells with alpha > 0 (square queries).
     const int *tbl_nz;
+    // pre-classified: (first, last) int16 value whose alpha plane is non-zero;
+    // cells / mcells then hold raw footprint bounds instead of interpolant bounds
+    const int *pre_range;
 
     unsigned long long *work_counter;  // persistent kernel's ray queue head (zeroed per launch)
     unsigned long long *debug_times;   // VR_DEBUG_TIMES builds: per warp (start, end, smid, lanes used)
