@@ -204,7 +204,7 @@ int vr_grid_visibility(const vr_grid *grid, const double *lut_rgba, int32_t nbin
  * the LUT on every call.  Tables are DEVICE pointers:
  *   lut   (nlut,4) float64  -- always
  *   table (ntbl,ntbl,4) float64 pre-integrated (classify == PREINT), else NULL
- *   rgba  4 planar uint8 volumes (nz,ny,nx) preclassified (classify == PRE),
+ *   rgba  (nz,ny,nx,4) uint8 preclassified volume, RGBA interleaved per voxel (classify == PRE),
  *         as transfer.py:142-145 paints them (see vr_preclassify), else NULL.
  * Outputs as in vr_render_outputs (device).  Asynchronous on `stream`. */
 int vr_render(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const vr_render_params *prm,
@@ -236,8 +236,8 @@ int vr_render_to_host(vr_volume *vol, vr_grid *grid, const vr_camera *cam,
                       const double *table_host, uint8_t *pixels_host, double *premult_host,
                       double *depth_host, uint64_t *totals_host, void *stream);
 
-/* preclassify_volume (transfer.py:142-145) on the device: rgba_out holds 4
- * planar (nz,ny,nx) uint8 channels = rint(lut[bin(v)] * 255).  lut is a device
+/* preclassify_volume (transfer.py:142-145) on the device: rgba_out holds the
+ * (nz,ny,nx,4) uint8 array the reference returns, rint(lut[bin(v)] * 255).  lut is a device
  * pointer.  Asynchronous. */
 int vr_preclassify(const vr_volume *vol, const double *lut, int32_t nbins, double lut_lo,
                    double lut_hi, uint8_t *rgba_out, void *stream);

@@ -328,6 +328,15 @@ struct BrickVol {
     }
 };
 
+// The pre-classified volume interleaved as one uchar4 (r, g, b, a) per voxel
+// -- the (nz, ny, nx, 4) uint8 array transfer.py:142-145 returns -- so one
+// 4-byte load serves all four channels of a tap.
+struct LinearRGBA {
+    const uchar4 *p;
+    long long py, pz;
+    VR_D uchar4 at(int x, int y, int z) const { return __ldg(p + (long long)z * pz + (long long)y * py + x); }
+};
+
 // A block of the decomposition seen through the reference's atlas
 // addressing: local coordinates in [0, e) per axis, local voxel i at global
 // index origin + i (the atlas copy of a block holds exactly those voxels,
@@ -640,6 +649,76 @@ VR_D double cub_sample(const Block<TexVol> &b, double x, double y, double z) {
         pl[c] = ((wy0 * s[0] + wy1 * s[1]) + wy2 * s[2]) + wy3 * s[3];
     }
     return ((wz0 * pl[0] + wz1 * pl[1]) + wz2 * pl[2]) + wz3 * pl[3];
+}
+
+// _kernels.py:52-143 for the four pre-classified channels at once: the same
+// taps and the same sums as four separate single-channel samples (c = r, g,
+// b, a in out[0..3]), each channel's arithmetic unchanged.
+VR_D void tri_sample4(const Block<LinearRGBA> &b, double x, double y, double z, double out[4]) {
+    x = clampf(x, 0.0, b.ex - 1.0);
+    y = clampf(y, 0.0, b.ey - 1.0);
+    z = clampf(z, 0.0, b.ez - 1.0);
+    int i0 = clampi((int)x, 0, b.ex - 2);
+    int j0 = clampi((int)y, 0, b.ey - 2);
+    int k0 = clampi((int)z, 0, b.ez - 2);
+    double fx = x - (double)i0;
+    double fy = y - (double)j0;
+    double fz = z - (double)k0;
+    const int gx = b.ox + i0, gy = b.oy + j0, gz = b.oz + k0;
+    const uchar4 t000 = b.vol.at(gx, gy, gz), t100 = b.vol.at(gx + 1, gy, gz);
+    const uchar4 t010 = b.vol.at(gx, gy + 1, gz), t110 = b.vol.at(gx + 1, gy + 1, gz);
+    const uchar4 t001 = b.vol.at(gx, gy, gz + 1), t101 = b.vol.at(gx + 1, gy, gz + 1);
+    const uchar4 t011 = b.vol.at(gx, gy + 1, gz + 1), t111 = b.vol.at(gx + 1, gy + 1, gz + 1);
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) {
+        auto C = [ch](uchar4 q) { return (double)(ch == 0 ? q.x : ch == 1 ? q.y : ch == 2 ? q.z : q.w); };
+        const double c00 = C(t000) + (C(t100) - C(t000)) * fx;
+        const double c10 = C(t010) + (C(t110) - C(t010)) * fx;
+        const double c01 = C(t001) + (C(t101) - C(t001)) * fx;
+        const double c11 = C(t011) + (C(t111) - C(t011)) * fx;
+        const double c0 = c00 + (c10 - c00) * fy;
+        const double c1 = c01 + (c11 - c01) * fy;
+        out[ch] = c0 + (c1 - c0) * fz;
+    }
+}
+
+VR_D void cub_sample4(const Block<LinearRGBA> &b, double x, double y, double z, double out[4]) {
+    x = clampf(x, 0.0, b.ex - 1.0);
+    y = clampf(y, 0.0, b.ey - 1.0);
+    z = clampf(z, 0.0, b.ez - 1.0);
+    int i0 = clampi((int)x, 0, b.ex - 1);
+    int j0 = clampi((int)y, 0, b.ey - 1);
+    int k0 = clampi((int)z, 0, b.ez - 1);
+    double wx0, wx1, wx2, wx3, wy0, wy1, wy2, wy3, wz0, wz1, wz2, wz3;
+    cr_weights(x - (double)i0, wx0, wx1, wx2, wx3);
+    cr_weights(y - (double)j0, wy0, wy1, wy2, wy3);
+    cr_weights(z - (double)k0, wz0, wz1, wz2, wz3);
+    const int gx[4] = {b.ox + max(i0 - 1, 0), b.ox + i0, b.ox + min(i0 + 1, b.ex - 1), b.ox + min(i0 + 2, b.ex - 1)};
+    const int gy[4] = {b.oy + max(j0 - 1, 0), b.oy + j0, b.oy + min(j0 + 1, b.ey - 1), b.oy + min(j0 + 2, b.ey - 1)};
+    const int gz[4] = {b.oz + max(k0 - 1, 0), b.oz + k0, b.oz + min(k0 + 1, b.ez - 1), b.oz + min(k0 + 2, b.ez - 1)};
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};  // the z sum, built in the reference's order
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        double pl[4] = {0.0, 0.0, 0.0, 0.0};  // per channel, the plane sum over rows
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const uchar4 q0 = b.vol.at(gx[0], gy[r], gz[c]), q1 = b.vol.at(gx[1], gy[r], gz[c]);
+            const uchar4 q2 = b.vol.at(gx[2], gy[r], gz[c]), q3 = b.vol.at(gx[3], gy[r], gz[c]);
+            const double wy = r == 0 ? wy0 : r == 1 ? wy1 : r == 2 ? wy2 : wy3;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                auto C = [ch](uchar4 q) { return (double)(ch == 0 ? q.x : ch == 1 ? q.y : ch == 2 ? q.z : q.w); };
+                const double srow = ((wx0 * C(q0) + wx1 * C(q1)) + wx2 * C(q2)) + wx3 * C(q3);
+                // ((wy0 s0 + wy1 s1) + wy2 s2) + wy3 s3, accumulated row by row
+                pl[ch] = r == 0 ? wy * srow : pl[ch] + wy * srow;
+            }
+        }
+        const double wz = c == 0 ? wz0 : c == 1 ? wz1 : c == 2 ? wz2 : wz3;
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) acc[ch] = c == 0 ? wz * pl[ch] : acc[ch] + wz * pl[ch];
+    }
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch) out[ch] = acc[ch];
 }
 
 template <class V>

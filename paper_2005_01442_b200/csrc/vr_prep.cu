@@ -715,8 +715,10 @@ __global__ void __launch_bounds__(kBlock) preclassify_kernel(const int16_t *__re
                                                              double lo, double bw, uint8_t *rgba) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         int k = classified_bin((double)vol[i], lo, bw, nbins);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) rgba[c * n + i] = (uint8_t)rint(__ldg(lut + 4 * k + c) * 255.0);
+        // interleaved (nz, ny, nx, 4), the layout transfer.py:142-145 returns
+        reinterpret_cast<uchar4 *>(rgba)[i] =
+            make_uchar4((uint8_t)rint(__ldg(lut + 4 * k) * 255.0), (uint8_t)rint(__ldg(lut + 4 * k + 1) * 255.0),
+                        (uint8_t)rint(__ldg(lut + 4 * k + 2) * 255.0), (uint8_t)rint(__ldg(lut + 4 * k + 3) * 255.0));
     }
 }
 

@@ -221,15 +221,27 @@ VR_D void attr_grad(const RenderArgs &a, double x, double y, double z, int bi, i
     g[2] = divide(g[2], a.dsz);
 }
 
-// _attr_rgba (_kernels.py:256-276)
+// _attr_rgba (_kernels.py:256-276) for the four channels at once: out =
+// (r, g, b, a), each clamp(v / 255, 0, 1) exactly as the per-channel call
 template <bool CUBIC>
-VR_D double attr_rgba(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z, int ch) {
-    LinearU8 plane;
-    plane.p = a.rgba + (long long)ch * a.rgba_plane;
-    plane.py = a.L.py;
-    plane.pz = a.L.pz;
-    double v = sample_in<CUBIC>(plane, a, bi, bj, bk, x, y, z);
-    return clampf(v / 255.0, 0.0, 1.0);
+VR_D void attr_rgba4(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z, double out[4]) {
+    Block<LinearRGBA> b;
+    b.vol.p = reinterpret_cast<const uchar4 *>(a.rgba);
+    b.vol.py = a.L.py;
+    b.vol.pz = a.L.pz;
+    b.ox = block_origin(a.L, bi);
+    b.oy = block_origin(a.L, bj);
+    b.oz = block_origin(a.L, bk);
+    b.ex = block_extent(a.L, 0, bi);
+    b.ey = block_extent(a.L, 1, bj);
+    b.ez = block_extent(a.L, 2, bk);
+    const double lx = x - (double)b.ox, ly = y - (double)b.oy, lz = z - (double)b.oz;
+    if (CUBIC)
+        cub_sample4(b, lx, ly, lz, out);
+    else
+        tri_sample4(b, lx, ly, lz, out);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[c] = clampf(out[c] / 255.0, 0.0, 1.0);
 }
 
 // _kernels.py:190-192
@@ -677,11 +689,11 @@ VR_D RayResult march(const RenderArgs &a, const Ray &r, double t0, double t1, ui
                     }
                 }
                 ++n_eval;
-                double sa = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 3);
+                double c4[4];
+                attr_rgba4<CUBIC>(a, bi, bj, bk, x, y, z, c4);
+                double sa = c4[3];
                 if (sa > 0.0) {
-                    double sr = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 0);
-                    double sg = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 1);
-                    double sb = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 2);
+                    double sr = c4[0], sg = c4[1], sb = c4[2];
                     double ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
                     if (LIGHT) {
                         double g[3];
@@ -1680,7 +1692,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
 // the next ray at once.  After each evaluated sample, a run of samples whose
 // interpolant bound rules out any contribution (chain_transparent) is
 // counted as taken and leapt over, exactly as raycast_kernel does.
-enum ChainStage { kcNone = -1, kcSample = 0, kcPrevExact = 1, kcPrevGap = 2, kcBisect = 3, kcGrad = 11, kcRGB = 17 };
+enum ChainStage { kcNone = -1, kcSample = 0, kcPrevExact = 1, kcPrevGap = 2, kcBisect = 3, kcGrad = 11 };
 
 // A chained-mode ray handed to the cooperative kernel: everything needed to
 // continue it exactly where it stopped.
@@ -1963,48 +1975,44 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                 qj = owner(a, 1, py);
                 qk = owner(a, 2, pz);
             }
-            double v;
-            if (KIND == kPre && (R.stage == kcSample || R.stage >= kcRGB)) {
-                // a pre-classified plane (_attr_rgba, _kernels.py:256-276): alpha first, then r, g, b
-                v = attr_rgba<CUBIC>(a, R.bi, R.bj, R.bk, R.x, R.y, R.z, R.stage == kcSample ? 3 : R.stage - kcRGB);
+            double v = 0.0;
+            double c4[4] = {0.0, 0.0, 0.0, 0.0};
+            if (KIND == kPre && R.stage == kcSample) {
+                // the pre-classified channels (_attr_rgba, _kernels.py:256-276), all four at once
+                attr_rgba4<CUBIC>(a, R.bi, R.bj, R.bk, R.x, R.y, R.z, c4);
             } else {
                 v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
             }
             if (KIND == kPre && R.stage == kcSample) {
                 // _kernels.py:471-507
                 ++c_eval;
-                if (v > 0.0) {
-                    R.ca = 1.0 - vr_pow(1.0 - v, a.corr);  // ahat
-                    R.stage = kcRGB;
+                if (c4[3] > 0.0) {
+                    R.ca = 1.0 - vr_pow(1.0 - c4[3], a.corr);  // ahat
+                    R.cr = c4[0];
+                    R.cg = c4[1];
+                    R.cb = c4[2];
+                    if (LIGHT) {
+                        R.hx = R.x;
+                        R.hy = R.y;
+                        R.hz = R.z;
+                        R.hbi = R.bi;
+                        R.hbj = R.bj;
+                        R.hbk = R.bk;
+                        R.stage = kcGrad;
+                    } else {
+                        const double w = (1.0 - R.acc_a) * R.ca;
+                        R.acc_r += w * R.cr;
+                        R.acc_g += w * R.cg;
+                        R.acc_b += w * R.cb;
+                        R.acc_a += w;
+                        ++R.nvis;
+                        R.stage = kcNone;
+                        R.n += 1;
+                        if (R.acc_a >= a.term_alpha) finished = true;
+                    }
                 } else {
                     R.stage = kcNone;
                     R.n += 1;
-                }
-            } else if (KIND == kPre && R.stage >= kcRGB) {
-                const int ch = R.stage - kcRGB;
-                if (ch == 0) R.cr = v;
-                else if (ch == 1) R.cg = v;
-                else R.cb = v;
-                if (ch < 2) {
-                    R.stage += 1;
-                } else if (LIGHT) {
-                    R.hx = R.x;
-                    R.hy = R.y;
-                    R.hz = R.z;
-                    R.hbi = R.bi;
-                    R.hbj = R.bj;
-                    R.hbk = R.bk;
-                    R.stage = kcGrad;
-                } else {
-                    const double w = (1.0 - R.acc_a) * R.ca;
-                    R.acc_r += w * R.cr;
-                    R.acc_g += w * R.cg;
-                    R.acc_b += w * R.cb;
-                    R.acc_a += w;
-                    ++R.nvis;
-                    R.stage = kcNone;
-                    R.n += 1;
-                    if (R.acc_a >= a.term_alpha) finished = true;
                 }
             } else if (R.stage == kcPrevExact || R.stage == kcPrevGap) {
                 R.prev_s = v;
@@ -2416,8 +2424,9 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_COOP_MIN_BLOCKS *(kT
             }
             // alpha of every candidate, then the terminating sample by replaying
             // A += (1 - A) ahat in sample order
-            double sa = 0.0, ahat = 0.0;
-            if (cand) sa = attr_rgba<CUBIC>(a, bi, bj, bk, x, y, z, 3);
+            double sa = 0.0, ahat = 0.0, c4[4] = {0.0, 0.0, 0.0, 0.0};
+            if (cand) attr_rgba4<CUBIC>(a, bi, bj, bk, x, y, z, c4);
+            sa = c4[3];
             const bool contrib = cand && sa > 0.0;
             if (contrib) ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
             const unsigned cm = __ballot_sync(full, contrib);
@@ -2437,54 +2446,45 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_COOP_MIN_BLOCKS *(kT
             }
             const unsigned upto = stop >= 31 ? full : ((2u << stop) - 1u);
             const unsigned vis = cm & upto;
-            // r, g, b (and 6 gradient taps with lighting) of every visible sample,
-            // spread over the lanes, 32 per round
-            constexpr int J = LIGHT ? 9 : 3;
-            double jv[J];
-#pragma unroll
-            for (int g = 0; g < J; ++g) jv[g] = 0.0;
-            if (vis) {
-                const int njobs = J * __popc(vis);
+            // the 6 gradient taps of every visible sample (lighting), spread
+            // over the lanes, 32 per round
+            double sr = c4[0], sg = c4[1], sb = c4[2];
+            if (LIGHT && vis) {
+                double tp[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                const int njobs = 6 * __popc(vis);
                 const int rank = __popc(vis & lower);
                 for (int base = 0; base < njobs; base += 32) {
                     const int id = base + lane;
                     const bool act = id < njobs;
-                    const int k = id / J, g = id - J * k;
+                    const int k = id / 6, g = id - 6 * k;
                     const int src = act ? nth_bit(vis, k) : lane;
                     double px = __shfl_sync(full, x, src), py = __shfl_sync(full, y, src);
                     double pz = __shfl_sync(full, z, src);
                     int qi = __shfl_sync(full, bi, src), qj = __shfl_sync(full, bj, src);
                     int qk = __shfl_sync(full, bk, src);
-                    double v = 0.0;
-                    if (g < 3) {
-                        v = attr_rgba<CUBIC>(a, qi, qj, qk, px, py, pz, g);
-                    } else {
-                        const int q = g - 3;
-                        const double hh = (q & 1) ? -0.5 : 0.5;
-                        const int axis = q >> 1;
-                        px = axis == 0 ? px + hh : px;
-                        py = axis == 1 ? py + hh : py;
-                        pz = axis == 2 ? pz + hh : pz;
-                        const int o = owner(a, axis, axis == 0 ? px : axis == 1 ? py : pz);
-                        qi = axis == 0 ? o : qi;
-                        qj = axis == 1 ? o : qj;
-                        qk = axis == 2 ? o : qk;
-                        v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
-                    }
+                    const double hh = (g & 1) ? -0.5 : 0.5;
+                    const int axis = g >> 1;
+                    px = axis == 0 ? px + hh : px;
+                    py = axis == 1 ? py + hh : py;
+                    pz = axis == 2 ? pz + hh : pz;
+                    const int o = owner(a, axis, axis == 0 ? px : axis == 1 ? py : pz);
+                    qi = axis == 0 ? o : qi;
+                    qj = axis == 1 ? o : qj;
+                    qk = axis == 2 ? o : qk;
+                    const double v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
 #pragma unroll
-                    for (int gg = 0; gg < J; ++gg) {
-                        const int sidx = J * rank + gg - base;
+                    for (int gg = 0; gg < 6; ++gg) {
+                        const int sidx = 6 * rank + gg - base;
                         const double w = __shfl_sync(full, v, sidx & 31);
-                        if (sidx >= 0 && sidx < 32) jv[gg] = w;
+                        if (sidx >= 0 && sidx < 32) tp[gg] = w;
                     }
                 }
-            }
-            double sr = jv[0], sg = jv[1], sb = jv[2];
-            if (LIGHT && ((vis >> lane) & 1u)) {
-                const double gx = divide(jv[J - 6] - jv[J - 5], a.dsx), gy = divide(jv[J - 4] - jv[J - 3], a.dsy),
-                             gz = divide(jv[J - 2] - jv[J - 1], a.dsz);
-                const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
-                if (norm > 1e-12) shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                if ((vis >> lane) & 1u) {
+                    const double gx = divide(tp[0] - tp[1], a.dsx), gy = divide(tp[2] - tp[3], a.dsy),
+                                 gz = divide(tp[4] - tp[5], a.dsz);
+                    const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                    if (norm > 1e-12) shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -r.dx, -r.dy, -r.dz);
+                }
             }
             if (LIGHT && lane == 0) c_shaded += __popc(vis);
             {

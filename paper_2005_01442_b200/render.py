@@ -762,5 +762,4 @@ def _preclassify_device(volume: ScalarVolume, lut: ClassifiedLUT) -> np.ndarray:
     _lib.check(_lib.load().vr_preclassify(dvol.handle, _lib.ptr(lut_t), lut.bins, float(lut.domain[0]),
                                           float(lut.domain[1]), _lib.ptr(out),
                                           _lib.ptr_stream(torch.cuda.current_stream(dev))))
-    planes = out.cpu().numpy().reshape(4, nz, ny, nx)
-    return np.ascontiguousarray(np.moveaxis(planes, 0, -1))
+    return out.cpu().numpy().reshape(nz, ny, nx, 4)
