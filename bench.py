@@ -53,6 +53,15 @@ CONFIGS = {
     "c3stress": dict(dims=(512, 512, 512), size=1024, tf="grayscale", projection="pinhole",
                      settings=dict(interpolation="tricubic", lighting=False, early_termination_alpha=1.0),
                      desc="C3-stress: monolithic, grayscale, ET off, no lighting (every step sampled)"),
+    "c3pre": dict(dims=(512, 512, 512), size=1024, tf="bone", projection="pinhole",
+                  settings=dict(interpolation="tricubic", use_blocks=True, classification="pre"),
+                  desc="C3, pre-classified (_kernels.py:471-507)"),
+    "c3preint": dict(dims=(512, 512, 512), size=1024, tf="bone", projection="pinhole",
+                     settings=dict(interpolation="tricubic", use_blocks=True, classification="preintegrated"),
+                     desc="C3, pre-integrated (_kernels.py:538-581; the reference service's default)"),
+    "c3iso": dict(dims=(512, 512, 512), size=1024, tf="bone", projection="pinhole",
+                  settings=dict(interpolation="tricubic", use_blocks=True, mode="isosurface", isovalue=600.0),
+                  desc="C3, isosurface at 600 HU (_kernels.py:405-468)"),
     "c4": dict(dims=(512, 512, 2048), size=2048, tf="bone", projection="pinhole",
                settings=dict(interpolation="tricubic", use_blocks=True),
                desc="512x512x2048 -> 2048^2, tricubic, bricks 64/3"),
@@ -398,14 +407,17 @@ def run_reference(args):
 
 
 def launches_per_frame(settings):
-    """Kernels of ours in one frame (vr_render): TF visibility (4 on the block
-    path: value bits, block intervals + LUT range + frame zeroing, AABB fit,
-    boxes), the LUT range kernel on the monolithic post path, the per-lane
-    and cooperative ray casters (post-classified) or the one-thread-per-ray
-    kernel, and the blocks_visited count."""
+    """Kernels of ours in one single-view frame (vr_render): TF visibility (4
+    on the block path: value bits, block intervals + LUT range + frame zeroing,
+    AABB fit, boxes; the LUT range kernel on the monolithic post path), the
+    mode's table kernel (pre-integrated: the non-zero prefix count; pre: the
+    non-zero-alpha value range), the per-lane and cooperative ray casters
+    (every mode, persistent), and the blocks_visited count."""
     post = settings.mode == "dvr" and settings.classification == "post"
     n = 4 if settings.use_blocks else (1 if post else 0)
-    n += 2 if post else 1
+    if settings.mode == "dvr" and settings.classification in ("pre", "preintegrated"):
+        n += 1
+    n += 2  # per-lane + cooperative ray casters
     return n + 1
 
 

@@ -288,6 +288,26 @@ def _lut_for(tf: TransferFunction):
     return lut
 
 
+_preint_cache: dict = {}
+
+
+def _preint_for(lut, step, ref_step):
+    """build_preintegrated(lut, step, ref_step).rgba, memoised per LUT object
+    and step pair (the LUT is immutable, _lut_for), in page-locked memory: a
+    frame loop with one TF pays the 256^2 x 64-substep table once."""
+    key = (id(lut), float(step), float(ref_step))
+    hit = _preint_cache.get(key)
+    if hit is not None and hit[0]() is lut:
+        return hit[1]
+    rgba = build_preintegrated(lut, step, ref_step).rgba
+    buf = _pinned_empty(rgba.shape, np.float64)
+    buf[...] = rgba
+    if len(_preint_cache) > 16:
+        _preint_cache.clear()
+    _preint_cache[key] = (weakref.ref(lut), buf)
+    return buf
+
+
 _lut_pinned: dict = {}
 
 
@@ -331,7 +351,7 @@ def _resolve(volume_spacing, value_range, tf: TransferFunction, settings: Render
         classify = _lib.CLS_POST
     table = None
     if classify == _lib.CLS_PREINT:
-        table = np.ascontiguousarray(build_preintegrated(lut, step, ref_step).rgba)
+        table = _preint_for(lut, step, ref_step)
     p = _lib.RenderParams()
     p.step = float(step)
     p.ref_step = float(ref_step)
@@ -497,7 +517,7 @@ def render(target, camera, tf: TransferFunction, settings: RenderSettings = Rend
     pixels = _pinned_empty((cam.tile_h, cam.tile_w, 4), np.uint8)
     premult = np.empty((npix, 4)) if return_premultiplied else None
     iso = settings.mode == "isosurface"
-    depth = np.empty(npix) if iso else None
+    depth = _pinned_empty((npix,), np.float64) if iso else None
     totals = np.zeros(8, dtype=np.uint64)
     lut = _lut_host_copy(res.lut)
     _lib.check(_lib.load().vr_render_to_host(

@@ -1,14 +1,25 @@
-# Round-end capture: tests, smoke, bench lines for every config + the reference arm,
-# launch list and ncu --set full of the ray-cast kernels and the AABB fit at C3.
-set -o pipefail
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-: > gpurun_out/final.jsonl
-timeout 600 python bench.py 2>gpurun_out/final_err.log | tail -1 >> gpurun_out/final.jsonl; echo c3=$?
-for c in c1 c2 c3soft c3stress c4 c5; do
-  timeout 600 python bench.py --config $c --steps 20 2>>gpurun_out/final_err.log | tail -1 >> gpurun_out/final.jsonl; echo $c=$?
+# Round-end measurement: tests, smoke, every bench line, the reference arm.
+cd "$GRAFT_REPO_ROOT"
+TAG=${1:-r02}
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_$TAG.log
+rm -f gpurun_out/bench_$TAG.jsonl
+timeout 900 python bench.py >> gpurun_out/bench_$TAG.jsonl 2>> gpurun_out/bench_$TAG.err; echo "default rc=$?"
+for c in c1 c2 c3soft c3stress c3pre c3preint c3iso c4 c5 k4; do
+  st=20; [ "$c" = c5 ] && st=3; [ "$c" = c3stress ] && st=10
+  timeout 900 python bench.py --config $c --steps $st --warmup 3 >> gpurun_out/bench_$TAG.jsonl 2>> gpurun_out/bench_$TAG.err; echo "$c rc=$?"
 done
-timeout 600 python bench.py --impl reference --steps 2 --warmup 1 2>>gpurun_out/final_err.log | tail -1 >> gpurun_out/final.jsonl; echo ref=$?
-bash tools/gpu_profile.sh c3
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:aabb_kernel -s 3 -c 1 -f \
-  -o gpurun_out/prof_c3_aabb_kernel python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_full_c3_aabb.log 2>&1; echo aabb=$?
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 >> gpurun_out/bench_$TAG.jsonl 2>> gpurun_out/bench_$TAG.err; echo "ref rc=$?"
+python - "$TAG" <<'PY'
+import json, sys
+for l in open(f"gpurun_out/bench_{sys.argv[1]}.jsonl"):
+    try:
+        d = json.loads(l)
+    except Exception:
+        continue
+    e = d.get("e2e") or {}
+    cpu = d.get("cpu_baseline") or {}
+    r = d.get("roofline") or {}
+    print(d.get("impl", "ours"), d["config"]["workload"], round(d["value"], 2), "e2e", round(e.get("value", 0) or 0, 1),
+          "frac", round(r.get("frac", 0) or 0, 3), "cpu", round(cpu.get("value", 0) or 0, 3), (d.get("clocks") or {}).get("sm_mhz"))
+PY
