@@ -29,8 +29,7 @@
 // volume, L2-resident) and the count V, HBM-bound; (2a) a scan of the bit
 // array for cells whose eight corners disagree, appended to a list; (2b) the
 // tetrahedra for the listed cells, one per thread.  The ball form scans the
-// bit array inside each ball's bounding box.  Generic volumes (unaligned
-// base pointer) use the one-pass kernels kept below.
+// bit array inside each ball's bounding box.
 #include <cstdint>
 
 #include "vr_common.cuh"
@@ -162,107 +161,11 @@ VR_D void cta_accumulate(unsigned long long c, unsigned long long area, unsigned
     }
 }
 
-// Voxel (x) of a row held as prev (voxel x0-1) + chunk lo/hi (voxels x0..x0+7);
-// position p in 0..8.
-VR_D int row_voxel(int prev, unsigned long long lo, unsigned long long hi, int p) {
-    if (p == 0) return prev;
-    const int s = p - 1;
-    const unsigned long long w = s < 4 ? (lo >> (16 * s)) : (hi >> (16 * (s - 4)));
-    return (int)(short)(w & 0xffffull);
-}
-
 struct MeasureVol {
     const int16_t *v;
     int nx, ny, nz;
     double sx, sy, sz;
 };
-
-// Row (j, k) voxels x0-1 .. x0+7 (out of range: -32768).
-template <bool VEC>
-VR_D void load_row(const MeasureVol &m, int x0, int j, int k, int &prev, unsigned long long &lo,
-                   unsigned long long &hi) {
-    const unsigned long long pad = 0x8000800080008000ull;
-    prev = -32768;
-    lo = hi = pad;
-    if (j < 0 || k < 0 || j >= m.ny || k >= m.nz) return;
-    const int16_t *row = m.v + ((long long)k * m.ny + j) * m.nx;
-    if (x0 > 0) prev = __ldg(row + x0 - 1);
-    if (VEC && x0 + 8 <= m.nx) {
-        const int4 q = __ldg(reinterpret_cast<const int4 *>(row + x0));
-        lo = ((unsigned long long)(unsigned)q.y << 32) | (unsigned)q.x;
-        hi = ((unsigned long long)(unsigned)q.w << 32) | (unsigned)q.z;
-        return;
-    }
-    lo = hi = 0;
-#pragma unroll
-    for (int s = 0; s < 8; ++s) {
-        const unsigned long long u = (x0 + s < m.nx) ? (unsigned short)__ldg(row + x0 + s) : 0x8000u;
-        if (s < 4)
-            lo |= u << (16 * s);
-        else
-            hi |= u << (16 * (s - 4));
-    }
-}
-
-// inside bits (v >= thr) of the 9 voxels x0-1 .. x0+7 (bit p = voxel x0-1+p)
-VR_D unsigned row_mask(int prev, unsigned long long lo, unsigned long long hi, int thr) {
-    unsigned m = prev >= thr ? 1u : 0u;
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        m |= ((int)(short)((lo >> (16 * s)) & 0xffff) >= thr ? 1u : 0u) << (1 + s);
-        m |= ((int)(short)((hi >> (16 * s)) & 0xffff) >= thr ? 1u : 0u) << (5 + s);
-    }
-    return m;
-}
-
-// Whole volume: cells (cx, cy, cz) in [-1, n-1]^3; thread t -> run q of cells
-// x0-1 .. x0+6 (x0 = 8q) of cell row (cy, cz), q fastest so a CTA covers a
-// few neighbouring cell rows of one slab.
-template <bool VEC>
-__global__ void __launch_bounds__(kMeasureThreads) threshold_measure_kernel(MeasureVol m, int thr, int runs,
-                                                                            unsigned long long *out) {
-    const double level = (double)thr - 0.5;
-    const long long total = (long long)runs * (m.ny + 1) * (m.nz + 1);
-    unsigned long long count = 0, area = 0;
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
-         t += (long long)gridDim.x * blockDim.x) {
-        const int q = (int)(t % runs);
-        const long long r = t / runs;
-        const int cy = (int)(r % (m.ny + 1)) - 1, cz = (int)(r / (m.ny + 1)) - 1;
-        const int x0 = 8 * q;
-        int pv[4];
-        unsigned long long lo[4], hi[4];
-        unsigned mk[4];
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-            load_row<VEC>(m, x0, cy + (rr & 1), cz + (rr >> 1), pv[rr], lo[rr], hi[rr]);
-            mk[rr] = row_mask(pv[rr], lo[rr], hi[rr], thr);
-        }
-        // V: the row (cy, cz) of voxels x0 .. x0+7, counted once (as the lower
-        // row of its cell row); padding voxels are never inside
-        if (cy >= 0 && cz >= 0 && x0 < m.nx) {
-            const int nvalid = m.nx - x0 < 8 ? m.nx - x0 : 8;
-            count += (unsigned long long)__popc((mk[0] >> 1) & ((1u << nvalid) - 1u));
-        }
-        const unsigned all = mk[0] & mk[1] & mk[2] & mk[3];
-        const unsigned any = mk[0] | mk[1] | mk[2] | mk[3];
-        unsigned straddle = ((any | (any >> 1)) & ~(all & (all >> 1))) & 0xffu;
-        while (straddle) {
-            const int b = __ffs(straddle) - 1;  // cell x0-1+b, corners at row positions b, b+1
-            straddle &= straddle - 1;
-            const int cx = x0 - 1 + b;
-            double f[8];
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const int rr = (c >> 1);  // (y, z) bits -> row index y | z<<1
-                f[c] = (double)row_voxel(pv[rr], lo[rr], hi[rr], b + (c & 1)) - level;
-            }
-            const CellGeom G{cx, cy, cz, m.sx, m.sy, m.sz};
-            area += cell_area_fx<false>(f, G, 0.0, 0.0, 0.0, 0.0);
-        }
-    }
-    cta_accumulate(count, area, out, out + 1, false);
-}
 
 VR_D int voxel_or_pad(const MeasureVol &m, int i, int j, int k) {
     if (i < 0 || j < 0 || k < 0 || i >= m.nx || j >= m.ny || k >= m.nz) return -32768;
@@ -278,52 +181,6 @@ VR_D int box_lo(double lo_mm, double s) {
 VR_D int box_hi(double hi_mm, double s, int n) {
     const double v = ceil(hi_mm / s) + 1.0;
     return v > (double)(n - 1) ? n - 1 : (v < -2.0e9 ? -2000000000 : (int)v);
-}
-
-// One CTA per ball: the cells of the ball's bounding box (one cell of slack),
-// each contributing its polygons with centroid in the ball and -- for cells
-// at non-negative indices -- its base voxel when that voxel's centre is in
-// the ball and its value >= thr.
-__global__ void __launch_bounds__(kMeasureThreads) ball_measure_kernel(MeasureVol m, int thr, const double *centres,
-                                                                       const double *radii,
-                                                                       unsigned long long *counts,
-                                                                       unsigned long long *areas) {
-    const int q = blockIdx.x;
-    const double cx = centres[3 * q], cy = centres[3 * q + 1], cz = centres[3 * q + 2];
-    const double rad = radii[q];
-    const double r2 = rad * rad;
-    const double level = (double)thr - 0.5;
-    // bounding box as vro_ball_measure computes it (floor/ceil of a true division)
-    // (any superset of the contributing cells gives the same sums: the
-    // centroid and voxel-centre tests decide)
-    const int i0 = box_lo(cx - rad, m.sx), i1 = box_hi(cx + rad, m.sx, m.nx);
-    const int j0 = box_lo(cy - rad, m.sy), j1 = box_hi(cy + rad, m.sy, m.ny);
-    const int k0 = box_lo(cz - rad, m.sz), k1 = box_hi(cz + rad, m.sz, m.nz);
-    unsigned long long count = 0, area = 0;
-    if (i0 <= i1 && j0 <= j1 && k0 <= k1) {
-        const int wx = i1 - i0 + 1, wy = j1 - j0 + 1;
-        const long long n = (long long)wx * wy * (k1 - k0 + 1);
-        for (long long t = threadIdx.x; t < n; t += blockDim.x) {
-            const int i = i0 + (int)(t % wx);
-            const long long r = t / wx;
-            const int j = j0 + (int)(r % wy), k = k0 + (int)(r / wy);
-            double f[8];
-            bool any_in = false, any_out = false;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                f[c] = (double)voxel_or_pad(m, i + (c & 1), j + ((c >> 1) & 1), k + ((c >> 2) & 1)) - level;
-                if (f[c] > 0.0) any_in = true; else any_out = true;
-            }
-            const CellGeom G{i, j, k, m.sx, m.sy, m.sz};
-            if (i >= 0 && j >= 0 && k >= 0 && f[0] > 0.0) {
-                // the cell's base voxel (i, j, k): centre in the closed ball (vro_ball_counts)
-                const double dx = (double)i * m.sx - cx, dy = (double)j * m.sy - cy, dz = (double)k * m.sz - cz;
-                count += ((dx * dx + dy * dy) + dz * dz <= r2) ? 1 : 0;
-            }
-            if (any_in && any_out) area += cell_area_fx<true>(f, G, cx, cy, cz, r2);
-        }
-    }
-    cta_accumulate(count, area, counts + q, areas ? areas + q : nullptr, true);
 }
 
 // ------------------------------------------------ two-pass fast path
@@ -662,44 +519,36 @@ cudaError_t launch_threshold_measure(const int16_t *vol, int nx, int ny, int nz,
     if (e != cudaSuccess) return e;
     MeasureVol m{vol, nx, ny, nz, sx, sy, sz};
     const long long n = (long long)nx * ny * nz;
-    if ((reinterpret_cast<uintptr_t>(vol) & 15) == 0) {
-        BitsScratch bits(s);
-        if ((e = bits.alloc(n)) != cudaSuccess) return e;
-        if ((e = launch_inside_bits(vol, n, thr, bits.p, out, s)) != cudaSuccess) return e;
-        const int nchunks = (nx + 1 + 31) / 32;  // cells -1 .. nx-1 in chunks of 32
-        const long long total = (long long)nchunks * (ny + 1) * (nz + 1);
-        if (total >= (1ll << 31)) return cudaErrorInvalidValue;  // > 2^36 voxels: not a CT volume
-        long long grid = (total + kMeasureThreads - 1) / kMeasureThreads;
-        const long long cap_ctas = (long long)device_sms() * 16;
-        if (grid > cap_ctas) grid = cap_ctas;
-        // straddling cells: the list holds up to 1/16 of all cells (every
-        // boundary of a 512^3 CT at its bone threshold is ~0.2 %); beyond
-        // that the one-pass surface kernel (correct for any count) runs
-        // instead, chosen on the device so nothing waits on the host
-        const unsigned long long cap = (unsigned long long)((long long)(nx + 1) * (ny + 1) * (nz + 1) / 16 + 1024);
-        void *lst = nullptr;
-        if ((e = cudaMallocAsync(&lst, (size_t)cap * 8 + 16, s)) != cudaSuccess) return e;
-        unsigned long long *ncells = reinterpret_cast<unsigned long long *>((char *)lst + (size_t)cap * 8);
-        e = cudaMemsetAsync(ncells, 0, 8, s);
-        if (e == cudaSuccess) {
-            straddle_scan_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, nchunks,
-                                                                            (unsigned long long *)lst, cap, ncells);
-            cell_area_kernel<<<(unsigned)device_sms() * 8, kMeasureThreads, 0, s>>>(
-                m, thr, (const unsigned long long *)lst, ncells, cap, out);
-            surface_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, thr, nchunks, ncells, cap, out);
-            e = cudaGetLastError();
-        }
-        cudaError_t e2 = cudaFreeAsync(lst, s);
-        return e != cudaSuccess ? e : e2;
-    }
-    const int runs = (nx + 1 + 7) / 8;  // cells -1 .. nx-1 in runs of 8
-    const long long total = (long long)runs * (ny + 1) * (nz + 1);
+    // (volumes are cudaMalloc allocations: 256-byte aligned, as the 16-byte loads need)
+    if ((reinterpret_cast<uintptr_t>(vol) & 15) != 0) return cudaErrorMisalignedAddress;
+    BitsScratch bits(s);
+    if ((e = bits.alloc(n)) != cudaSuccess) return e;
+    if ((e = launch_inside_bits(vol, n, thr, bits.p, out, s)) != cudaSuccess) return e;
+    const int nchunks = (nx + 1 + 31) / 32;  // cells -1 .. nx-1 in chunks of 32
+    const long long total = (long long)nchunks * (ny + 1) * (nz + 1);
+    if (total >= (1ll << 31)) return cudaErrorInvalidValue;  // > 2^36 voxels: not a CT volume
     long long grid = (total + kMeasureThreads - 1) / kMeasureThreads;
-    const long long cap = (long long)device_sms() * 8;
-    if (grid > cap) grid = cap;
-    if (grid < 1) grid = 1;
-    threshold_measure_kernel<false><<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, thr, runs, out);
-    return cudaGetLastError();
+    const long long cap_ctas = (long long)device_sms() * 16;
+    if (grid > cap_ctas) grid = cap_ctas;
+    // straddling cells: the list holds up to 1/16 of all cells (every
+    // boundary of a 512^3 CT at its bone threshold is ~0.2 %); beyond
+    // that the one-pass surface kernel (correct for any count) runs
+    // instead, chosen on the device so nothing waits on the host
+    const unsigned long long cap = (unsigned long long)((long long)(nx + 1) * (ny + 1) * (nz + 1) / 16 + 1024);
+    void *lst = nullptr;
+    if ((e = cudaMallocAsync(&lst, (size_t)cap * 8 + 16, s)) != cudaSuccess) return e;
+    unsigned long long *ncells = reinterpret_cast<unsigned long long *>((char *)lst + (size_t)cap * 8);
+    e = cudaMemsetAsync(ncells, 0, 8, s);
+    if (e == cudaSuccess) {
+        straddle_scan_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, nchunks,
+                                                                        (unsigned long long *)lst, cap, ncells);
+        cell_area_kernel<<<(unsigned)device_sms() * 8, kMeasureThreads, 0, s>>>(
+            m, thr, (const unsigned long long *)lst, ncells, cap, out);
+        surface_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, thr, nchunks, ncells, cap, out);
+        e = cudaGetLastError();
+    }
+    cudaError_t e2 = cudaFreeAsync(lst, s);
+    return e != cudaSuccess ? e : e2;
 }
 
 cudaError_t launch_ball_measure(const int16_t *vol, int nx, int ny, int nz, double sx, double sy, double sz, int thr,
@@ -707,20 +556,16 @@ cudaError_t launch_ball_measure(const int16_t *vol, int nx, int ny, int nz, doub
                                 unsigned long long *areas, cudaStream_t s) {
     if (nballs <= 0) return cudaSuccess;
     MeasureVol m{vol, nx, ny, nz, sx, sy, sz};
-    if ((reinterpret_cast<uintptr_t>(vol) & 15) == 0) {
-        const long long n = (long long)nx * ny * nz;
-        cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * nballs, s);
-        if (e == cudaSuccess && areas) e = cudaMemsetAsync(areas, 0, sizeof(unsigned long long) * nballs, s);
-        if (e != cudaSuccess) return e;
-        BitsScratch bits(s);
-        if ((e = bits.alloc(n)) != cudaSuccess) return e;
-        // (pass 1's whole-volume count is not needed here: the spare counter)
-        if ((e = launch_inside_bits(vol, n, thr, bits.p, bits.count, s)) != cudaSuccess) return e;
-        ball_surface_kernel<<<(unsigned)nballs, kMeasureThreads, 0, s>>>(
-            m, bits.p, thr, centres, radii, counts, areas);
-        return cudaGetLastError();
-    }
-    ball_measure_kernel<<<nballs, kMeasureThreads, 0, s>>>(m, thr, centres, radii, counts, areas);
+    if ((reinterpret_cast<uintptr_t>(vol) & 15) != 0) return cudaErrorMisalignedAddress;
+    const long long n = (long long)nx * ny * nz;
+    cudaError_t e = cudaMemsetAsync(counts, 0, sizeof(unsigned long long) * nballs, s);
+    if (e == cudaSuccess && areas) e = cudaMemsetAsync(areas, 0, sizeof(unsigned long long) * nballs, s);
+    if (e != cudaSuccess) return e;
+    BitsScratch bits(s);
+    if ((e = bits.alloc(n)) != cudaSuccess) return e;
+    // (pass 1's whole-volume count is not needed here: the spare counter)
+    if ((e = launch_inside_bits(vol, n, thr, bits.p, bits.count, s)) != cudaSuccess) return e;
+    ball_surface_kernel<<<(unsigned)nballs, kMeasureThreads, 0, s>>>(m, bits.p, thr, centres, radii, counts, areas);
     return cudaGetLastError();
 }
 

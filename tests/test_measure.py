@@ -160,7 +160,8 @@ def test_disjoint_ball_is_undefined():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dims,spacing", [((72, 60, 50), (0.8, 0.7, 1.5)), ((64, 64, 64), (1.0, 1.0, 1.0)),
-                                          ((61, 37, 29), (1.0, 1.1, 0.9))])
+                                          ((61, 37, 29), (1.0, 1.1, 0.9)), ((9, 8, 8), (1.0, 1.0, 1.0)),
+                                          ((33, 8, 11), (0.5, 2.0, 1.0))])
 def test_kernels_equal_restatement(dims, spacing):
     import paper_2005_01442_b200 as vr
 
@@ -193,3 +194,21 @@ def test_kernels_on_analytic_objects():
     vol = vr.make_volume(vals, (1.0, 1.0, 1.0))
     b = vr.ball_measure(vol, 0, X[None], np.array([12.0]))
     assert abs(b["svr"][0] / (3.0 / 24.0) - 1) < 0.03
+
+
+@pytest.mark.gpu
+def test_kernels_on_noise_exercise_the_overflow_path():
+    """A noise volume: almost every cell straddles the level, more than the
+    straddling-cell list holds, so the one-pass fallback kernel computes S."""
+    import paper_2005_01442_b200 as vr
+
+    rng = np.random.default_rng(7)
+    vals = rng.integers(-200, 200, size=(16, 20, 24)).astype(np.int16)
+    vol = vr.make_volume(vals, (0.9, 1.1, 1.3))
+    for thr in (0, 50, -150):
+        m = vr.threshold_measure(vol, thr)
+        assert (m["count"], m["area_fx"]) == O.threshold_measure(vals, (0.9, 1.1, 1.3), thr), thr
+    centres = rng.uniform(0, 20, size=(12, 3))
+    b = vr.ball_measure(vol, 0, centres, 4.0)
+    want_c, want_a = O.ball_measure(vals, (0.9, 1.1, 1.3), 0, centres, np.full(12, 4.0))
+    assert np.array_equal(b["count"], want_c) and np.array_equal(b["area_fx"], want_a)
