@@ -40,6 +40,7 @@ namespace {
 
 constexpr int kMeasureThreads = 256;
 constexpr double kAreaScale = 16777216.0;  // 2^24
+constexpr int kBallSplit = 8;  // CTAs per probe ball
 
 // Cell corner c (bit 0: x, 1: y, 2: z) of the cell with base voxel (cx, cy,
 // cz), in mm (voxel centres at index * spacing).
@@ -348,43 +349,66 @@ VR_D unsigned long long chunk_straddle(const MeasureVol &m, const unsigned *bits
 // resident bit array.  Cells are packed as (cx + 1) | (cy + 1) << 21 |
 // (cz + 1) << 42.  Returns the list length in *ncells (capped at cap; the
 // overflow count is what tells the host to fall back, see the launcher).
+#ifndef VR_SCAN_SLABS
+#define VR_SCAN_SLABS 4  // measured at 512^3: 2: 160 us, 4: 156, 8: 158, 16: 173, 32: 190 (whole measure)
+#endif
+constexpr int kScanSlabs = VR_SCAN_SLABS;  // cell slabs per thread of the straddle scan (the z window slides)
+
 __global__ void __launch_bounds__(kMeasureThreads) straddle_scan_kernel(MeasureVol m, const unsigned *__restrict__ bits,
                                                                         int nchunks, unsigned long long *list,
                                                                         unsigned long long cap,
                                                                         unsigned long long *ncells) {
-    // (32-bit index arithmetic: the item count is checked < 2^31 by the launcher)
-    const int total = nchunks * (m.ny + 1) * (m.nz + 1);
+    // thread = (32-cell chunk, cell row, run of kScanSlabs cell slabs): the
+    // upper voxel rows of one slab are the lower rows of the next, so each
+    // step fetches two rows instead of four.  (32-bit index arithmetic: the
+    // launcher checks the counts.)
+    const int nseg = (m.nz + 1 + kScanSlabs - 1) / kScanSlabs;
+    const int total = nchunks * (m.ny + 1) * nseg;
     const int lane = threadIdx.x & 31;
     for (int t0 = (int)((blockIdx.x * blockDim.x + threadIdx.x) & ~31u); t0 < total; t0 += gridDim.x * blockDim.x) {
         const int t = t0 + lane;
-        unsigned st = 0;
-        int x0 = 0, cy = 0, cz = 0;
-        if (t < total) {
-            const int c = t % nchunks;
-            const int r = t / nchunks;
-            cy = r % (m.ny + 1) - 1;
-            cz = r / (m.ny + 1) - 1;
-            x0 = 32 * c - 1;
-            st = (unsigned)chunk_straddle(m, bits, x0, cy, cz);
-        }
-        const int cnt = __popc(st);
-        int incl = cnt;
+        const bool valid = t < total;
+        const int tc = valid ? t : 0;
+        const int c = tc % nchunks;
+        const int r = tc / nchunks;
+        const int cy = r % (m.ny + 1) - 1;
+        const int cz0 = (r / (m.ny + 1)) * kScanSlabs - 1;
+        const int x0 = 32 * c - 1;
+        const int ncl = m.nx - x0;  // cells x0 .. nx-1 exist (cx <= nx-1)
+        const unsigned long long cmask = ncl >= 32 ? 0xffffffffull : (ncl <= 0 ? 0ull : ((1ull << ncl) - 1ull));
+        unsigned long long lo0 = row_bits33(m, bits, x0, cy, cz0), lo1 = row_bits33(m, bits, x0, cy + 1, cz0);
+        const unsigned long long yz0 = ((unsigned long long)(cy + 1) << 21);
+        for (int k = 0; k < kScanSlabs; ++k) {
+            const int cz = cz0 + k;
+            const bool live = valid && cz < m.nz;  // cell slabs -1 .. nz-1
+            unsigned long long hi0 = 0, hi1 = 0;
+            if (live) {
+                hi0 = row_bits33(m, bits, x0, cy, cz + 1);
+                hi1 = row_bits33(m, bits, x0, cy + 1, cz + 1);
+            }
+            const unsigned long long all = lo0 & lo1 & hi0 & hi1, any = lo0 | lo1 | hi0 | hi1;
+            unsigned st = live ? (unsigned)(((any | (any >> 1)) & ~(all & (all >> 1))) & cmask) : 0u;
+            lo0 = hi0;
+            lo1 = hi1;
+            if (!__any_sync(0xffffffffu, st != 0u)) continue;  // (most steps: no straddling cell)
+            const int cnt = __popc(st);
+            int incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
-        if (wtotal == 0) continue;
-        unsigned long long base = 0;
-        if (lane == 31) base = atomicAdd(ncells, (unsigned long long)wtotal);
-        base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - cnt);
-        const unsigned long long yz = ((unsigned long long)(cy + 1) << 21) | ((unsigned long long)(cz + 1) << 42);
-        while (st) {
-            const int b = __ffs(st) - 1;
-            st &= st - 1;
-            if (base < cap) list[base] = (unsigned long long)(x0 + b + 1) | yz;
-            ++base;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int v = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += v;
+            }
+            const int wtotal = __shfl_sync(0xffffffffu, incl, 31);
+            unsigned long long base = 0;
+            if (lane == 31) base = atomicAdd(ncells, (unsigned long long)wtotal);
+            base = __shfl_sync(0xffffffffu, base, 31) + (unsigned long long)(incl - cnt);
+            const unsigned long long yz = yz0 | ((unsigned long long)(cz + 1) << 42);
+            while (st) {
+                const int b = __ffs(st) - 1;
+                st &= st - 1;
+                if (base < cap) list[base] = (unsigned long long)(x0 + b + 1) | yz;
+                ++base;
+            }
         }
     }
 }
@@ -459,8 +483,10 @@ __global__ void __launch_bounds__(kMeasureThreads) ball_surface_kernel(MeasureVo
     if (i0 <= i1 && j0 <= j1 && k0 <= k1) {
         const int nc = (i1 - i0) / 32 + 1, nj = j1 - j0 + 1;
         const int items = nc * nj * (k1 - k0 + 1);  // (32-cell chunk, cell row, cell slab)
-        // warp-uniform trip counts: tetrahedra shared out warp-wide
-        for (int t0 = threadIdx.x & ~31; t0 < items; t0 += blockDim.x) {
+        // warp-uniform trip counts: tetrahedra shared out warp-wide; the
+        // ball's items are split over gridDim.y CTAs (counts added atomically)
+        const int stride = (int)(blockDim.x * gridDim.y);
+        for (int t0 = (int)(blockIdx.y * blockDim.x + (threadIdx.x & ~31u)); t0 < items; t0 += stride) {
             const int t = t0 + (threadIdx.x & 31);
             const bool valid = t < items;
             const int tc = valid ? t : 0;
@@ -530,6 +556,9 @@ cudaError_t launch_threshold_measure(const int16_t *vol, int nx, int ny, int nz,
     long long grid = (total + kMeasureThreads - 1) / kMeasureThreads;
     const long long cap_ctas = (long long)device_sms() * 16;
     if (grid > cap_ctas) grid = cap_ctas;
+    const long long scan_items = (long long)nchunks * (ny + 1) * ((nz + 1 + kScanSlabs - 1) / kScanSlabs);
+    long long scan_grid = (scan_items + kMeasureThreads - 1) / kMeasureThreads;
+    if (scan_grid > cap_ctas) scan_grid = cap_ctas;
     // straddling cells: the list holds up to 1/16 of all cells (every
     // boundary of a 512^3 CT at its bone threshold is ~0.2 %); beyond
     // that the one-pass surface kernel (correct for any count) runs
@@ -540,7 +569,7 @@ cudaError_t launch_threshold_measure(const int16_t *vol, int nx, int ny, int nz,
     unsigned long long *ncells = reinterpret_cast<unsigned long long *>((char *)lst + (size_t)cap * 8);
     e = cudaMemsetAsync(ncells, 0, 8, s);
     if (e == cudaSuccess) {
-        straddle_scan_kernel<<<(unsigned)grid, kMeasureThreads, 0, s>>>(m, bits.p, nchunks,
+        straddle_scan_kernel<<<(unsigned)scan_grid, kMeasureThreads, 0, s>>>(m, bits.p, nchunks,
                                                                         (unsigned long long *)lst, cap, ncells);
         cell_area_kernel<<<(unsigned)device_sms() * 8, kMeasureThreads, 0, s>>>(
             m, thr, (const unsigned long long *)lst, ncells, cap, out);
@@ -565,7 +594,9 @@ cudaError_t launch_ball_measure(const int16_t *vol, int nx, int ny, int nz, doub
     if ((e = bits.alloc(n)) != cudaSuccess) return e;
     // (pass 1's whole-volume count is not needed here: the spare counter)
     if ((e = launch_inside_bits(vol, n, thr, bits.p, bits.count, s)) != cudaSuccess) return e;
-    ball_surface_kernel<<<(unsigned)nballs, kMeasureThreads, 0, s>>>(m, bits.p, thr, centres, radii, counts, areas);
+    // several CTAs per ball: one per ball left most SMs idle (ncu: 17 % warps active)
+    ball_surface_kernel<<<dim3((unsigned)nballs, kBallSplit), kMeasureThreads, 0, s>>>(m, bits.p, thr, centres, radii,
+                                                                                      counts, areas);
     return cudaGetLastError();
 }
 
