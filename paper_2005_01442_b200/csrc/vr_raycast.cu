@@ -174,11 +174,23 @@ VR_D double sample_in(const V &vol, const RenderArgs &a, int bi, int bj, int bk,
 
 // the ray casters' interpolant: brick windows through L1 (default) or the
 // x-quad texture (VR_SAMPLER_TEX A/B builds)
-template <bool CUBIC>
+// (FUNNEL: the brick sampler's funnel tap extraction, for the unlit kernels)
+template <bool CUBIC, bool FUNNEL = false>
 VR_D double vol_sample(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z) {
 #if VR_SAMPLER_TEX
     return sample_in<CUBIC>(a.tv, a, bi, bj, bk, x, y, z);
 #else
+    if (CUBIC && FUNNEL) {
+        Block<BrickVol> b;
+        b.vol = a.bv;
+        b.ox = block_origin(a.L, bi);
+        b.oy = block_origin(a.L, bj);
+        b.oz = block_origin(a.L, bk);
+        b.ex = block_extent(a.L, 0, bi);
+        b.ey = block_extent(a.L, 1, bj);
+        b.ez = block_extent(a.L, 2, bk);
+        return cub_sample_brick<true>(b, x - (double)b.ox, y - (double)b.oy, z - (double)b.oz);
+    }
     return sample_in<CUBIC>(a.bv, a, bi, bj, bk, x, y, z);
 #endif
 }
@@ -1221,7 +1233,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
                     qk = owner(a, 2, pz);
                 }
             }
-            const double v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
+            const double v = vol_sample<CUBIC, !LIGHT>(a, qi, qj, qk, px, py, pz);
             c_eval += R.stage == 0;  // sample interpolations (gradient taps: 6 per shaded sample)
             bool composite = false;
             if (R.stage == 0) {
