@@ -332,6 +332,16 @@ VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z,
     return bounds_transparent(w, vlo, vhi) ? 2 : 0;
 }
 
+// The cell level of provably_transparent alone: every sample based in the
+// 4^3 cell around (x, y, z) classifies to a zero-opacity bin.
+VR_D bool cell_transparent(const RenderArgs &a, double x, double y, double z, int vlo, int vhi) {
+    const int gx = clampi((int)x, 0, a.L.n[0] - 1);
+    const int gy = clampi((int)y, 0, a.L.n[1] - 1);
+    const int gz = clampi((int)z, 0, a.L.n[2] - 1);
+    return bounds_transparent(__ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2)), vlo,
+                              vhi);
+}
+
 // Chained modes (iso, pre-integrated), the analogue of provably_transparent:
 // the level (3 macro cell, 1 cell, 2 unit cube; 0 none) of the largest
 // region around (x, y, z) whose interpolant bound [lo, hi] guarantees that
@@ -951,6 +961,10 @@ struct PostRay {
 #define VR_PHASE_A_CAP 32  // swept 4..64: 32 best (C2 1656 -> 2279 fps vs 8; C3 +1 %)
 #endif
 constexpr int kPhaseACap = VR_PHASE_A_CAP;  // cheap steps a lane may take per trip
+#ifndef VR_DENSE_BURST
+#define VR_DENSE_BURST 32
+#endif
+constexpr int kDenseBurst = VR_DENSE_BURST;  // consecutive interpolated samples per trip (unlit, no skip)
 
 // A long ray handed from the per-lane kernel to the warp-cooperative one:
 // everything needed to continue it exactly where it stopped.
@@ -1283,6 +1297,54 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
                 R.stage = -1;
                 R.n += 1;
                 if (R.acc_a >= a.term_alpha) finished = true;  // early ray termination
+            }
+            // Dense burst (unlit, no skip predicate): once a sample needed its
+            // interpolation, the following ones usually do too -- march them
+            // here, consecutively, without a trip each (a trip's queue visit,
+            // cheap-step phase and culling hierarchy cost as much as the
+            // interpolation).  The burst stops at the first sample whose 4^3
+            // cell is provably transparent, where the next trip's phase A
+            // takes over with its culled runs; the samples are the
+            // reference's (_kernels.py:508-537), in order.
+            if (!LIGHT && !SKIP && !MV && !finished && R.stage < 0) {
+                int burst = 0;
+#pragma unroll 1
+                while (burst < kDenseBurst && R.n < R.N) {
+                    const long long n = R.n;
+                    const double t = R.t0 + ((double)n + 0.5) * a.step;
+                    const double x = divide(R.r.ox + t * R.r.dx, a.dsx);
+                    const double y = divide(R.r.oy + t * R.r.dy, a.dsy);
+                    const double z = divide(R.r.oz + t * R.r.dz, a.dsz);
+                    if (cull && cell_transparent(a, x, y, z, first_vis, last_vis)) break;
+                    const int bi = owner(a, 0, x), bj = owner(a, 1, y), bk = owner(a, 2, z);
+                    const int b = (bk * nby + bj) * nbx + bi;
+                    if (b != R.last_hit) {
+                        if (a.blocks_hit) a.blocks_hit[b] = 1;
+                        R.last_hit = b;
+                    }
+                    const double v = vol_sample<CUBIC, true>(a, bi, bj, bk, x, y, z);
+                    ++burst;
+                    R.taken += 1;
+                    R.n = n + 1;
+                    const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
+                    const double sa = __ldg(a.lut + 4 * sbin + 3);
+                    if (sa > 0.0) {
+                        ++R.nvis;
+                        const double ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
+                        const double w = (1.0 - R.acc_a) * ahat;
+                        R.acc_r += w * __ldg(a.lut + 4 * sbin);
+                        R.acc_g += w * __ldg(a.lut + 4 * sbin + 1);
+                        R.acc_b += w * __ldg(a.lut + 4 * sbin + 2);
+                        R.acc_a += w;
+                        if (R.acc_a >= a.term_alpha) {  // early ray termination
+                            finished = true;
+                            break;
+                        }
+                    }
+                }
+                c_eval += burst;
+                c_iter += burst;
+                R.work += burst;
             }
         }
         if (R.stage < 0 && R.n >= R.N) finished = true;
