@@ -174,8 +174,11 @@ VR_D double sample_in(const V &vol, const RenderArgs &a, int bi, int bj, int bk,
 
 // the ray casters' interpolant: brick windows through L1 (default) or the
 // x-quad texture (VR_SAMPLER_TEX A/B builds)
-// (FUNNEL: the brick sampler's funnel tap extraction, for the unlit kernels)
-template <bool CUBIC, bool FUNNEL = false>
+// (FUNNEL: the brick sampler's funnel + byte-permute tap extraction)
+#ifndef VR_LIT_FUNNEL
+#define VR_LIT_FUNNEL 1  // 0: per-tap window shifts in the lit kernels (A/B builds)
+#endif
+template <bool CUBIC, bool FUNNEL = (VR_LIT_FUNNEL != 0)>
 VR_D double vol_sample(const RenderArgs &a, int bi, int bj, int bk, double x, double y, double z) {
 #if VR_SAMPLER_TEX
     return sample_in<CUBIC>(a.tv, a, bi, bj, bk, x, y, z);
@@ -1247,7 +1250,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads
                     qk = owner(a, 2, pz);
                 }
             }
-            const double v = vol_sample<CUBIC, !LIGHT>(a, qi, qj, qk, px, py, pz);
+            const double v = vol_sample<CUBIC, !LIGHT || VR_LIT_FUNNEL>(a, qi, qj, qk, px, py, pz);
             c_eval += R.stage == 0;  // sample interpolations (gradient taps: 6 per shaded sample)
             bool composite = false;
             if (R.stage == 0) {
