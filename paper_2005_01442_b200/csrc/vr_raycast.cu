@@ -994,7 +994,8 @@ VR_D bool item_pixel(const RenderArgs &a, long long item, int &cx, int &cy, long
     const int slot = (int)(item >> 7), local = (int)(item & 127);
     const int w = local >> 5, l = local & 31;
     const int lx = (w & 1) * 8 + (l & 7), ly = (w >> 1) * 4 + (l >> 3);
-    const int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
+    int cell = a.il_n > 1 ? slot * a.il_n + a.il_k : slot;
+    if (a.cell_order) cell = __ldg(a.cell_order + cell);  // centre-first visiting order
     cx = (cell % a.cells_x) * kTileW + lx;
     cy = (cell / a.cells_x) * kTileH + ly;
     out = (MV ? (long long)view * a.view_pix : 0ll) +
