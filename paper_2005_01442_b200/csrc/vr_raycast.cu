@@ -965,7 +965,7 @@ struct PostRay {
 #endif
 constexpr int kPhaseACap = VR_PHASE_A_CAP;  // cheap steps a lane may take per trip
 #ifndef VR_DENSE_BURST
-#define VR_DENSE_BURST 32
+#define VR_DENSE_BURST 64  // (C3-stress: 8 -> 31.9, 32 -> 38.2, 64 -> 39.0 fps)
 #endif
 constexpr int kDenseBurst = VR_DENSE_BURST;  // consecutive interpolated samples per trip (unlit, no skip)
 
@@ -1065,7 +1065,11 @@ template <bool CUBIC, bool LIGHT, bool SKIP, bool MV>
 #ifndef VR_POST_MIN_BLOCKS
 #define VR_POST_MIN_BLOCKS 4  // <= 128 registers: 16 warps/SM (latency-bound; swept 1..5)
 #endif
-__global__ void __launch_bounds__(kPersistThreads, VR_POST_MIN_BLOCKS *(kThreads / kPersistThreads))
+#ifndef VR_UNLIT_MIN_BLOCKS
+#define VR_UNLIT_MIN_BLOCKS 5  // unlit: <= 96 registers, 20 warps/SM (C3-stress +4 % over 16; 24: -1 %)
+#endif
+__global__ void __launch_bounds__(kPersistThreads,
+                                  (LIGHT ? VR_POST_MIN_BLOCKS : VR_UNLIT_MIN_BLOCKS) * (kThreads / kPersistThreads))
     raycast_post_kernel(const __grid_constant__ RenderArgs a) {
     pdl_enter();
 #ifdef VR_DEBUG_STATS

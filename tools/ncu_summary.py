@@ -98,7 +98,9 @@ def full(rep, out, config=None):
                "dram_bytes_per_launch": dram,
                "metrics": {k: [vals[k], units.get(k, "")] for k in sorted(vals)},
                "top_lines": [[f"{k[0]}:{k[1]}", samples[k] / tot_s, insts[k] / tot_i, text.get(k, "")]
-                             for k, _ in sorted(samples.items(), key=lambda x: -x[1])[:60]]}
+                             for k, _ in sorted(samples.items(), key=lambda x: -x[1])[:60]],
+               "top_inst_lines": [[f"{k[0]}:{k[1]}", samples[k] / tot_s, insts[k] / tot_i, text.get(k, "")]
+                                  for k, _ in sorted(insts.items(), key=lambda x: -x[1])[:80]]}
     Path(out + ".json").write_text(json.dumps(summary, indent=1))
     md = [f"# ncu --set full: `{kernel.split('(')[0]}`", "", f"report: `{Path(rep).name}` (gpurun_out, not committed)", "",
           "| metric | value | unit |", "|---|---:|---|"]
