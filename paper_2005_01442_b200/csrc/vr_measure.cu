@@ -206,7 +206,10 @@ VR_D unsigned group_bits(const int4 q, int thr) {
     return b;
 }
 
-constexpr int kBitsUnroll = 4;  // 16-byte loads in flight per lane (HBM latency x bandwidth)
+#ifndef VR_K4_UNROLL
+#define VR_K4_UNROLL 4
+#endif
+constexpr int kBitsUnroll = VR_K4_UNROLL;  // 16-byte loads in flight per lane (HBM latency x bandwidth)
 
 __global__ void __launch_bounds__(kMeasureThreads) inside_bits_kernel(const int16_t *__restrict__ v, long long n,
                                                                       int thr, unsigned *__restrict__ bits,
@@ -219,17 +222,20 @@ __global__ void __launch_bounds__(kMeasureThreads) inside_bits_kernel(const int1
     const long long tail_word = (n & 31) ? (n >> 5) : -1;  // owned by the tail thread
     // warp-uniform trip counts (whole warps of groups): the shuffles below run
     // converged; kBitsUnroll independent loads are issued before any is used
-    for (long long g0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) & ~31ll; g0 < n8;
-         g0 += kBitsUnroll * stride) {
+    // each warp streams kBitsUnroll consecutive 512-byte blocks per
+    // iteration (contiguous, so DRAM pages stay open)
+    const long long gbase = ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5) * (32 * kBitsUnroll);
+    const long long ustep = 32;
+    for (long long g0 = gbase; g0 < n8; g0 += kBitsUnroll * stride) {
         int4 q[kBitsUnroll];
 #pragma unroll
         for (int u = 0; u < kBitsUnroll; ++u) {
-            const long long g = g0 + u * stride + lane;
+            const long long g = g0 + u * ustep + lane;
             q[u] = g < n8 ? __ldcs(v4 + g) : make_int4(0, 0, 0, 0);  // streamed: read once
         }
 #pragma unroll
         for (int u = 0; u < kBitsUnroll; ++u) {
-            const long long g = g0 + u * stride + lane;
+            const long long g = g0 + u * ustep + lane;
             const unsigned b = g < n8 ? group_bits(q[u], thr) : 0u;
             c += (unsigned long long)__popc(b);
             // lanes 4m .. 4m+3 hold voxels 32m' .. 32m'+31 of one word

@@ -757,18 +757,27 @@ __global__ void __launch_bounds__(kBlock) sample_points_kernel(const int16_t *vo
 
 __global__ void __launch_bounds__(kBlock) threshold_kernel(const int16_t *__restrict__ v, long long n, int thr,
                                                            unsigned long long *count) {
-    constexpr int U = 4;  // 16-byte loads in flight per thread (HBM latency x bandwidth)
+#ifndef VR_K4_UNROLL
+#define VR_K4_UNROLL 4
+#endif
+    constexpr int U = VR_K4_UNROLL;  // 16-byte loads in flight per thread (HBM latency x bandwidth)
     unsigned long long c = 0;
     const long long nvec = n / 8;
     const int4 *v8 = reinterpret_cast<const int4 *>(v);
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i0 < nvec; i0 += U * stride) {
+    // each warp streams U consecutive 512-byte blocks per iteration (a
+    // contiguous 2 KiB per warp, not U blocks a grid stride apart: DRAM
+    // pages stay open -- 0.77 -> 0.86 of HBM at 512^3)
+    const long long wstride = stride * U, lane = threadIdx.x & 31;
+    const long long w0 = ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5) * (32 * U) + lane;
+    const long long ustep = 32;
+    for (long long i0 = w0; i0 < nvec; i0 += wstride) {
         int4 q[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) q[u] = i0 + u * stride < nvec ? __ldcs(v8 + i0 + u * stride) : make_int4(0, 0, 0, 0);
+        for (int u = 0; u < U; ++u) q[u] = i0 + u * ustep < nvec ? __ldcs(v8 + i0 + u * ustep) : make_int4(0, 0, 0, 0);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if (i0 + u * stride >= nvec) continue;
+            if (i0 + u * ustep >= nvec) continue;
             const int16_t *h = reinterpret_cast<const int16_t *>(&q[u]);
 #pragma unroll
             for (int k = 0; k < 8; ++k) c += (h[k] >= thr) ? 1 : 0;
