@@ -967,7 +967,10 @@ constexpr int kPhaseACap = VR_PHASE_A_CAP;  // cheap steps a lane may take per t
 #ifndef VR_DENSE_BURST
 #define VR_DENSE_BURST 64  // (C3-stress: 8 -> 31.9, 32 -> 38.2, 64 -> 39.0 fps)
 #endif
-constexpr int kDenseBurst = VR_DENSE_BURST;  // consecutive interpolated samples per trip (unlit, no skip)
+constexpr int kDenseBurst = VR_DENSE_BURST;
+#ifndef VR_HEAVY_SMEM
+#define VR_HEAVY_SMEM 3  // cooperative kernel, chunk exchange through shared memory: 1 scans, 2 tap positions
+#endif  // consecutive interpolated samples per trip (unlit, no skip)
 
 // A long ray handed from the per-lane kernel to the warp-cooperative one:
 // everything needed to continue it exactly where it stopped.
@@ -1456,6 +1459,20 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
     pdl_enter();
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
+#if VR_HEAVY_SMEM
+    // per warp: the chunk's sample opacities and premultiplied colours (read
+    // in sample order by the serial scans, one broadcast load per sample
+    // instead of shuffles) and the positions of its visible samples (read by
+    // the lanes that take their gradient taps)
+    constexpr int kW = kPersistThreads / 32;
+    __shared__ double s_ahat[kW][32];
+    __shared__ double4 s_col[kW][32];
+#if VR_HEAVY_SMEM & 2
+    __shared__ double s_px[kW][32], s_py[kW][32], s_pz[kW][32];
+    __shared__ int4 s_blk[kW][32];
+#endif
+    const int wib = threadIdx.x >> 5;
+#endif
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
     const int first_vis = a.cull ? __ldg(a.lut_range + 2) : INT_MIN;  // value thresholds (vlo, vhi)
     const int last_vis = a.cull ? __ldg(a.lut_range + 3) : INT_MAX;
@@ -1558,6 +1575,17 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
                     const int id = base + lane;
                     act = id < ntaps;
                     const int k = id / 6, g = id - 6 * k;
+#if VR_HEAVY_SMEM & 2
+                    if (act) {  // (inactive lanes interpolate at their own position)
+                        px = s_px[wib][k];
+                        py = s_py[wib][k];
+                        pz = s_pz[wib][k];
+                        const int4 q = s_blk[wib][k];
+                        qi = q.x;
+                        qj = q.y;
+                        qk = q.z;
+                    }
+#else
                     const int src = act ? nth_bit(vis, k) : lane;
                     px = __shfl_sync(full, x, src);
                     py = __shfl_sync(full, y, src);
@@ -1565,6 +1593,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
                     qi = __shfl_sync(full, bi, src);
                     qj = __shfl_sync(full, bj, src);
                     qk = __shfl_sync(full, bk, src);
+#endif
                     // branch-free: lanes of a round take different taps, and a
                     // divergent branch here lets the compiler split the warp
                     const double hh = (g & 1) ? -0.5 : 0.5;
@@ -1595,10 +1624,18 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
                     // the terminating sample (_kernels.py:531-537: A += (1 - A) * a)
                     unsigned cm = __ballot_sync(full, contrib);
                     double A = acc_a;
+#if VR_HEAVY_SMEM
+                    s_ahat[wib][lane] = ahat;
+                    __syncwarp();
+#endif
                     while (cm) {
                         const int src = __ffs(cm) - 1;
                         cm &= cm - 1;
+#if VR_HEAVY_SMEM
+                        const double w = (1.0 - A) * s_ahat[wib][src];
+#else
                         const double w = (1.0 - A) * __shfl_sync(full, ahat, src);
+#endif
                         if (lane == src) wself = w;  // this sample's weight, reused by the composite
                         A += w;
                         if (A >= a.term_alpha) {
@@ -1611,6 +1648,15 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
                         vis = __ballot_sync(full, contrib) & upto;
                         ntaps = 6 * __popc(vis);
                         rank = __popc(vis & ((1u << lane) - 1u));
+#if VR_HEAVY_SMEM & 2
+                        if ((vis >> lane) & 1u) {
+                            s_px[wib][rank] = x;
+                            s_py[wib][rank] = y;
+                            s_pz[wib][rank] = z;
+                            s_blk[wib][rank] = make_int4(bi, bj, bk, 0);
+                        }
+                        __syncwarp();
+#endif
                     }
                 } else {
 #pragma unroll
@@ -1634,6 +1680,25 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
             {
                 const unsigned upto = et_lane >= 31 ? full : ((2u << et_lane) - 1u);
                 unsigned cm = __ballot_sync(full, contrib) & upto;
+#if VR_HEAVY_SMEM
+                // each lane's products w * colour (the reference's products,
+                // formed in parallel); only the sums run in sample order.
+                // w == (1 - acc_a) * ahat: the same operations on the same
+                // values as in the termination scan above
+                __syncwarp();
+                s_col[wib][lane] = make_double4(wself * sr, wself * sg, wself * sb, wself);
+                __syncwarp();
+                while (cm) {
+                    const int src = __ffs(cm) - 1;
+                    cm &= cm - 1;
+                    const double4 c = s_col[wib][src];
+                    acc_r += c.x;
+                    acc_g += c.y;
+                    acc_b += c.z;
+                    acc_a += c.w;
+                }
+                __syncwarp();
+#else
                 while (cm) {
                     const int src = __ffs(cm) - 1;
                     cm &= cm - 1;
@@ -1647,6 +1712,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
                     acc_b += w * b_;
                     acc_a += w;
                 }
+#endif
             }
             // counts up to and including the terminating sample
             const unsigned upto = et_lane >= 31 ? full : ((2u << et_lane) - 1u);
