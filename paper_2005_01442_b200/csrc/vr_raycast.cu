@@ -969,7 +969,7 @@ constexpr int kPhaseACap = VR_PHASE_A_CAP;  // cheap steps a lane may take per t
 #endif
 constexpr int kDenseBurst = VR_DENSE_BURST;
 #ifndef VR_HEAVY_SMEM
-#define VR_HEAVY_SMEM 3  // cooperative kernel, chunk exchange through shared memory: 1 scans, 2 tap positions
+#define VR_HEAVY_SMEM 7  // cooperative kernel, chunk exchange through shared memory: 1 scans, 2 tap positions, 4 tap values
 #endif  // consecutive interpolated samples per trip (unlit, no skip)
 
 // A long ray handed from the per-lane kernel to the warp-cooperative one:
@@ -1467,6 +1467,9 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
     constexpr int kW = kPersistThreads / 32;
     __shared__ double s_ahat[kW][32];
     __shared__ double4 s_col[kW][32];
+#if VR_HEAVY_SMEM & 4
+    __shared__ double s_tap[kW][6 * 32];
+#endif
 #if VR_HEAVY_SMEM & 2
     __shared__ double s_px[kW][32], s_py[kW][32], s_pz[kW][32];
     __shared__ int4 s_blk[kW][32];
@@ -1659,14 +1662,27 @@ __global__ void __launch_bounds__(kPersistThreads, VR_HEAVY_MIN_BLOCKS *(kThread
 #endif
                     }
                 } else {
+#if VR_HEAVY_SMEM & 4
+                    if (act) s_tap[wib][base + lane] = v;
+#else
 #pragma unroll
                     for (int g = 0; g < 6; ++g) {
                         const int s = 6 * rank + g - base;
                         const double w = __shfl_sync(full, v, s & 31);
                         if (s >= 0 && s < 32) tp[g] = w;
                     }
+#endif
                 }
             }
+#if VR_HEAVY_SMEM & 4
+            if (LIGHT && ntaps) {
+                __syncwarp();
+                if ((vis >> lane) & 1u) {
+#pragma unroll
+                    for (int g = 0; g < 6; ++g) tp[g] = s_tap[wib][6 * rank + g];
+                }
+            }
+#endif
             if (LIGHT && ((vis >> lane) & 1u)) {
                 const double gx = divide(tp[0] - tp[1], a.dsx);
                 const double gy = divide(tp[2] - tp[3], a.dsy);
