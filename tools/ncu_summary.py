@@ -16,6 +16,9 @@ import sys
 from collections import defaultdict
 from pathlib import Path
 
+TIME_UNITS = {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1.0,
+              "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
+
 METRICS = [
     "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
     "lts__t_bytes.sum", "l1tex__t_bytes.sum", "launch__registers_per_thread", "launch__grid_size",
@@ -90,8 +93,8 @@ def full(rep, out, config=None):
         u = units.get(name, "")
         if isinstance(x, float) and u in ("Kbyte", "Mbyte", "Gbyte", "byte"):
             return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
-        if isinstance(x, float) and u in ("usecond", "msecond", "nsecond"):
-            return x * {"nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3}[u]
+        if isinstance(x, float) and u in TIME_UNITS:
+            return x * TIME_UNITS[u]
         return x
     dram = (scaled("dram__bytes_read.sum") or 0) + (scaled("dram__bytes_write.sum") or 0)
     summary = {"kernel": kernel, "report": Path(rep).name, "duration_s": scaled("gpu__time_duration.sum"),
@@ -132,6 +135,15 @@ if __name__ == "__main__":
         def metric(p, name):
             m = p["metrics"].get(name)
             return float(m[0]) if m and isinstance(m[0], (int, float)) else None
+
+        def seconds(p):
+            m = p["metrics"].get("gpu__time_duration.sum")
+            if m and isinstance(m[0], (int, float)) and m[1] in TIME_UNITS:
+                return float(m[0]) * TIME_UNITS[m[1]]
+            return p.get("duration_s") or 0.0
+
+        for p in parts:
+            p["duration_s"] = seconds(p)
 
         def weighted(name):
             num = den = 0.0
