@@ -968,6 +968,10 @@ constexpr int kPhaseACap = VR_PHASE_A_CAP;  // cheap steps a lane may take per t
 #define VR_DENSE_BURST 64  // (C3-stress: 8 -> 31.9, 32 -> 38.2, 64 -> 39.0 fps)
 #endif
 constexpr int kDenseBurst = VR_DENSE_BURST;
+#ifndef VR_COOP_GRAD
+#define VR_COOP_GRAD 1  // lit per-lane kernel: a shaded sample's six gradient taps spread over its warp
+#endif
+constexpr bool kCoopGrad = VR_COOP_GRAD != 0;
 #ifndef VR_HEAVY_SMEM
 #define VR_HEAVY_SMEM 7  // cooperative kernel, chunk exchange through shared memory: 1 scans, 2 tap positions, 4 tap values
 #endif  // consecutive interpolated samples per trip (unlit, no skip)
@@ -1082,6 +1086,15 @@ __global__ void __launch_bounds__(kPersistThreads,
     const int lane = threadIdx.x & 31;
     const unsigned full = 0xffffffffu;
     const long long total = a.items_per_view * a.nviews;
+#if VR_COOP_GRAD
+    // (lit) per warp: positions of the samples being shaded this trip and
+    // their gradient-tap values, spread over the warp's lanes
+    constexpr int kW = kPersistThreads / 32;
+    __shared__ double s_px[kW][32], s_py[kW][32], s_pz[kW][32];
+    __shared__ int4 s_blk[kW][32];
+    __shared__ double s_tap[kW][6 * 32];
+    const int wib = threadIdx.x >> 5;
+#endif
     const int nbx = a.L.nb[0], nby = a.L.nb[1];
     const int first_vis = a.cull ? __ldg(a.lut_range + 2) : INT_MIN;  // value thresholds (vlo, vhi)
     const int last_vis = a.cull ? __ldg(a.lut_range + 3) : INT_MAX;
@@ -1142,7 +1155,9 @@ __global__ void __launch_bounds__(kPersistThreads,
         if (drained && t_drain == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_drain));
         n_trips_after += drained ? 1 : 0;
 #endif
-        if (!R.live) continue;
+        // (lit, cooperative gradients: idle lanes stay for the trip -- they
+        // take gradient taps of the warp's shaded samples)
+        if (!(kCoopGrad && LIGHT) && !R.live) continue;
 
         // ---- once the ray queue has drained, hand long rays to the
         // warp-cooperative kernel (at a clean point, nothing pending): the
@@ -1153,7 +1168,7 @@ __global__ void __launch_bounds__(kPersistThreads,
         // a hand-off record and a warp's fetch (C3 +3 %, C2 +4 %).  A frame
         // with fewer rays than this kernel has lanes hands them over at once:
         // one lane per ray cannot fill the GPU (C1: 7,300 vs 2,900 frames/s).
-        if (a.heavy && ((drained && (R.work > 0 || starved)) || R.work > a.heavy_after || (R.nvis >= a.heavy_vis && R.acc_a < a.heavy_vis_alpha)) &&
+        if (R.live && a.heavy && ((drained && (R.work > 0 || starved)) || R.work > a.heavy_after || (R.nvis >= a.heavy_vis && R.acc_a < a.heavy_vis_alpha)) &&
             R.work >= 0 && R.stage < 0 &&
             R.N - R.n >= a.heavy_min_left) {
             // long rays go to their own queue, which the cooperative kernel
@@ -1184,14 +1199,15 @@ __global__ void __launch_bounds__(kPersistThreads,
                 dbg[4] += 1;
                 dbg[5] += (unsigned long long)R.work;
 #endif
-                continue;
+                if (!(kCoopGrad && LIGHT)) continue;
+            } else {
+                R.work = INT_MIN;  // queue full: keep it here
             }
-            R.work = INT_MIN;  // queue full: keep it here
         }
 
         // ---- phase A: cheap steps until an interpolation is needed
         int steps = 0;
-        while (R.stage < 0 && R.n < R.N && steps < kPhaseACap) {
+        while (R.live && R.stage < 0 && R.n < R.N && steps < kPhaseACap) {
             ++steps;
             ++c_iter;
             const long long n = R.n;
@@ -1241,6 +1257,104 @@ __global__ void __launch_bounds__(kPersistThreads,
 
         // ---- phase B: one interpolation per lane with pending work
         bool finished = false;
+#if VR_COOP_GRAD
+        if (LIGHT) {
+            // Cooperative gradients: the lanes whose sample turns out visible
+            // get all six taps this trip, computed by the whole warp (32 taps
+            // per round, as in the cooperative kernel) instead of one tap per
+            // trip each: a shaded sample takes one trip, not seven, and every
+            // lane of a tap round does useful work.
+            __syncwarp();
+            const bool need = R.live && R.stage == 0;
+            if (__any_sync(full, need)) {
+                bool shading = false;
+                int ntaps = 0, rank = 0;
+#pragma unroll 1
+                for (int base = -32; base < ntaps; base += 32) {
+                    double px = 0.0, py = 0.0, pz = 0.0;  // (idle lanes: a valid position)
+                    int qi = 0, qj = 0, qk = 0;
+                    const int id = base + lane;
+                    const bool act = base < 0 ? need : id < ntaps;
+                    if (base < 0) {
+                        if (need) {
+                            px = R.x;
+                            py = R.y;
+                            pz = R.z;
+                            qi = R.bi;
+                            qj = R.bj;
+                            qk = R.bk;
+                        }
+                    } else if (act) {
+                        const int k = id / 6, g = id - 6 * k;
+                        px = s_px[wib][k];
+                        py = s_py[wib][k];
+                        pz = s_pz[wib][k];
+                        const int4 q = s_blk[wib][k];
+                        // tap g: +x, -x, +y, -y, +z, -z (_kernels.py:236-253)
+                        const double hh = (g & 1) ? -0.5 : 0.5;
+                        const int axis = g >> 1;
+                        px = axis == 0 ? px + hh : px;
+                        py = axis == 1 ? py + hh : py;
+                        pz = axis == 2 ? pz + hh : pz;
+                        const int o = owner(a, axis, axis == 0 ? px : axis == 1 ? py : pz);
+                        qi = axis == 0 ? o : q.x;
+                        qj = axis == 1 ? o : q.y;
+                        qk = axis == 2 ? o : q.z;
+                    }
+                    const double v = vol_sample<CUBIC, VR_LIT_FUNNEL>(a, qi, qj, qk, px, py, pz);
+                    if (base < 0) {
+                        if (need) {
+                            ++c_eval;
+                            const int sbin = lut_bin(v, a.lut_lo, a.lut_inv_w, a.nlut);
+                            const double sa = __ldg(a.lut + 4 * sbin + 3);
+                            if (sa > 0.0) {
+                                R.sr = __ldg(a.lut + 4 * sbin);
+                                R.sg = __ldg(a.lut + 4 * sbin + 1);
+                                R.sb = __ldg(a.lut + 4 * sbin + 2);
+                                R.ahat = 1.0 - vr_pow(1.0 - sa, a.corr);
+                                shading = true;
+                            } else {
+                                R.stage = -1;
+                                R.n += 1;
+                            }
+                        }
+                        const unsigned gm = __ballot_sync(full, shading);
+                        ntaps = 6 * __popc(gm);
+                        rank = __popc(gm & ((1u << lane) - 1u));
+                        if (shading) {
+                            s_px[wib][rank] = R.x;
+                            s_py[wib][rank] = R.y;
+                            s_pz[wib][rank] = R.z;
+                            s_blk[wib][rank] = make_int4(R.bi, R.bj, R.bk, 0);
+                        }
+                        __syncwarp();
+                    } else if (act) {
+                        s_tap[wib][id] = v;
+                    }
+                }
+                __syncwarp();
+                if (shading) {
+                    const double *tp = s_tap[wib] + 6 * rank;
+                    const double gx = divide(tp[0] - tp[1], a.dsx), gy = divide(tp[2] - tp[3], a.dsy),
+                                 gz = divide(tp[4] - tp[5], a.dsz);
+                    ++c_shaded;
+                    const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+                    if (norm > 1e-12)
+                        shade(a, R.sr, R.sg, R.sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
+                    ++R.nvis;
+                    const double w = (1.0 - R.acc_a) * R.ahat;
+                    R.acc_r += w * R.sr;
+                    R.acc_g += w * R.sg;
+                    R.acc_b += w * R.sb;
+                    R.acc_a += w;
+                    R.stage = -1;
+                    R.n += 1;
+                    if (R.acc_a >= a.term_alpha) finished = true;  // early ray termination
+                }
+                __syncwarp();  // the shared arrays are refilled next trip
+            }
+        } else
+#endif
         if (R.stage >= 0) {
             double px = R.x, py = R.y, pz = R.z;
             int qi = R.bi, qj = R.bj, qk = R.bk;
@@ -1358,7 +1472,7 @@ __global__ void __launch_bounds__(kPersistThreads,
                 R.work += burst;
             }
         }
-        if (R.stage < 0 && R.n >= R.N) finished = true;
+        if (R.live && R.stage < 0 && R.n >= R.N) finished = true;
         R.work += steps + 1;
 
         // ---- finish: background, epilogue, per-pixel outputs
