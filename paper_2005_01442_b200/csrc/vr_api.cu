@@ -37,7 +37,7 @@
 #define VR_HEAVY_AFTER (1 << 30)
 #endif
 #ifndef VR_HEAVY_VIS
-#define VR_HEAVY_VIS 4
+#define VR_HEAVY_VIS 64
 #endif
 #ifndef VR_HEAVY_VIS_ALPHA
 #define VR_HEAVY_VIS_ALPHA 0.5
@@ -837,12 +837,15 @@ static int render_impl(vr_volume *vol, vr_grid *grid, const vr_camera *cam, cons
         a.heavy_cap = items < cap ? items : cap;
         a.heavy_min_left = VR_HEAVY_MIN_LEFT;
         a.heavy_after = VR_HEAVY_AFTER;
-        // Dense rays (4 composited samples) go to the cooperative kernel at
-        // once when it can save work on them: with lighting and early
-        // termination it computes gradients only up to the terminating
-        // sample (C3-soft 94 -> 145 fps; C1/C2/C3 unchanged, sweep 2..32).
-        // Without, its in-order composite of a fully visible chunk is serial
-        // and the per-lane kernel is faster (C3-stress 21 vs 12 fps).
+        // Dense rays (64 composited samples, still below alpha 0.5) go to
+        // the cooperative kernel at once when it can save work on them: with
+        // lighting and early termination it computes gradients only up to
+        // the terminating sample.  Before the per-lane kernel spread its
+        // gradient taps over the warp, 4 was best (C3-soft 94 -> 145 fps);
+        // since then 64 is (C3-soft +1.9 %, others unchanged; no early
+        // hand-off at all measures the same).  Without lighting, its in-order
+        // composite of a fully visible chunk is serial and the per-lane
+        // kernel is faster (C3-stress 21 vs 12 fps).
         a.heavy_vis_alpha = VR_HEAVY_VIS_ALPHA;
         a.heavy_vis = prm->lighting && prm->term_alpha < 1.0 ? VR_HEAVY_VIS : 1 << 30;
         if (a.heavy_min_left > 0) {

@@ -1,3 +1,2 @@
 cd "$GRAFT_REPO_ROOT"
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -2
-bash tools/gpu_ab_variants.sh "c3 c3soft c2 c4 c1" build_variants/cg0.so
+bash tools/gpu_ab_variants.sh "c3pre c3preint c3soft c3 c2 c4" build_variants/hv64.so build_variants/hv1073741824.so
