@@ -189,6 +189,12 @@ bool finite_positive(double v) { return std::isfinite(v) && v > 0.0; }
 // rectangle) and kept; any failure leaves row-major order (nullptr), which
 // renders the same pixels.
 constexpr long long kCentreFirstWaves = 6;
+#ifndef VR_PHASE_CAP_MANY
+#define VR_PHASE_CAP_MANY 24  // (16: C3 +1.4 %, C3-soft -3 %; 24: C3 +1.5 %, C4 +1.4 %, C3-soft -1 %)
+#endif
+#ifndef VR_PHASE_CAP_FEW
+#define VR_PHASE_CAP_FEW 32
+#endif
 #ifndef VR_ROW_MAJOR_CELLS
 std::mutex g_order_mu;
 
@@ -744,9 +750,13 @@ static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
     a.il_k = cam->interleave_n > 1 ? cam->interleave_k : 0;
     a.il_packed = cam->interleave_n > 1 && !cam->interleave_frame;
     // (the sort-first interleave keeps its slot -> cell map)
-    a.cell_order = a.il_n > 1 || a.items_per_view >= kCentreFirstWaves * vr::device_sms() * 16 * 32
-                       ? nullptr
-                       : cell_order_table(a.cells_x, a.ncells);
+    const bool many_waves = a.items_per_view >= kCentreFirstWaves * vr::device_sms() * 16 * 32;
+    a.cell_order = a.il_n > 1 || many_waves ? nullptr : cell_order_table(a.cells_x, a.ncells);
+    // cheap steps per trip of the per-lane post-classified kernel: frames of
+    // many waves reach their next interpolation (and its cooperative
+    // gradient round) sooner with a shorter trip; frames of few waves keep
+    // the longer one (their queue drains while the first waves are in flight)
+    a.phase_cap = many_waves ? VR_PHASE_CAP_MANY : VR_PHASE_CAP_FEW;
     a.step = prm->step;
     a.ref_step = prm->ref_step;
     a.corr = vr::make_pow(prm->step / prm->ref_step);  // _kernels.py:338

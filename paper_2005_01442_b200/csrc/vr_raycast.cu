@@ -1217,7 +1217,7 @@ __global__ void __launch_bounds__(kPersistThreads,
 
         // ---- phase A: cheap steps until an interpolation is needed
         int steps = 0;
-        while (R.live && R.stage < 0 && R.n < R.N && steps < kPhaseACap) {
+        while (R.live && R.stage < 0 && R.n < R.N && steps < a.phase_cap) {
             ++steps;
             ++c_iter;
             const long long n = R.n;

@@ -19,6 +19,7 @@ struct RenderArgs {
     int il_packed;         // outputs packed slot after slot (else at row-major rectangle positions)
     int cells_x, ncells;   // 16x8 cells across the rectangle, total
     const int *cell_order; // persistent ray queue: slot -> cell (nullptr: row-major)
+    int phase_cap;         // per-lane post-classified kernel: cheap steps per trip
     int slots;             // CTAs launched (cells rendered by this call)
     double pos[3], fwd[3], right[3], up[3];
     double half_w, half_h;
