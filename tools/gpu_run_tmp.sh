@@ -1,3 +1,5 @@
+# scratch A/B driver used during tuning: edit the config list and variant libraries, then
+#   gpurun -- 'bash tools/gpu_run_tmp.sh'
 cd "$GRAFT_REPO_ROOT"
 timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -1
-for c in c5 c3; do timeout 600 python bench.py --config $c --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['value'],1))"; done
+bash tools/gpu_ab_variants.sh "c3 c3soft c2 c4" "$@"
