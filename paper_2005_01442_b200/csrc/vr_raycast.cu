@@ -982,6 +982,9 @@ constexpr int kDenseBurst = VR_DENSE_BURST;
 #define VR_COOP_GRAD 1  // lit per-lane kernel: a shaded sample's six gradient taps spread over its warp
 #endif
 constexpr bool kCoopGrad = VR_COOP_GRAD != 0;
+#ifndef VR_CHAIN_COOP
+#define VR_CHAIN_COOP 1  // chained per-lane kernel: cooperative gradients (pre-classified)
+#endif
 #ifndef VR_HEAVY_SMEM
 #define VR_HEAVY_SMEM 7  // cooperative kernel, chunk exchange through shared memory: 1 scans, 2 tap positions, 4 tap values
 #endif  // consecutive interpolated samples per trip (unlit, no skip)
@@ -2032,6 +2035,18 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
     ChainRay R;
     R.live = false;
     bool exhausted = false;
+#if VR_CHAIN_COOP
+    constexpr int kW = kPersistThreads / 32;
+    __shared__ double s_px[kW][32], s_py[kW][32], s_pz[kW][32];
+    __shared__ int4 s_blk[kW][32];
+    __shared__ double s_tap[kW][6 * 32];
+    const int wib = threadIdx.x >> 5;
+    // (pre-classified only: iso and pre-integrated measured slower with it,
+    // their kernels spill more)
+    constexpr bool coop = LIGHT && KIND == kPre;
+#else
+    constexpr bool coop = false;
+#endif
     for (;;) {
         // ---- fetch rays for idle lanes (one atomic per warp)
         const bool want = !R.live && !exhausted;
@@ -2082,7 +2097,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
         if (lane == 0 && a.heavy)
             head_done = *reinterpret_cast<volatile unsigned long long *>(a.work_counter) >= (unsigned long long)total;
         const bool drained = __shfl_sync(full, head_done, 0) != 0 || __any_sync(full, exhausted);
-        if (!R.live) continue;
+        if (!coop && !R.live) continue;
 
         // ---- once the queue has drained, long rays go to the cooperative
         // kernel at a clean point (the frame would otherwise end with a few
@@ -2090,7 +2105,7 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
         // (dense lit rays -- several composited samples, still far from
         // termination -- go at once: the cooperative kernel spreads their
         // gradient taps over the warp)
-        if (a.heavy && R.stage == kcNone && R.N - R.n >= a.heavy_min_left &&
+        if (R.live && a.heavy && R.stage == kcNone && R.N - R.n >= a.heavy_min_left &&
             (drained || (R.nvis >= a.heavy_vis && R.acc_a < a.heavy_vis_alpha))) {
             const unsigned long long slot = atomicAdd(a.heavy_count, 1ull);
             if (slot < (unsigned long long)a.heavy_cap) {
@@ -2115,13 +2130,13 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                 h.flags = (R.prev_valid ? 1 : 0) | (R.prev_pending ? 2 : 0) | (R.prev_skippable ? 4 : 0);
                 static_cast<ChainRec *>(a.heavy)[slot] = h;
                 R.live = false;
-                continue;
+                if (!coop) continue;
             }
         }
 
         // ---- phase A: skip leaps until a taken sample needs an interpolation
         int steps = 0;
-        while (R.stage == kcNone && R.n < R.N && steps < kPhaseACap) {
+        while (R.live && R.stage == kcNone && R.n < R.N && steps < kPhaseACap) {
             ++steps;
             ++c_iter;
             const long long n = R.n;
@@ -2222,7 +2237,60 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
 
         // ---- phase B: one interpolation
         bool finished = false;
-        if (R.stage != kcNone) {
+        auto gradient_done = [&](double dgx, double dgy, double dgz) {
+            const double gx = divide(dgx, a.dsx), gy = divide(dgy, a.dsy), gz = divide(dgz, a.dsz);
+            ++c_shaded;
+            const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
+            if (KIND == kPre) {
+                double sr = R.cr, sg = R.cg, sb = R.cb;
+                if (norm > 1e-12) shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
+                const double w = (1.0 - R.acc_a) * R.ca;
+                R.acc_r += w * sr;
+                R.acc_g += w * sg;
+                R.acc_b += w * sb;
+                R.acc_a += w;
+                ++R.nvis;
+                R.stage = kcNone;
+                R.n += 1;
+                if (R.acc_a >= a.term_alpha) finished = true;
+            } else if (KIND == kIso) {
+                const int ib = lut_bin(a.isovalue, a.lut_lo, a.lut_inv_w, a.nlut);
+                double cr = __ldg(a.lut + 4 * ib), cg = __ldg(a.lut + 4 * ib + 1), cb = __ldg(a.lut + 4 * ib + 2);
+                if (LIGHT && norm > 1e-12)
+                    shade(a, cr, cg, cb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
+                R.acc_r = cr;
+                R.acc_g = cg;
+                R.acc_b = cb;
+                R.acc_a = 1.0;
+                finished = true;
+            } else {
+                double seg_r = R.cr, seg_g = R.cg, seg_b = R.cb;
+                const double seg_a = R.ca;
+                if (norm > 1e-12) {
+                    const double ndl = fabs(((gx * -R.r.dx + gy * -R.r.dy) + gz * -R.r.dz) / norm);
+                    const double scale = a.ka + a.kd * ndl;
+                    const double spec = a.ks * vr_pow(ndl, a.shin) * seg_a;
+                    seg_r = clampf(scale * seg_r + spec, 0.0, 1.0);
+                    seg_g = clampf(scale * seg_g + spec, 0.0, 1.0);
+                    seg_b = clampf(scale * seg_b + spec, 0.0, 1.0);
+                }
+                const double w = 1.0 - R.acc_a;
+                R.acc_r += w * seg_r;
+                R.acc_g += w * seg_g;
+                R.acc_b += w * seg_b;
+                R.acc_a += w * seg_a;
+                ++R.nvis;
+                if (R.acc_a >= a.term_alpha) {
+                    finished = true;
+                } else {
+                    R.prev_s = R.s;
+                    R.prev_valid = true;
+                    R.stage = kcNone;
+                    R.n += 1;
+                }
+            }
+        };
+        if (R.live && R.stage != kcNone && !(coop && R.stage >= kcGrad)) {
             double px = R.x, py = R.y, pz = R.z;
             int qi = R.bi, qj = R.bj, qk = R.bk;
             bool own = false;  // position not attributed yet (owner from the position)
@@ -2419,65 +2487,60 @@ __global__ void __launch_bounds__(kPersistThreads, VR_CHAIN_MIN_BLOCKS *(kThread
                 if (q < 5) {
                     R.stage += 1;
                 } else {
-                    const double gx = divide(R.gx, a.dsx), gy = divide(R.gy, a.dsy), gz = divide(R.gz, a.dsz);
-                    ++c_shaded;
-                    const double norm = sqrt((gx * gx + gy * gy) + gz * gz);
-                    if (KIND == kPre) {
-                        // _kernels.py:495-507
-                        double sr = R.cr, sg = R.cg, sb = R.cb;
-                        if (norm > 1e-12)
-                            shade(a, sr, sg, sb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
-                        const double w = (1.0 - R.acc_a) * R.ca;
-                        R.acc_r += w * sr;
-                        R.acc_g += w * sg;
-                        R.acc_b += w * sb;
-                        R.acc_a += w;
-                        ++R.nvis;
-                        R.stage = kcNone;
-                        R.n += 1;
-                        if (R.acc_a >= a.term_alpha) finished = true;
-                    } else if (KIND == kIso) {
-                        // _kernels.py:466-483: LUT colour at the isovalue, shaded, opaque
-                        const int ib = lut_bin(a.isovalue, a.lut_lo, a.lut_inv_w, a.nlut);
-                        double cr = __ldg(a.lut + 4 * ib), cg = __ldg(a.lut + 4 * ib + 1), cb = __ldg(a.lut + 4 * ib + 2);
-                        if (LIGHT && norm > 1e-12)
-                            shade(a, cr, cg, cb, -gx / norm, -gy / norm, -gz / norm, -R.r.dx, -R.r.dy, -R.r.dz);
-                        R.acc_r = cr;
-                        R.acc_g = cg;
-                        R.acc_b = cb;
-                        R.acc_a = 1.0;
-                        finished = true;
-                    } else {
-                        // _kernels.py:560-581
-                        double seg_r = R.cr, seg_g = R.cg, seg_b = R.cb;
-                        const double seg_a = R.ca;
-                        if (norm > 1e-12) {
-                            const double ndl = fabs(((gx * -R.r.dx + gy * -R.r.dy) + gz * -R.r.dz) / norm);
-                            const double scale = a.ka + a.kd * ndl;
-                            const double spec = a.ks * vr_pow(ndl, a.shin) * seg_a;
-                            seg_r = clampf(scale * seg_r + spec, 0.0, 1.0);
-                            seg_g = clampf(scale * seg_g + spec, 0.0, 1.0);
-                            seg_b = clampf(scale * seg_b + spec, 0.0, 1.0);
-                        }
-                        const double w = 1.0 - R.acc_a;
-                        R.acc_r += w * seg_r;
-                        R.acc_g += w * seg_g;
-                        R.acc_b += w * seg_b;
-                        R.acc_a += w * seg_a;
-                        ++R.nvis;
-                        if (R.acc_a >= a.term_alpha) {
-                            finished = true;
-                        } else {
-                            R.prev_s = R.s;
-                            R.prev_valid = true;
-                            R.stage = kcNone;
-                            R.n += 1;  // (no culled run after a contributing segment: the next may contribute)
-                        }
-                    }
+                    gradient_done(R.gx, R.gy, R.gz);
                 }
             }
         }
-        if (R.stage == kcNone && R.n >= R.N) finished = true;
+#if VR_CHAIN_COOP
+        if (coop) {
+            __syncwarp();
+            const bool grad = R.live && R.stage == kcGrad;
+            const unsigned gm = __ballot_sync(full, grad);
+            if (gm) {
+                const int ntaps = 6 * __popc(gm);
+                const int rank = __popc(gm & ((1u << lane) - 1u));
+                if (grad) {
+                    s_px[wib][rank] = R.hx;
+                    s_py[wib][rank] = R.hy;
+                    s_pz[wib][rank] = R.hz;
+                    s_blk[wib][rank] = make_int4(R.hbi, R.hbj, R.hbk, 0);
+                }
+                __syncwarp();
+#pragma unroll 1
+                for (int base = 0; base < ntaps; base += 32) {
+                    const int id = base + lane;
+                    const bool act = id < ntaps;
+                    double px = 0.0, py = 0.0, pz = 0.0;
+                    int qi = 0, qj = 0, qk = 0;
+                    if (act) {
+                        const int k = id / 6, g = id - 6 * k;
+                        px = s_px[wib][k];
+                        py = s_py[wib][k];
+                        pz = s_pz[wib][k];
+                        const int4 q = s_blk[wib][k];
+                        const double hh = (g & 1) ? -0.5 : 0.5;
+                        const int axis = g >> 1;
+                        px = axis == 0 ? px + hh : px;
+                        py = axis == 1 ? py + hh : py;
+                        pz = axis == 2 ? pz + hh : pz;
+                        const int o = owner(a, axis, axis == 0 ? px : axis == 1 ? py : pz);
+                        qi = axis == 0 ? o : q.x;
+                        qj = axis == 1 ? o : q.y;
+                        qk = axis == 2 ? o : q.z;
+                    }
+                    const double v = vol_sample<CUBIC>(a, qi, qj, qk, px, py, pz);
+                    if (act) s_tap[wib][id] = v;
+                }
+                __syncwarp();
+                if (grad) {
+                    const double *tp = s_tap[wib] + 6 * rank;
+                    gradient_done(tp[0] - tp[1], tp[2] - tp[3], tp[4] - tp[5]);
+                }
+                __syncwarp();
+            }
+        }
+#endif
+        if (R.live && R.stage == kcNone && R.n >= R.N) finished = true;
 
         if (finished) {
             // background, epilogue, per-pixel outputs (_kernels.py:583-594)
