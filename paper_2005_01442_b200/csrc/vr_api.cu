@@ -715,6 +715,7 @@ static int build_args(vr_volume *vol, vr_grid *grid, const vr_camera *cam, const
     a.bv.p = vol->bricks;
     a.bv.bpy = (long long)vol->bnx * 64;
     a.bv.bpz = (long long)vol->bnx * vol->bny * 64;
+    a.bv.n = a.bv.bpz * vol->bnz;
     a.tv.tex = vol->qtex;
     a.L = grid ? grid->L : monolithic_layout(vol);
     a.dsx = vr::make_divisor(vol->sx);

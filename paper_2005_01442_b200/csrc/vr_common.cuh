@@ -292,21 +292,40 @@ struct LinearU8 {
     }
 };
 
+// Bounds-checked builds (-DVR_BOUNDS_CHECK, test only: compute-sanitizer is
+// closed on this GPU pool): every brick-window load traps when it leaves the
+// allocation.
+#ifdef VR_BOUNDS_CHECK
+#define VR_CHECK_SPAN(base, n, q, len)                                                   \
+    do {                                                                                 \
+        if ((const void *)(q) < (const void *)(base) ||                                  \
+            (const char *)((q) + (len)) > (const char *)((base) + (n))) __trap();         \
+    } while (0)
+#else
+#define VR_CHECK_SPAN(base, n, q, len) ((void)0)
+#endif
+
 struct BrickVol {
     const int16_t *p;
     long long bpy, bpz;  // int16 elements per row of bricks / per plane of bricks
+    long long n;         // int16 elements of the allocation (bounds-checked builds)
     VR_D const int16_t *row_ptr(int x, int y, int z) const {
         return p + (long long)(z >> 2) * bpz + (long long)(y >> 2) * bpy + ((long long)(x >> 2) << 6) +
                ((z & 3) << 4) + ((y & 3) << 2);
     }
-    VR_D double at(int x, int y, int z) const { return tap(row_ptr(x, y, z) + (x & 3)); }
+    VR_D double at(int x, int y, int z) const {
+        VR_CHECK_SPAN(p, n, row_ptr(x, y, z) + (x & 3), 1);
+        return tap(row_ptr(x, y, z) + (x & 3));
+    }
     // four (two) consecutive voxels from x: the 8-byte brick row holding x,
     // plus the next brick's row when the run crosses into it
     VR_D unsigned long long run(int x, int y, int z, int len) const {
         const int16_t *q = row_ptr(x, y, z);
+        VR_CHECK_SPAN(p, n, q, 4);
         unsigned long long lo = __ldg(reinterpret_cast<const unsigned long long *>(q));
         const int o = x & 3;
         if (o + len > 4) {
+            VR_CHECK_SPAN(p, n, q + 64, 4);
             unsigned long long hi = __ldg(reinterpret_cast<const unsigned long long *>(q + 64));
             lo = (lo >> (16 * o)) | (hi << (64 - 16 * o));
         } else {
@@ -479,6 +498,8 @@ VR_D double tri_sample(const Block<BrickVol> &b, double x, double y, double z) {
     const unsigned long long *q10 = reinterpret_cast<const unsigned long long *>(px + (y1 + z0));
     const unsigned long long *q01 = reinterpret_cast<const unsigned long long *>(px + (y0 + z1));
     const unsigned long long *q11 = reinterpret_cast<const unsigned long long *>(px + (y1 + z1));
+    VR_CHECK_SPAN(b.vol.p, b.vol.n, px + (y0 + z0), need_hi ? 68 : 4);
+    VR_CHECK_SPAN(b.vol.p, b.vol.n, px + (y1 + z1), need_hi ? 68 : 4);
     const unsigned long long l00 = __ldg(q00), l10 = __ldg(q10), l01 = __ldg(q01), l11 = __ldg(q11);
     unsigned long long h00 = 0, h10 = 0, h01 = 0, h11 = 0;
     if (need_hi) {
@@ -539,6 +560,7 @@ VR_D double cub_sample_brick(const Block<BrickVol> &b, double x, double y, doubl
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
             const unsigned long long *q = reinterpret_cast<const unsigned long long *>(px + (zo[c] + yo[r]));
+            VR_CHECK_SPAN(b.vol.p, b.vol.n, px + (zo[c] + yo[r]), need_hi ? 68 : 4);
             lo[4 * c + r] = __ldg(q);
             hi[4 * c + r] = need_hi ? __ldg(q + 16) : 0ull;
         }

@@ -1,5 +1,5 @@
-# scratch A/B driver used during tuning: edit the config list and variant libraries, then
-#   gpurun -- 'bash tools/gpu_run_tmp.sh'
+# bounds-checked build over the whole GPU suite, then the release library's frame rates
 cd "$GRAFT_REPO_ROOT"
-timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -1
-bash tools/gpu_ab_variants.sh "c3 c3soft c2 c4" "$@"
+VR_LIB=build_variants/bounds.so timeout 1500 python -m pytest tests -q -m gpu -p no:cacheprovider 2>&1 | tail -2
+VR_LIB=build_variants/bounds.so timeout 300 python bench.py --config c3 --steps 3 --warmup 2 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('bounds-checked c3', round(d['value'],1))"
+bash tools/gpu_ab_variants.sh "c3 c3soft"
