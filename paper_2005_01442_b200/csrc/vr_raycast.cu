@@ -340,8 +340,10 @@ VR_D int provably_transparent(const RenderArgs &a, double x, double y, double z,
     if (bounds_transparent(__ldg(a.cells + ((long long)(gz >> 2) * a.ncy + (gy >> 2)) * a.ncx + (gx >> 2)), vlo, vhi))
         return 1;
     if (!a.cubes) return 0;
-    const short2 w = __ldg(a.cubes + (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
-                           ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3));
+    const long long ci = (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
+                         ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3);
+    VR_CHECK_SPAN(a.cubes, a.bv.n, a.cubes + ci, 1);  // (one bound per voxel, brick order)
+    const short2 w = __ldg(a.cubes + ci);
     return bounds_transparent(w, vlo, vhi) ? 2 : 0;
 }
 
@@ -395,8 +397,10 @@ VR_D int chain_transparent(const RenderArgs &a, double x, double y, double z, sh
         return 1;
     }
     if (!a.cubes) return 0;
-    const short2 w = __ldg(a.cubes + (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
-                           ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3));
+    const long long ci = (long long)(gz >> 2) * a.bv.bpz + (long long)(gy >> 2) * a.bv.bpy +
+                         ((long long)(gx >> 2) << 6) + ((gz & 3) << 4) + ((gy & 3) << 2) + (gx & 3);
+    VR_CHECK_SPAN(a.cubes, a.bv.n, a.cubes + ci, 1);  // (one bound per voxel, brick order)
+    const short2 w = __ldg(a.cubes + ci);
     if (!chain_bound_ok<KIND>(a, w)) return 0;
     if (bound) *bound = w;
     return 2;
