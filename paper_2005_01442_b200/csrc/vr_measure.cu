@@ -195,7 +195,21 @@ VR_D int box_hi(double hi_mm, double s, int n) {
 // equal; only those (a few per mille at CT thresholds) read their 8 voxels
 // and run the tetrahedra.
 // 8 inside bits (v >= thr) of the 8 voxels of a 16-byte group
+#ifndef VR_K4_SIMD
+#define VR_K4_SIMD 1  // whole-volume measure 155 -> 147 us, balls 268 -> 260 us
+#endif
 VR_D unsigned group_bits(const int4 q, int thr) {
+#if VR_K4_SIMD
+    // two 16-bit compares per instruction; thr outside int16 is all or none
+    if (thr <= -32768) return 0xffu;
+    if (thr > 32767) return 0u;
+    const unsigned t2 = ((unsigned)thr & 0xffffu) * 0x10001u;
+    const unsigned m0 = __vcmpges2((unsigned)q.x, t2), m1 = __vcmpges2((unsigned)q.y, t2);
+    const unsigned m2 = __vcmpges2((unsigned)q.z, t2), m3 = __vcmpges2((unsigned)q.w, t2);
+    // low halves -> bits 0, 2, 4, 6 and high halves -> bits 16, 18, 20, 22
+    const unsigned b = (m0 & 0x10001u) | ((m1 & 0x10001u) << 2) | ((m2 & 0x10001u) << 4) | ((m3 & 0x10001u) << 6);
+    return (b & 0xffu) | ((b >> 15) & 0xffu);
+#else
     const unsigned w[4] = {(unsigned)q.x, (unsigned)q.y, (unsigned)q.z, (unsigned)q.w};
     unsigned b = 0;
 #pragma unroll
@@ -204,6 +218,7 @@ VR_D unsigned group_bits(const int4 q, int thr) {
         b |= ((int)(short)(w[k] >> 16) >= thr ? 1u : 0u) << (2 * k + 1);
     }
     return b;
+#endif
 }
 
 #ifndef VR_K4_UNROLL
